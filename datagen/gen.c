@@ -1,0 +1,107 @@
+/*
+ * datagen/gen.c -- seeded synthetic rating generator (test data, NOT method).
+ *
+ * This module is the one piece shared by both sides of the parity check
+ * (the oracle in oracle/ and the CUDA path in paper_1610_05838_b200/): it
+ * produces COO triples (u, v, r) from a planted low-rank model.  It holds
+ * none of the SGD method's arithmetic (no update, no dot product of trained
+ * factors, no init, no shuffle).  Recipe: SURVEY.md §8(d) "Synthetic inputs",
+ * restated in DESIGN.md §"Input recipe".
+ *
+ *   H(seed, tag, idx) = splitmix64(seed ^ (tag << 60) ^ idx)
+ *   P*[u][j], Q*[v][j] ~ N(0, var = rank^-1/2)  (Box-Muller on tags 0 / 1)
+ *   sample i: u = H(seed,2,i) mod m, v = H(seed,3,i) mod n  (with replacement)
+ *             r = P*_u . Q*_v + sigma * N(0,1)             (noise: tag 4)
+ *   without replacement (small configs): candidate cell
+ *             c_j = H(seed,5,j) mod (m*n), first-come distinct cells kept.
+ *
+ * Ratings therefore have mean 0 and std ~ 1, uniform (Poisson) degrees.
+ * Generated once on the host and handed to both sides (libm's log/cos are
+ * not bit-identical to CUDA's, so nothing regenerates it on the device).
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+static inline uint64_t gen_mix(uint64_t x) {
+    uint64_t z = x + 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+
+static inline uint64_t gen_H(uint64_t seed, uint64_t tag, uint64_t idx) {
+    return gen_mix(seed ^ (tag << 60) ^ idx);
+}
+
+/* standard normal from two counter draws (Box-Muller, cosine branch) */
+static inline double gen_gauss(uint64_t seed, uint64_t tag, uint64_t idx) {
+    uint64_t h1 = gen_H(seed, tag, 2 * idx), h2 = gen_H(seed, tag, 2 * idx + 1);
+    double u1 = ((double)(h1 >> 11) + 1.0) * 0x1.0p-53; /* (0, 1] */
+    double u2 = (double)(h2 >> 11) * 0x1.0p-53;         /* [0, 1) */
+    return sqrt(-2.0 * log(u1)) * cos(6.283185307179586476925 * u2);
+}
+
+/* planted factor tables, row-major rows x rank, fp64 */
+static void planted(uint64_t seed, uint64_t tag, int64_t rows, int rank, double *out) {
+    double sd = pow((double)rank, -0.25); /* variance rank^-1/2 */
+#pragma omp parallel for schedule(static)
+    for (int64_t i = 0; i < rows; i++)
+        for (int j = 0; j < rank; j++)
+            out[i * rank + j] = sd * gen_gauss(seed, tag, (uint64_t)(i * rank + j));
+}
+
+int mfgen_planted_factors(uint64_t seed, int64_t m, int64_t n, int rank, double *Pstar, double *Qstar) {
+    if (m <= 0 || n <= 0 || rank <= 0 || !Pstar || !Qstar) return -1;
+    planted(seed, 0, m, rank, Pstar);
+    planted(seed, 1, n, rank, Qstar);
+    return 0;
+}
+
+/*
+ * Fill u[0..total), v, r.  with_replacement=0 draws distinct cells (requires
+ * total <= 0.9 m*n so rejection terminates quickly).  Returns 0 or -1.
+ */
+int mfgen_planted_coo(uint64_t seed, int64_t m, int64_t n, int rank, double sigma, int64_t total,
+                      int with_replacement, int32_t *u, int32_t *v, float *r) {
+    if (m <= 0 || n <= 0 || rank <= 0 || total < 0 || !u || !v || !r) return -1;
+    if (m > 2147483647ll || n > 2147483647ll) return -1;
+    double *Ps = (double *)malloc(sizeof(double) * (size_t)m * rank);
+    double *Qs = (double *)malloc(sizeof(double) * (size_t)n * rank);
+    if (!Ps || !Qs) { free(Ps); free(Qs); return -1; }
+    planted(seed, 0, m, rank, Ps);
+    planted(seed, 1, n, rank, Qs);
+    if (with_replacement) {
+#pragma omp parallel for schedule(static)
+        for (int64_t i = 0; i < total; i++) {
+            u[i] = (int32_t)(gen_H(seed, 2, (uint64_t)i) % (uint64_t)m);
+            v[i] = (int32_t)(gen_H(seed, 3, (uint64_t)i) % (uint64_t)n);
+        }
+    } else {
+        uint64_t cells = (uint64_t)m * (uint64_t)n;
+        if ((uint64_t)total > cells - cells / 10) { free(Ps); free(Qs); return -1; }
+        uint8_t *seen = (uint8_t *)calloc((size_t)(cells / 8 + 1), 1);
+        if (!seen) { free(Ps); free(Qs); return -1; }
+        int64_t got = 0;
+        for (uint64_t j = 0; got < total; j++) {
+            uint64_t c = gen_H(seed, 5, j) % cells;
+            if (seen[c >> 3] & (1u << (c & 7))) continue;
+            seen[c >> 3] |= (uint8_t)(1u << (c & 7));
+            u[got] = (int32_t)(c / (uint64_t)n);
+            v[got] = (int32_t)(c % (uint64_t)n);
+            got++;
+        }
+        free(seen);
+    }
+#pragma omp parallel for schedule(static)
+    for (int64_t i = 0; i < total; i++) {
+        const double *p = Ps + (int64_t)u[i] * rank, *q = Qs + (int64_t)v[i] * rank;
+        double s = 0.0;
+        for (int j = 0; j < rank; j++) s += p[j] * q[j];
+        r[i] = (float)(s + sigma * gen_gauss(seed, 4, (uint64_t)i));
+    }
+    free(Ps);
+    free(Qs);
+    return 0;
+}

@@ -1,0 +1,43 @@
+"""The shared input generator (datagen/): determinism, shapes and the planted-model statistics."""
+import numpy as np
+
+import datagen
+
+
+def test_deterministic_and_in_range():
+    a = datagen.planted_coo(5, 300, 200, 8, 0.1, 5000)
+    b = datagen.planted_coo(5, 300, 200, 8, 0.1, 5000)
+    for x, y in zip(a, b):
+        np.testing.assert_array_equal(x, y)
+    u, v, r = a
+    assert u.min() >= 0 and u.max() < 300 and v.min() >= 0 and v.max() < 200
+    assert np.isfinite(r).all()
+
+
+def test_without_replacement_distinct_cells():
+    u, v, _ = datagen.planted_coo(1, 100, 80, 8, 0.01, 4000, with_replacement=False)
+    cells = u.astype(np.int64) * 80 + v
+    assert len(np.unique(cells)) == 4000
+
+
+def test_planted_statistics():
+    """r = P*_u.Q*_v + sigma*g with var(P*), var(Q*) = rank^-1/2: std(r) ~ 1, residual std = sigma."""
+    m, n, rank, sigma = 2000, 1500, 8, 0.1
+    u, v, r = datagen.planted_coo(3, m, n, rank, sigma, 200_000)
+    P, Q = datagen.planted_factors(3, m, n, rank)
+    assert abs(P.var() - rank ** -0.5) < 0.02 and abs(Q.var() - rank ** -0.5) < 0.02
+    resid = r.astype(np.float64) - np.einsum("ij,ij->i", P[u], Q[v])
+    assert abs(resid.std() - sigma) < 0.005 and abs(resid.mean()) < 0.002
+    assert abs(r.std() - 1.0) < 0.1
+    # uniform degrees (with replacement): Poisson around N/m
+    deg = np.bincount(u, minlength=m)
+    assert abs(deg.mean() - 100) < 1e-9 and deg.std() < 15
+
+
+def test_configs_table2_shapes():
+    """PAPER.md:373-377 Table 2."""
+    c = datagen.CONFIGS
+    assert (c["C2"].m, c["C2"].n, c["C2"].n_train, c["C2"].n_test) == (480190, 17771, 99072112, 1408395)
+    assert (c["C3"].m, c["C3"].n, c["C3"].n_train, c["C3"].n_test) == (1000990, 624961, 252800275, 4003960)
+    assert (c["C4"].m, c["C4"].n, c["C4"].n_train, c["C4"].n_test) == (50082604, 39781, 3069817980, 31327899)
+    assert all(c[x].k == 128 for x in ("C2", "C3", "C4"))
