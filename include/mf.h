@@ -1,0 +1,153 @@
+/*
+ * include/mf.h -- C ABI of the B200 SGD matrix-factorization hot path.
+ *
+ * The library (paper_1610_05838_b200/libmf.so, CUDA for sm_100a) trains
+ * R ~ P x Q by stochastic gradient descent (§2.2):
+ *
+ *     err_uv = r_uv - p_u . q_v
+ *     p_u   <- p_u + eta_t (err_uv q_v - lambda p_u)
+ *     q_v   <- q_v + eta_t (err_uv p_u - lambda q_v)      (both from the
+ *                                                       pre-update snapshot)
+ *     eta_t  = alpha / (1 + beta t^1.5),  t = 0,1,...    (§5.1)
+ *
+ * under the paper's schedules: batch-Hogwild! (§3.2.2),
+ * wavefront-update (§3.2.3), a deterministic
+ * conflict-free wave mode that reproduces serial SGD (D-3), and the
+ * multi-GPU block partition with Q-segment rotation (§4.1).
+ *
+ * Conventions
+ *  - Every function returns MF_OK (0) or a negative mf_status; no C++
+ *    exception crosses the ABI.  mf_last_error() returns a message for the
+ *    last failing call on that context.
+ *  - Ratings are COO triples (u, v, r): int32 row index 0 <= u < m, int32
+ *    column index 0 <= v < n, fp32 rating (12 bytes/sample).
+ *  - P is m x k and Q is n x k, both ROW-MAJOR with one contiguous k-vector
+ *    per user / item (the paper's Q is k x n; stored
+ *    transposed for coalescing; reading A-4).
+ *  - Input pointers may be host (pageable or pinned) or device pointers; the
+ *    library detects which and COPIES the data.  The caller keeps ownership.
+ *    Output buffers are caller-allocated HOST memory unless stated otherwise.
+ *  - The context owns every device allocation it makes; mf_destroy frees it.
+ *  - One context per device per thread; calls on one context are not
+ *    reentrant.  All calls are synchronous with respect to the host unless
+ *    stated otherwise; work is issued on the context stream (MF_OPT_STREAM).
+ *  - There is no CPU fallback: without a usable CUDA device every call that
+ *    needs one fails with MF_ECUDA.
+ */
+#ifndef MF_H
+#define MF_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct mf_ctx mf_ctx;
+
+typedef enum {
+    MF_OK = 0,
+    MF_EINVAL = -1,     /* bad argument: sizes <= 0, lr <= 0, lambda < 0, null pointer, index out of range, non-finite rating */
+    MF_ENOMEM = -2,     /* device or host allocation failed */
+    MF_ECUDA = -3,      /* CUDA runtime error or no device (message in mf_last_error) */
+    MF_ESTATE = -4,     /* call out of order, e.g. mf_epoch before mf_load_coo */
+    MF_EDIVERGED = -5,  /* a non-finite prediction error occurred during the epoch */
+    MF_ENCCL = -6       /* NCCL failure in the partitioned path */
+} mf_status;
+
+typedef enum {
+    MF_SCHED_HOGWILD = 0,        /* batch-Hogwild!: workers claim f consecutive shuffled samples, lock-free */
+    MF_SCHED_WAVEFRONT = 1,      /* wavefront-update: s row bands x c column blocks, column lock array */
+    MF_SCHED_DETERMINISTIC = 2,  /* conflict-free waves: bit-reproducible, equals serial SGD on the shuffled order (D-3) */
+    MF_SCHED_PARTITIONED = 3     /* P row segments x rotating Q segments over G ranks or G logical partitions */
+} mf_schedule;
+
+typedef enum {
+    MF_OPT_STORAGE = 0,       /* feature storage: 0 fp32, 1 fp16, 2 bf16; math is fp32. Before the first load. */
+    MF_OPT_BETA = 1,          /* beta of the LR schedule (default 0) */
+    MF_OPT_WORKERS = 2,       /* batch-Hogwild! concurrent workers (groups); 0 = auto (A-10) */
+    MF_OPT_BATCH_F = 3,       /* samples per batch-Hogwild! chunk, multiple of 32 (default 256) */
+    MF_OPT_WAVE_ROWS = 4,     /* wavefront workers s = row bands (0 = auto) */
+    MF_OPT_WAVE_COLS = 5,     /* wavefront column blocks c >= s (0 = auto) */
+    MF_OPT_DEVICE = 6,        /* CUDA device ordinal (before the first load) */
+    MF_OPT_STREAM = 7,        /* cudaStream_t as an integer; 0 = the context's own stream */
+    MF_OPT_SHUFFLE = 8,       /* 1 = permute samples once at load by the A-8 hash sort (default); 0 = keep the given order */
+    MF_OPT_COUNT_UPDATES = 9, /* 1 = count updates per epoch on the device (exactly-once check) */
+    MF_OPT_WAVE_PERM = 10,    /* wavefront column sequences: 0 randomized Latin rectangle (default), 1 independent random permutations */
+    MF_OPT_EPOCH = 11,        /* set the epoch index t used by the LR schedule */
+    MF_OPT_PARTITIONS = 12,   /* MF_SCHED_PARTITIONED without NCCL: G logical partitions run on this GPU (loopback) */
+    MF_OPT_SEED_SHUFFLE = 13, /* seed of the A-8 shuffle (default: the mf_create seed) */
+    MF_OPT_VARIANT = 14,      /* kernel variant selector for tuning (0 = default) */
+    MF_OPT_TRACE = 15         /* wavefront audit trace: 1 = record (worker, block, t_start, t_end) per block */
+} mf_option;
+
+typedef struct {
+    int64_t updates;         /* samples processed (exact if MF_OPT_COUNT_UPDATES, else N) */
+    double seconds;          /* device time of the whole epoch (CUDA events on the context stream) */
+    double kernel_seconds;   /* device time of the update kernel(s) alone */
+    float lr;                /* eta_t used */
+    int32_t epoch;           /* t used */
+    int32_t workers;         /* concurrent workers used */
+    int32_t launches;        /* kernels launched by this call */
+} mf_epoch_stats;
+
+/* Create a context for an m x n rating matrix with rank k, initial LR alpha (= lr), regulariser
+ * lambda (lambda_p = lambda_q, A-2) and seed (factor init A-7, and shuffle A-8 unless
+ * MF_OPT_SEED_SHUFFLE).  Requires 0 < m, n < 2^31, 0 < k <= 1024, lr > 0, lambda >= 0. */
+int mf_create(int64_t m, int64_t n, int32_t k, float lr, float lambda, uint64_t seed, mf_ctx **out);
+
+/* Set / get an mf_option.  Layout-affecting keys (STORAGE, DEVICE) fail with MF_ESTATE after the factors exist. */
+int mf_set_option(mf_ctx *ctx, int key, double value);
+int mf_get_option(const mf_ctx *ctx, int key, double *value);
+
+/* Load the training set (replacing any previous one): validate 0 <= u < m, 0 <= v < n and finite r on the
+ * device (MF_EINVAL on failure, nothing loaded), then permute (MF_OPT_SHUFFLE) and store as device SoA.
+ * Allocates and initialises P, Q (A-7) on first use.  nnz >= 1. */
+int mf_load_coo(mf_ctx *ctx, const int32_t *u, const int32_t *v, const float *r, int64_t nnz);
+
+/* Run one epoch (N updates) under `schedule` at eta_t, then t += 1.  stats may be NULL.
+ * Returns MF_EDIVERGED if any err was non-finite (factors are left as they are). */
+int mf_epoch(mf_ctx *ctx, int schedule, mf_epoch_stats *stats);
+
+/* Test RMSE sqrt(sum (r - p_u.q_v)^2 / nnz) over the given triples: fp32 dot, fp64 sum,
+ * deterministic reduction order.  nnz >= 1.  In the partitioned NCCL mode the call is collective and
+ * every rank passes its local test triples (u in its row segment); all ranks get the global value. */
+int mf_rmse(mf_ctx *ctx, const int32_t *u, const int32_t *v, const float *r, int64_t nnz, double *out);
+
+/* Copy factors to caller host buffers, widened to fp32, row-major (P: m x k, Q: n x k); either may be NULL.
+ * In the partitioned NCCL mode P is the local row segment and Q is the full matrix (collective). */
+int mf_get_factors(mf_ctx *ctx, float *P, float *Q);
+
+/* Overwrite factors from fp32 host/device buffers (rounded to storage, RNE); either may be NULL. */
+int mf_set_factors(mf_ctx *ctx, const float *P, const float *Q);
+
+/* The processing order: perm[i] = index (into the arrays given to mf_load_coo) of the i-th stored
+ * sample.  perm is a caller-allocated host array of nnz int64. */
+int mf_get_order(const mf_ctx *ctx, int64_t *perm);
+
+/* Number of waves of the deterministic layout (builds it if needed). */
+int mf_wave_count(mf_ctx *ctx, int64_t *out);
+
+/* Multi-GPU (MF_SCHED_PARTITIONED over NCCL).  Rank 0 calls mf_nccl_unique_id (128 bytes), the caller
+ * broadcasts the bytes (e.g. torch.distributed), then every rank calls mf_attach_nccl before loading. */
+int mf_nccl_unique_id(void *out128);
+int mf_attach_nccl(mf_ctx *ctx, const void *id128, int rank, int world);
+
+/* Host-only helpers of the partitioned schedule (no device needed):
+ * row segment of rank g among G: [seg_begin, seg_end) = [floor(g*m/G), floor((g+1)*m/G));
+ * column segment held by rank g in round r of epoch e (a Latin square). */
+int mf_segment(int64_t extent, int32_t parts, int32_t index, int64_t *begin, int64_t *end);
+int mf_round_segment(uint64_t seed, int32_t epoch, int32_t G, int32_t round, int32_t rank, int32_t *col_segment);
+
+/* Wavefront audit (MF_OPT_TRACE=1): copies up to cap records of 4 int64 (worker, block, t_start, t_end
+ * in globaltimer ns) from the last wavefront epoch; *count = records written. */
+int mf_wavefront_trace(mf_ctx *ctx, int64_t *records, int64_t cap, int64_t *count);
+
+void mf_destroy(mf_ctx *ctx);
+const char *mf_last_error(const mf_ctx *ctx);
+const char *mf_status_string(int status);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MF_H */

@@ -1,0 +1,641 @@
+// mf_api.cu -- host side of the C ABI declared in include/mf.h.
+//
+// Owns the context (device buffers, stream, options), the data layout steps
+// that run once per load (validation, A-8 shuffle, deterministic wave layout)
+// and the per-epoch dispatch to the kernels in mf_kernels.cu / mf_wavefront.cu
+// / mf_partition.cu.  All numerical work happens on the device.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/mf.h"
+#include "mf_ctx.h"
+#include "mf_kernels.cuh"
+
+using namespace mf;
+
+// ------------------------------------------------------------------ errors --
+int mf_ctx::fail(int code, const char *fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    err = buf;
+    return code;
+}
+
+int mf_ctx::cuda(cudaError_t e, const char *what) {
+    if (e == cudaSuccess) return MF_OK;
+    cudaGetLastError();  // clear sticky-free errors
+    if (e == cudaErrorMemoryAllocation) return fail(MF_ENOMEM, "%s: %s", what, cudaGetErrorString(e));
+    return fail(MF_ECUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+
+#define CK(expr)                                                  \
+    do {                                                          \
+        int _rc = ctx->cuda((expr), #expr);                       \
+        if (_rc != MF_OK) return _rc;                             \
+    } while (0)
+#define RC(expr)                 \
+    do {                         \
+        int _rc = (expr);        \
+        if (_rc != MF_OK) return _rc; \
+    } while (0)
+
+template <class T>
+static int dev_alloc(mf_ctx *ctx, T **p, size_t count, const char *what) {
+    if (*p) return MF_OK;
+    if (count == 0) count = 1;
+    cudaError_t e = cudaMalloc((void **)p, sizeof(T) * count);
+    if (e != cudaSuccess) {
+        *p = nullptr;
+        return ctx->cuda(e, what);
+    }
+    return MF_OK;
+}
+template <class T>
+static void dev_free(T **p) {
+    if (*p) cudaFree((void *)*p);
+    *p = nullptr;
+}
+
+static bool is_device_ptr(const void *p) {
+    cudaPointerAttributes at;
+    if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
+}
+
+int mf_ctx::storage_bytes() const { return storage == kF32 ? 4 : 2; }
+
+// ------------------------------------------------------------ device setup --
+int mf_ctx::ensure_device() {
+    if (dev_ready) return MF_OK;
+    int ndev = 0;
+    cudaError_t e = cudaGetDeviceCount(&ndev);
+    if (e != cudaSuccess || ndev == 0) {
+        cudaGetLastError();
+        return fail(MF_ECUDA, "no CUDA device available (%s); there is no CPU fallback",
+                    e == cudaSuccess ? "0 devices" : cudaGetErrorString(e));
+    }
+    if (device < 0 || device >= ndev) return fail(MF_EINVAL, "device %d out of range (%d devices)", device, ndev);
+    mf_ctx *ctx = this;
+    CK(cudaSetDevice(device));
+    if (!user_stream) {
+        CK(cudaStreamCreateWithFlags(&own_stream, cudaStreamNonBlocking));
+    }
+    CK(cudaMalloc((void **)&scratch, sizeof(DevScratch)));
+    CK(cudaMemset(scratch, 0, sizeof(DevScratch)));
+    CK(cudaMallocHost((void **)&h_scratch, sizeof(DevScratch)));
+    for (auto &ev : events) CK(cudaEventCreate(&ev));
+    CK(cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, device));
+    dev_ready = true;
+    return MF_OK;
+}
+
+cudaStream_t mf_ctx::stream() const { return user_stream ? user_stream : own_stream; }
+
+int mf_ctx::ensure_factors() {
+    if (P && Q) return MF_OK;
+    RC(ensure_device());
+    mf_ctx *ctx = this;
+    CK(cudaSetDevice(device));
+    const size_t b = (size_t)storage_bytes();
+    const int64_t prow = p_rows();
+    RC(dev_alloc(this, (char **)&P, b * (size_t)prow * k, "alloc P"));
+    RC(dev_alloc(this, (char **)&Q, b * (size_t)n * k, "alloc Q"));
+    // A-7 init; in the partitioned NCCL mode P holds rows [p_begin, p_end) of the global P:
+    // the hash index is the global row*k+col, so shift the row origin.
+    CK(launch_init_rows(storage, P, p_begin, prow, k, seed, 0, stream()));
+    CK(launch_init_rows(storage, Q, 0, n, k, seed, 1, stream()));
+    CK(cudaStreamSynchronize(stream()));
+    return MF_OK;
+}
+
+// init for rows [row0, row0+rows) stored from X[0]
+cudaError_t mf::launch_init_rows(int storage, void *X, int64_t row0, int64_t rows, int k, uint64_t seed, uint32_t tag,
+                                 cudaStream_t st) {
+    return launch_init_offset(storage, X, row0 * (int64_t)k, rows * (int64_t)k, k, seed, tag, st);
+}
+
+void mf_ctx::drop_layouts() {
+    dev_free(&wu);
+    dev_free(&wv);
+    dev_free(&wr);
+    dev_free(&wave_off);
+    nwaves = -1;
+    wf_valid = false;
+    part_valid = false;
+}
+
+void mf_ctx::release() {
+    if (dev_ready) cudaSetDevice(device);
+    drop_layouts();
+    dev_free(&u);
+    dev_free(&v);
+    dev_free(&r);
+    dev_free(&perm);
+    dev_free(&tu);
+    dev_free(&tv);
+    dev_free(&tr);
+    dev_free(&partials);
+    dev_free(&d_out);
+    dev_free(&f32_tmp);
+    if (P) cudaFree(P);
+    if (Q) cudaFree(Q);
+    P = Q = nullptr;
+    release_wavefront();
+    release_partition();
+    if (scratch) cudaFree(scratch);
+    scratch = nullptr;
+    if (h_scratch) cudaFreeHost(h_scratch);
+    h_scratch = nullptr;
+    for (auto &ev : events)
+        if (ev) cudaEventDestroy(ev), ev = nullptr;
+    if (own_stream) cudaStreamDestroy(own_stream);
+    own_stream = nullptr;
+    dev_ready = false;
+}
+
+// ------------------------------------------------------------ public: create
+extern "C" int mf_create(int64_t m, int64_t n, int32_t k, float lr, float lambda, uint64_t seed, mf_ctx **out) {
+    if (!out) return MF_EINVAL;
+    *out = nullptr;
+    if (m <= 0 || n <= 0 || m >= (1ll << 31) || n >= (1ll << 31) || k <= 0 || k > 1024) return MF_EINVAL;
+    if (!(lr > 0.f) || !std::isfinite(lr) || !(lambda >= 0.f) || !std::isfinite(lambda)) return MF_EINVAL;
+    mf_ctx *c = new (std::nothrow) mf_ctx();
+    if (!c) return MF_ENOMEM;
+    c->m = m;
+    c->n = n;
+    c->k = k;
+    c->alpha = lr;
+    c->lambda = lambda;
+    c->seed = seed;
+    c->seed_shuffle = seed;
+    c->p_begin = 0;
+    c->p_end = m;
+    *out = c;
+    return MF_OK;
+}
+
+extern "C" void mf_destroy(mf_ctx *ctx) {
+    if (!ctx) return;
+    ctx->release();
+    delete ctx;
+}
+
+extern "C" const char *mf_last_error(const mf_ctx *ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+extern "C" const char *mf_status_string(int s) {
+    switch (s) {
+        case MF_OK: return "MF_OK";
+        case MF_EINVAL: return "MF_EINVAL";
+        case MF_ENOMEM: return "MF_ENOMEM";
+        case MF_ECUDA: return "MF_ECUDA";
+        case MF_ESTATE: return "MF_ESTATE";
+        case MF_EDIVERGED: return "MF_EDIVERGED";
+        case MF_ENCCL: return "MF_ENCCL";
+        default: return "MF_UNKNOWN";
+    }
+}
+
+extern "C" int mf_set_option(mf_ctx *ctx, int key, double value) {
+    if (!ctx) return MF_EINVAL;
+    if (!std::isfinite(value)) return ctx->fail(MF_EINVAL, "option %d: non-finite value", key);
+    const int64_t iv = (int64_t)value;
+    switch (key) {
+        case MF_OPT_STORAGE:
+            if (iv < 0 || iv > 2) return ctx->fail(MF_EINVAL, "storage must be 0 (fp32), 1 (fp16) or 2 (bf16)");
+            if (ctx->P && iv != ctx->storage) return ctx->fail(MF_ESTATE, "storage must be set before the factors exist");
+            ctx->storage = (int)iv;
+            return MF_OK;
+        case MF_OPT_BETA:
+            if (value < 0) return ctx->fail(MF_EINVAL, "beta must be >= 0");
+            ctx->beta = value;
+            return MF_OK;
+        case MF_OPT_WORKERS:
+            if (iv < 0) return ctx->fail(MF_EINVAL, "workers must be >= 0");
+            ctx->workers = (int)std::min<int64_t>(iv, 1 << 30);
+            return MF_OK;
+        case MF_OPT_BATCH_F:
+            if (iv < 32 || iv % 32 || iv > (1 << 24)) return ctx->fail(MF_EINVAL, "batch f must be a positive multiple of 32");
+            ctx->batch_f = (int)iv;
+            return MF_OK;
+        case MF_OPT_WAVE_ROWS:
+            if (iv < 0) return ctx->fail(MF_EINVAL, "wave rows must be >= 0");
+            ctx->wave_rows = (int)iv;
+            ctx->wf_valid = false;
+            return MF_OK;
+        case MF_OPT_WAVE_COLS:
+            if (iv < 0) return ctx->fail(MF_EINVAL, "wave cols must be >= 0");
+            ctx->wave_cols = (int)iv;
+            ctx->wf_valid = false;
+            return MF_OK;
+        case MF_OPT_DEVICE:
+            if (ctx->dev_ready && iv != ctx->device) return ctx->fail(MF_ESTATE, "device must be set before first use");
+            ctx->device = (int)iv;
+            return MF_OK;
+        case MF_OPT_STREAM:
+            ctx->user_stream = (cudaStream_t)(uintptr_t)iv;
+            return MF_OK;
+        case MF_OPT_SHUFFLE:
+            if (iv < 0 || iv > 1) return ctx->fail(MF_EINVAL, "shuffle must be 0 or 1");
+            ctx->shuffle = (int)iv;
+            return MF_OK;
+        case MF_OPT_COUNT_UPDATES:
+            ctx->count_updates = iv ? 1 : 0;
+            return MF_OK;
+        case MF_OPT_WAVE_PERM:
+            if (iv < 0 || iv > 1) return ctx->fail(MF_EINVAL, "wave perm must be 0 (latin) or 1 (random)");
+            ctx->wave_perm = (int)iv;
+            return MF_OK;
+        case MF_OPT_EPOCH:
+            if (iv < 0) return ctx->fail(MF_EINVAL, "epoch must be >= 0");
+            ctx->epoch = (int32_t)iv;
+            return MF_OK;
+        case MF_OPT_PARTITIONS:
+            if (iv < 0 || iv > 1024) return ctx->fail(MF_EINVAL, "partitions must be in [0, 1024]");
+            ctx->partitions = (int)iv;
+            ctx->part_valid = false;
+            return MF_OK;
+        case MF_OPT_SEED_SHUFFLE:
+            ctx->seed_shuffle = (uint64_t)value;
+            return MF_OK;
+        case MF_OPT_VARIANT:
+            ctx->variant = (int)iv;
+            return MF_OK;
+        case MF_OPT_TRACE:
+            ctx->trace = iv ? 1 : 0;
+            return MF_OK;
+        default:
+            return ctx->fail(MF_EINVAL, "unknown option %d", key);
+    }
+}
+
+extern "C" int mf_get_option(const mf_ctx *ctx, int key, double *value) {
+    if (!ctx || !value) return MF_EINVAL;
+    switch (key) {
+        case MF_OPT_STORAGE: *value = ctx->storage; return MF_OK;
+        case MF_OPT_BETA: *value = ctx->beta; return MF_OK;
+        case MF_OPT_WORKERS: *value = ctx->workers; return MF_OK;
+        case MF_OPT_BATCH_F: *value = ctx->batch_f; return MF_OK;
+        case MF_OPT_WAVE_ROWS: *value = ctx->wave_rows; return MF_OK;
+        case MF_OPT_WAVE_COLS: *value = ctx->wave_cols; return MF_OK;
+        case MF_OPT_DEVICE: *value = ctx->device; return MF_OK;
+        case MF_OPT_STREAM: *value = (double)(uintptr_t)ctx->user_stream; return MF_OK;
+        case MF_OPT_SHUFFLE: *value = ctx->shuffle; return MF_OK;
+        case MF_OPT_COUNT_UPDATES: *value = ctx->count_updates; return MF_OK;
+        case MF_OPT_WAVE_PERM: *value = ctx->wave_perm; return MF_OK;
+        case MF_OPT_EPOCH: *value = ctx->epoch; return MF_OK;
+        case MF_OPT_PARTITIONS: *value = ctx->partitions; return MF_OK;
+        case MF_OPT_SEED_SHUFFLE: *value = (double)ctx->seed_shuffle; return MF_OK;
+        case MF_OPT_VARIANT: *value = ctx->variant; return MF_OK;
+        case MF_OPT_TRACE: *value = ctx->trace; return MF_OK;
+        default: return MF_EINVAL;
+    }
+}
+
+// ---------------------------------------------------------------- load_coo --
+// Copy in (host or device source), validate on the device, permute (A-8),
+// store SoA.  Buffers are reused when nnz does not change (repeated loads in
+// the end-to-end benchmark allocate nothing).
+extern "C" int mf_load_coo(mf_ctx *ctx, const int32_t *u, const int32_t *v, const float *r, int64_t nnz) {
+    if (!ctx) return MF_EINVAL;
+    if (!u || !v || !r || nnz <= 0) return ctx->fail(MF_EINVAL, "mf_load_coo: null pointer or nnz <= 0");
+    if (ctx->shuffle && nnz > (int64_t)0xFFFFFFFFll)
+        return ctx->fail(MF_EINVAL, "mf_load_coo: shuffle supports nnz < 2^32");
+    RC(ctx->ensure_device());
+    CK(cudaSetDevice(ctx->device));
+    cudaStream_t st = ctx->stream();
+    if (nnz != ctx->cap_n) {
+        dev_free(&ctx->u);
+        dev_free(&ctx->v);
+        dev_free(&ctx->r);
+        dev_free(&ctx->perm);
+        ctx->cap_n = 0;
+        RC(dev_alloc(ctx, &ctx->u, nnz, "alloc u"));
+        RC(dev_alloc(ctx, &ctx->v, nnz, "alloc v"));
+        RC(dev_alloc(ctx, &ctx->r, nnz, "alloc r"));
+        if (ctx->shuffle) RC(dev_alloc(ctx, &ctx->perm, nnz, "alloc perm"));
+        ctx->cap_n = nnz;
+    }
+    if (ctx->shuffle && !ctx->perm) RC(dev_alloc(ctx, &ctx->perm, nnz, "alloc perm"));
+    ctx->drop_layouts();
+    ctx->N = 0;
+    const bool dev_src = is_device_ptr(u);
+    const cudaMemcpyKind kind = dev_src ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+    int32_t *su = ctx->u, *sv = ctx->v;
+    float *sr = ctx->r;
+    int32_t *tmp_u = nullptr, *tmp_v = nullptr;
+    float *tmp_r = nullptr;
+    if (ctx->shuffle) {  // stage unshuffled copy, then gather into the final buffers
+        CK(cudaMallocAsync((void **)&tmp_u, sizeof(int32_t) * nnz, st));
+        CK(cudaMallocAsync((void **)&tmp_v, sizeof(int32_t) * nnz, st));
+        CK(cudaMallocAsync((void **)&tmp_r, sizeof(float) * nnz, st));
+        su = tmp_u;
+        sv = tmp_v;
+        sr = tmp_r;
+    }
+    int rc = MF_OK;
+    auto cleanup = [&]() {
+        if (tmp_u) cudaFreeAsync(tmp_u, st);
+        if (tmp_v) cudaFreeAsync(tmp_v, st);
+        if (tmp_r) cudaFreeAsync(tmp_r, st);
+    };
+#define CKL(expr)                                   \
+    do {                                            \
+        rc = ctx->cuda((expr), #expr);              \
+        if (rc != MF_OK) { cleanup(); return rc; }  \
+    } while (0)
+    CKL(cudaMemcpyAsync(su, u, sizeof(int32_t) * nnz, kind, st));
+    CKL(cudaMemcpyAsync(sv, v, sizeof(int32_t) * nnz, kind, st));
+    CKL(cudaMemcpyAsync(sr, r, sizeof(float) * nnz, kind, st));
+    CKL(cudaMemsetAsync(ctx->scratch, 0, sizeof(DevScratch), st));
+    int64_t row_lo = ctx->p_begin, row_hi = ctx->p_end;
+    CKL(launch_validate_rows(su, sv, sr, nnz, row_lo, row_hi, ctx->n, ctx->scratch, st));
+    CKL(cudaMemcpyAsync(ctx->h_scratch, ctx->scratch, sizeof(DevScratch), cudaMemcpyDeviceToHost, st));
+    CKL(cudaStreamSynchronize(st));
+    if (ctx->h_scratch->bad) {
+        cleanup();
+        return ctx->fail(MF_EINVAL, "mf_load_coo: %llu samples with u outside [%lld,%lld), v outside [0,%lld) or non-finite r",
+                         (unsigned long long)ctx->h_scratch->bad, (long long)row_lo, (long long)row_hi, (long long)ctx->n);
+    }
+    if (row_lo != 0) CKL(launch_rebase(su, nnz, (int32_t)row_lo, st));  // P holds rows [row_lo, row_hi) only
+    if (ctx->shuffle) {
+        CKL(launch_shuffle(su, sv, sr, nnz, ctx->seed_shuffle, ctx->u, ctx->v, ctx->r, ctx->perm, st));
+        CKL(cudaStreamSynchronize(st));
+    }
+    cleanup();
+#undef CKL
+    ctx->N = nnz;
+    ctx->shuffled = ctx->shuffle;
+    RC(ctx->ensure_factors());
+    return MF_OK;
+}
+
+// -------------------------------------------------------------- wave layout --
+// DESIGN.md D-3: scanning samples in stored (shuffled) order,
+// wave(i) = max(last[u_i], last[v_i]) + 1, last[] = -1 initially.  Samples are
+// then stably bucketed by wave; inside a wave no two share a row or column.
+int mf_ctx::build_waves() {
+    if (nwaves >= 0) return MF_OK;
+    mf_ctx *ctx = this;
+    cudaStream_t st = stream();
+    std::vector<int32_t> hu((size_t)N), hv((size_t)N);
+    CK(cudaMemcpyAsync(hu.data(), u, sizeof(int32_t) * N, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(hv.data(), v, sizeof(int32_t) * N, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    std::vector<int32_t> wave((size_t)N);
+    int64_t nw = 0;
+    {
+        std::vector<int32_t> lu((size_t)p_rows(), -1), lv((size_t)n, -1);
+        for (int64_t i = 0; i < N; i++) {
+            const int32_t a = hu[(size_t)i], b = hv[(size_t)i];
+            const int32_t w = std::max(lu[(size_t)a], lv[(size_t)b]) + 1;
+            wave[(size_t)i] = w;
+            lu[(size_t)a] = w;
+            lv[(size_t)b] = w;
+            if (w + 1 > nw) nw = w + 1;
+        }
+    }
+    std::vector<int64_t> off((size_t)nw + 1, 0);
+    for (int64_t i = 0; i < N; i++) off[(size_t)wave[(size_t)i] + 1]++;
+    for (int64_t w = 0; w < nw; w++) off[(size_t)w + 1] += off[(size_t)w];
+    std::vector<uint32_t> idx((size_t)N);
+    {
+        std::vector<int64_t> pos(off.begin(), off.end() - 1);
+        for (int64_t i = 0; i < N; i++) idx[(size_t)pos[(size_t)wave[(size_t)i]]++] = (uint32_t)i;
+    }
+    uint32_t *didx = nullptr;
+    RC(dev_alloc(this, &wu, N, "alloc wave u"));
+    RC(dev_alloc(this, &wv, N, "alloc wave v"));
+    RC(dev_alloc(this, &wr, N, "alloc wave r"));
+    RC(dev_alloc(this, &wave_off, nw + 1, "alloc wave offsets"));
+    CK(cudaMallocAsync((void **)&didx, sizeof(uint32_t) * N, st));
+    CK(cudaMemcpyAsync(didx, idx.data(), sizeof(uint32_t) * N, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(wave_off, off.data(), sizeof(int64_t) * (nw + 1), cudaMemcpyHostToDevice, st));
+    CK(launch_gather(u, v, r, didx, N, wu, wv, wr, st));
+    CK(cudaFreeAsync(didx, st));
+    CK(cudaStreamSynchronize(st));
+    nwaves = nw;
+    return MF_OK;
+}
+
+extern "C" int mf_wave_count(mf_ctx *ctx, int64_t *out) {
+    if (!ctx || !out) return MF_EINVAL;
+    if (ctx->N <= 0) return ctx->fail(MF_ESTATE, "mf_wave_count before mf_load_coo");
+    RC(ctx->build_waves());
+    *out = ctx->nwaves;
+    return MF_OK;
+}
+
+// ------------------------------------------------------------------- epoch --
+float mf_ctx::eta_at(int32_t t) const {
+    // s_t = alpha / (1 + beta t^1.5) in double, then fp32 (A-5)
+    return (float)((double)alpha / (1.0 + beta * std::pow((double)t, 1.5)));
+}
+
+int mf_ctx::auto_workers() const {
+    // DESIGN.md A-10: every worker processes >= 10^4 samples per epoch
+    return (int)std::max<int64_t>(1, std::min<int64_t>(N / 10000, 1 << 30));
+}
+
+UpdateArgs mf_ctx::update_args(float eta) const {
+    UpdateArgs a{};
+    a.u = u;
+    a.v = v;
+    a.r = r;
+    a.n = N;
+    a.P = P;
+    a.Q = Q;
+    a.k = k;
+    a.eta = eta;
+    a.lam = lambda;
+    a.batch_f = batch_f;
+    a.count_updates = count_updates;
+    a.scratch = scratch;
+    return a;
+}
+
+int mf_ctx::finish_epoch(int schedule, float eta, int launches, int workers_used, mf_epoch_stats *stats) {
+    mf_ctx *ctx = this;
+    cudaStream_t st = stream();
+    CK(cudaEventRecord(events[3], st));
+    CK(cudaMemcpyAsync(h_scratch, scratch, sizeof(DevScratch), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    float ms_all = 0.f, ms_k = 0.f;
+    CK(cudaEventElapsedTime(&ms_all, events[0], events[3]));
+    CK(cudaEventElapsedTime(&ms_k, events[1], events[2]));
+    const int32_t t = epoch;
+    epoch++;
+    if (stats) {
+        stats->updates = count_updates ? (int64_t)h_scratch->updates : N;
+        stats->seconds = ms_all * 1e-3;
+        stats->kernel_seconds = ms_k * 1e-3;
+        stats->lr = eta;
+        stats->epoch = t;
+        stats->workers = workers_used;
+        stats->launches = launches;
+    }
+    (void)schedule;
+    if (h_scratch->diverged) return fail(MF_EDIVERGED, "non-finite prediction error in epoch %d", (int)t);
+    return MF_OK;
+}
+
+extern "C" int mf_epoch(mf_ctx *ctx, int schedule, mf_epoch_stats *stats) {
+    if (!ctx) return MF_EINVAL;
+    if (schedule < MF_SCHED_HOGWILD || schedule > MF_SCHED_PARTITIONED)
+        return ctx->fail(MF_EINVAL, "unknown schedule %d", schedule);
+    if (ctx->N <= 0 || !ctx->P) return ctx->fail(MF_ESTATE, "mf_epoch before mf_load_coo");
+    CK(cudaSetDevice(ctx->device));
+    if (schedule == MF_SCHED_DETERMINISTIC) RC(ctx->build_waves());
+    if (schedule == MF_SCHED_WAVEFRONT) RC(ctx->build_wavefront());
+    if (schedule == MF_SCHED_PARTITIONED) return ctx->epoch_partitioned(stats);
+    cudaStream_t st = ctx->stream();
+    const float eta = ctx->eta_at(ctx->epoch);
+    const ShapeId sh = select_shape(ctx->k, ctx->storage, ctx->variant & 0xF);
+    CK(cudaEventRecord(ctx->events[0], st));
+    CK(cudaMemsetAsync(ctx->scratch, 0, sizeof(DevScratch), st));
+    UpdateArgs a = ctx->update_args(eta);
+    int launches = 2, used = 0;
+    CK(cudaEventRecord(ctx->events[1], st));
+    if (schedule == MF_SCHED_HOGWILD) {
+        const int w = ctx->workers > 0 ? ctx->workers : ctx->auto_workers();
+        CK(launch_hogwild(sh, a, w, ctx->variant, st, &used));
+    } else if (schedule == MF_SCHED_DETERMINISTIC) {
+        a.u = ctx->wu;
+        a.v = ctx->wv;
+        a.r = ctx->wr;
+        a.wave_off = ctx->wave_off;
+        a.nwaves = ctx->nwaves;
+        int l = 0;
+        CK(launch_waves(sh, a, st, &l));
+        used = 0;
+    } else {  // wavefront
+        int l = 0;
+        RC(ctx->run_wavefront(sh, a, &l, &used));
+        launches += l - 1;
+    }
+    CK(cudaEventRecord(ctx->events[2], st));
+    return ctx->finish_epoch(schedule, eta, launches, used, stats);
+}
+
+// -------------------------------------------------------------------- rmse --
+extern "C" int mf_rmse(mf_ctx *ctx, const int32_t *u, const int32_t *v, const float *r, int64_t nnz, double *out) {
+    if (!ctx || !out) return MF_EINVAL;
+    if (!u || !v || !r || nnz <= 0) return ctx->fail(MF_EINVAL, "mf_rmse: null pointer or nnz <= 0");
+    RC(ctx->ensure_factors());
+    CK(cudaSetDevice(ctx->device));
+    cudaStream_t st = ctx->stream();
+    if (nnz > ctx->cap_t) {
+        dev_free(&ctx->tu);
+        dev_free(&ctx->tv);
+        dev_free(&ctx->tr);
+        ctx->cap_t = 0;
+        RC(dev_alloc(ctx, &ctx->tu, nnz, "alloc test u"));
+        RC(dev_alloc(ctx, &ctx->tv, nnz, "alloc test v"));
+        RC(dev_alloc(ctx, &ctx->tr, nnz, "alloc test r"));
+        ctx->cap_t = nnz;
+    }
+    RC(dev_alloc(ctx, &ctx->partials, rmse_parts(), "alloc partials"));
+    RC(dev_alloc(ctx, &ctx->d_out, 2, "alloc out"));
+    const cudaMemcpyKind kind = is_device_ptr(u) ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+    CK(cudaMemcpyAsync(ctx->tu, u, sizeof(int32_t) * nnz, kind, st));
+    CK(cudaMemcpyAsync(ctx->tv, v, sizeof(int32_t) * nnz, kind, st));
+    CK(cudaMemcpyAsync(ctx->tr, r, sizeof(float) * nnz, kind, st));
+    CK(cudaMemsetAsync(ctx->scratch, 0, sizeof(DevScratch), st));
+    CK(launch_validate_rows(ctx->tu, ctx->tv, ctx->tr, nnz, ctx->p_begin, ctx->p_end, ctx->n, ctx->scratch, st));
+    CK(cudaMemcpyAsync(ctx->h_scratch, ctx->scratch, sizeof(DevScratch), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (ctx->h_scratch->bad) return ctx->fail(MF_EINVAL, "mf_rmse: %llu invalid test samples",
+                                              (unsigned long long)ctx->h_scratch->bad);
+    if (ctx->p_begin != 0) CK(launch_rebase(ctx->tu, nnz, (int32_t)ctx->p_begin, st));
+    if (ctx->is_distributed()) return ctx->rmse_partitioned(nnz, out);
+    const ShapeId sh = select_shape(ctx->k, ctx->storage, 0);
+    CK(launch_rmse(sh, ctx->tu, ctx->tv, ctx->tr, nnz, ctx->P, ctx->Q, ctx->k, ctx->partials, rmse_parts(),
+                   ctx->d_out, st));
+    double h = 0;
+    CK(cudaMemcpyAsync(&h, ctx->d_out, sizeof(double), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    *out = h;
+    return MF_OK;
+}
+
+// ----------------------------------------------------------------- factors --
+int mf_ctx::copy_out(const void *X, int64_t count, float *dst) {
+    mf_ctx *ctx = this;
+    cudaStream_t st = stream();
+    if (storage == kF32) {
+        CK(cudaMemcpyAsync(dst, X, sizeof(float) * count, is_device_ptr(dst) ? cudaMemcpyDeviceToDevice
+                                                                               : cudaMemcpyDeviceToHost, st));
+    } else {
+        float *tmp = nullptr;
+        CK(cudaMallocAsync((void **)&tmp, sizeof(float) * std::max<int64_t>(count, 1), st));
+        CK(launch_to_f32(storage, X, tmp, count, st));
+        CK(cudaMemcpyAsync(dst, tmp, sizeof(float) * count, is_device_ptr(dst) ? cudaMemcpyDeviceToDevice
+                                                                                : cudaMemcpyDeviceToHost, st));
+        CK(cudaFreeAsync(tmp, st));
+    }
+    CK(cudaStreamSynchronize(st));
+    return MF_OK;
+}
+
+int mf_ctx::copy_in(void *X, int64_t count, const float *src) {
+    mf_ctx *ctx = this;
+    cudaStream_t st = stream();
+    const bool dsrc = is_device_ptr(src);
+    if (storage == kF32) {
+        CK(cudaMemcpyAsync(X, src, sizeof(float) * count, dsrc ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st));
+    } else {
+        float *tmp = nullptr;
+        CK(cudaMallocAsync((void **)&tmp, sizeof(float) * std::max<int64_t>(count, 1), st));
+        CK(cudaMemcpyAsync(tmp, src, sizeof(float) * count, dsrc ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st));
+        CK(launch_from_f32(storage, X, tmp, count, st));
+        CK(cudaFreeAsync(tmp, st));
+    }
+    CK(cudaStreamSynchronize(st));
+    return MF_OK;
+}
+
+extern "C" int mf_get_factors(mf_ctx *ctx, float *P, float *Q) {
+    if (!ctx) return MF_EINVAL;
+    RC(ctx->ensure_factors());
+    CK(cudaSetDevice(ctx->device));
+    if (ctx->is_distributed()) RC(ctx->gather_q());
+    if (P) RC(ctx->copy_out(ctx->P, ctx->p_rows() * ctx->k, P));
+    if (Q) RC(ctx->copy_out(ctx->Q, ctx->n * ctx->k, Q));
+    return MF_OK;
+}
+
+extern "C" int mf_set_factors(mf_ctx *ctx, const float *P, const float *Q) {
+    if (!ctx) return MF_EINVAL;
+    RC(ctx->ensure_factors());
+    CK(cudaSetDevice(ctx->device));
+    if (P) RC(ctx->copy_in(ctx->P, ctx->p_rows() * ctx->k, P));
+    if (Q) RC(ctx->copy_in(ctx->Q, ctx->n * ctx->k, Q));
+    return MF_OK;
+}
+
+extern "C" int mf_get_order(const mf_ctx *ctx_c, int64_t *out) {
+    mf_ctx *ctx = const_cast<mf_ctx *>(ctx_c);
+    if (!ctx || !out) return MF_EINVAL;
+    if (ctx->N <= 0) return ctx->fail(MF_ESTATE, "mf_get_order before mf_load_coo");
+    if (!ctx->shuffled) {
+        for (int64_t i = 0; i < ctx->N; i++) out[i] = i;
+        return MF_OK;
+    }
+    CK(cudaSetDevice(ctx->device));
+    std::vector<uint32_t> h((size_t)ctx->N);
+    CK(cudaMemcpyAsync(h.data(), ctx->perm, sizeof(uint32_t) * ctx->N, cudaMemcpyDeviceToHost, ctx->stream()));
+    CK(cudaStreamSynchronize(ctx->stream()));
+    for (int64_t i = 0; i < ctx->N; i++) out[i] = (int64_t)h[(size_t)i];
+    return MF_OK;
+}

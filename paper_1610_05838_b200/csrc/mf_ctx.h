@@ -1,0 +1,122 @@
+// mf_ctx.h -- the opaque context behind `mf_ctx *` (include/mf.h).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdarg>
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "../../include/mf.h"
+#include "mf_kernels.cuh"
+
+struct mf_nccl;  // defined in mf_partition.cu
+
+struct mf_ctx {
+    // problem (global)
+    int64_t m = 0, n = 0;
+    int32_t k = 0;
+    float alpha = 0.f, lambda = 0.f;
+    double beta = 0.0;
+    uint64_t seed = 0, seed_shuffle = 0;
+    int32_t epoch = 0;
+
+    // options
+    int storage = 0;  // mf::StorageKind
+    int device = 0;
+    int workers = 0;
+    int batch_f = 256;
+    int wave_rows = 0, wave_cols = 0, wave_perm = 0;
+    int shuffle = 1;
+    int count_updates = 0;
+    int partitions = 0;
+    int variant = 0;
+    int trace = 0;
+    cudaStream_t user_stream = nullptr;
+
+    // device state
+    bool dev_ready = false;
+    int num_sms = 0;
+    cudaStream_t own_stream = nullptr;
+    cudaEvent_t events[4] = {nullptr, nullptr, nullptr, nullptr};
+    mf::DevScratch *scratch = nullptr;
+    mf::DevScratch *h_scratch = nullptr;  // pinned
+    void *P = nullptr, *Q = nullptr;      // storage precision, row-major
+    int64_t p_begin = 0, p_end = 0;       // rows of the global P held here
+
+    // training set (device SoA, stored order)
+    int32_t *u = nullptr, *v = nullptr;
+    float *r = nullptr;
+    uint32_t *perm = nullptr;  // perm[i] = caller index of stored sample i
+    int64_t N = 0, cap_n = 0;
+    int shuffled = 0;
+
+    // deterministic wave layout
+    int32_t *wu = nullptr, *wv = nullptr;
+    float *wr = nullptr;
+    int64_t *wave_off = nullptr;
+    int64_t nwaves = -1;
+
+    // wavefront layout (mf_wavefront.cu)
+    bool wf_valid = false;
+    int wf_s = 0, wf_c = 0;
+    int32_t *fu = nullptr, *fv = nullptr;
+    float *fr = nullptr;
+    int64_t *wf_off = nullptr;    // (s*c + 1) block offsets, block (w, c) at w*c + c
+    int32_t *wf_locks = nullptr;  // c column locks
+    int32_t *wf_seq = nullptr;    // s x c column sequences (this epoch)
+    int64_t *wf_trace = nullptr;  // 4 int64 per block
+    int64_t wf_trace_n = 0;
+
+    // partitioned layout (mf_partition.cu)
+    bool part_valid = false;
+    int part_G = 0;                  // logical partitions (loopback) or world size
+    int32_t *bu = nullptr, *bv = nullptr;
+    float *br = nullptr;
+    int64_t *blk_off = nullptr;      // device copy of block offsets
+    std::vector<int64_t> h_blk_off;  // host copy
+    std::vector<int64_t> q_seg;      // column segment boundaries (G + 1)
+    void *q_buf[2] = {nullptr, nullptr};
+    mf_nccl *nccl = nullptr;
+    int rank = 0, world = 1;
+    cudaStream_t comm_stream = nullptr;
+
+    // scratch for rmse / factors
+    int32_t *tu = nullptr, *tv = nullptr;
+    float *tr = nullptr;
+    int64_t cap_t = 0;
+    double *partials = nullptr, *d_out = nullptr;
+    float *f32_tmp = nullptr;
+
+    std::string err;
+
+    int fail(int code, const char *fmt, ...);
+    int cuda(cudaError_t e, const char *what);
+    int ensure_device();
+    int ensure_factors();
+    cudaStream_t stream() const;
+    int storage_bytes() const;
+    int64_t p_rows() const { return p_end - p_begin; }
+    bool is_distributed() const { return nccl != nullptr; }
+    float eta_at(int32_t t) const;
+    int auto_workers() const;
+    mf::UpdateArgs update_args(float eta) const;
+    int finish_epoch(int schedule, float eta, int launches, int workers_used, mf_epoch_stats *stats);
+    int build_waves();
+    int copy_out(const void *X, int64_t count, float *dst);
+    int copy_in(void *X, int64_t count, const float *src);
+    void drop_layouts();
+    void release();
+
+    // mf_wavefront.cu
+    int build_wavefront();
+    int run_wavefront(const mf::ShapeId &sh, const mf::UpdateArgs &a, int *launches, int *workers_used);
+    void release_wavefront();
+
+    // mf_partition.cu
+    int epoch_partitioned(mf_epoch_stats *stats);
+    int rmse_partitioned(int64_t nnz, double *out);
+    int gather_q();
+    void release_partition();
+};

@@ -1,0 +1,475 @@
+// mf_kernels.cu -- sm_100a kernels of the SGD-MF hot path and their launchers.
+//
+//   k_hogwild  batch-Hogwild! (§3.2.2): persistent warps claim
+//              chunks of f consecutive shuffled samples with one atomic per
+//              chunk and update them lock-free; each L-lane group keeps D
+//              ratings in flight.
+//   k_waves    deterministic conflict-free waves (D-3): one persistent
+//              cooperative kernel, samples pre-sorted by wave, grid barrier
+//              between waves.
+//   k_rmse     test RMSE: fp32 dot, fp64 squared error, fixed
+//              two-level reduction (deterministic).
+//   k_init     A-7 counter-hash initialisation.
+//   k_validate index range / finite rating check.
+//   shuffle    A-8 hash-key radix sort (CUB) + gather.
+#include <cub/device/device_radix_sort.cuh>
+
+#include <algorithm>
+#include <cstdio>
+
+#include "mf_kernels.cuh"
+#include "sgd_core.cuh"
+
+namespace mf {
+
+static constexpr int kBlock = 256;  // 8 warps per CTA
+static constexpr int kWarpsPerBlock = kBlock / 32;
+
+// ------------------------------------------------------------------ shapes --
+// Shape table: (storage, L, V, VB, full).  Fast shapes cover k = L*V*VB/bytes
+// exactly; generic shapes (full = 0) mask lanes beyond k.
+#define MF_FAST_SHAPES(X)                                                                                \
+    X(kF32, 8, 1, 16, 1) X(kF32, 16, 1, 16, 1) X(kF32, 32, 1, 16, 1) X(kF32, 32, 2, 16, 1)               \
+    X(kF32, 16, 2, 16, 1) X(kF32, 8, 4, 16, 1)                                                           \
+    X(kF16, 4, 1, 16, 1) X(kF16, 8, 1, 16, 1) X(kF16, 16, 1, 16, 1) X(kF16, 32, 1, 16, 1)                \
+    X(kF16, 8, 2, 16, 1) X(kF16, 32, 1, 8, 1)                                                            \
+    X(kBF16, 4, 1, 16, 1) X(kBF16, 8, 1, 16, 1) X(kBF16, 16, 1, 16, 1) X(kBF16, 32, 1, 16, 1)            \
+    X(kBF16, 8, 2, 16, 1) X(kBF16, 32, 1, 8, 1)
+#define MF_GENERIC_SHAPES(X)                                                                             \
+    X(kF32, 32, 1, 4, 0) X(kF32, 32, 4, 4, 0) X(kF32, 32, 16, 4, 0) X(kF32, 32, 32, 4, 0)                \
+    X(kF16, 32, 1, 4, 0) X(kF16, 32, 4, 4, 0) X(kF16, 32, 16, 4, 0)                                      \
+    X(kF16, 32, 1, 2, 0) X(kF16, 32, 4, 2, 0) X(kF16, 32, 16, 2, 0) X(kF16, 32, 32, 2, 0)                \
+    X(kBF16, 32, 1, 4, 0) X(kBF16, 32, 4, 4, 0) X(kBF16, 32, 16, 4, 0)                                   \
+    X(kBF16, 32, 1, 2, 0) X(kBF16, 32, 4, 2, 0) X(kBF16, 32, 16, 2, 0) X(kBF16, 32, 32, 2, 0)
+
+template <class F>
+static cudaError_t dispatch_shape(const ShapeId &s, F &&f) {
+#define MF_CASE(S_, L_, V_, VB_, FULL_)                                                                  \
+    if (s.storage == S_ && s.L == L_ && s.V == V_ && s.VB == VB_ && s.full == FULL_)                     \
+        return f(Shape<S_, L_, V_, VB_, (bool)FULL_>{});
+    MF_FAST_SHAPES(MF_CASE)
+    MF_GENERIC_SHAPES(MF_CASE)
+#undef MF_CASE
+    return cudaErrorInvalidValue;
+}
+
+ShapeId select_shape(int k, int storage, int variant) {
+    const int bytes = storage == kF32 ? 4 : 2;
+    if (storage == kF32) {
+        if (k == 128) {
+            if (variant == 1) return {storage, 16, 2, 16, 1};
+            if (variant == 2) return {storage, 8, 4, 16, 1};
+            return {storage, 32, 1, 16, 1};
+        }
+        if (k == 32) return {storage, 8, 1, 16, 1};
+        if (k == 64) return {storage, 16, 1, 16, 1};
+        if (k == 256) return {storage, 32, 2, 16, 1};
+    } else {
+        if (k == 128) {
+            if (variant == 1) return {storage, 8, 2, 16, 1};
+            if (variant == 2) return {storage, 32, 1, 8, 1};
+            return {storage, 16, 1, 16, 1};
+        }
+        if (k == 32) return {storage, 4, 1, 16, 1};
+        if (k == 64) return {storage, 8, 1, 16, 1};
+        if (k == 256) return {storage, 32, 1, 16, 1};
+    }
+    // generic: L = 32, VB = 4 bytes (or 2 for odd k with 16-bit storage), V vectors per lane
+    const int vb = (bytes == 2 && (k % 2)) ? 2 : 4;
+    const int epv = vb / bytes;
+    const int per_lane = (k + 32 * epv - 1) / (32 * epv);
+    int V = per_lane <= 1 ? 1 : per_lane <= 4 ? 4 : per_lane <= 16 ? 16 : 32;
+    if (vb == 4 && bytes == 2 && V == 32) V = 16;  // 16-bit, even k: 32*16*2 = 1024 covers k <= 1024
+    return {storage, 32, V, vb, 0};
+}
+
+// ------------------------------------------------------------- batch-Hogwild!
+// Grid: persistent CTAs of 8 warps.  A warp claims chunk c (f samples) with one
+// atomicAdd, loads the chunk's COO triples 32 at a time (lane i holds sample
+// base+i; three coalesced 128-byte loads, read-only path as in PAPER.md:183)
+// and hands them to its G groups by __shfl_sync.  Each group then keeps D
+// ratings in flight: D row-pair loads are issued before the first dot.
+template <class SH, int D>
+__global__ void __launch_bounds__(kBlock) k_hogwild(UpdateArgs a) {
+    constexpr int L = SH::L, G = SH::G;
+    static_assert(L % D == 0, "D must divide the per-group samples of a 32-sample tile");
+    const int lane = threadIdx.x & 31;
+    const int grp = lane / L, sub = lane % L;
+    const int k = SH::FULL ? SH::KMAX : a.k;
+    const int64_t N = a.n;
+    const int f = a.batch_f;
+    if ((int)((blockIdx.x * kBlock + threadIdx.x) >> 5) >= a.active_warps) return;  // warp-uniform
+    unsigned long long done = 0;
+    int bad = 0;
+
+    for (;;) {
+        unsigned long long c = 0;
+        if (lane == 0) c = atomicAdd(&a.scratch->chunk, 1ull);
+        c = __shfl_sync(0xffffffffu, c, 0);
+        const int64_t beg = (int64_t)c * f;
+        if (beg >= N) break;
+        const int64_t end = min(beg + (int64_t)f, N);
+        for (int64_t base = beg; base < end; base += 32) {
+            const int64_t i = base + lane;
+            const bool ok = i < end;
+            const int32_t tu = ok ? __ldg(a.u + i) : 0;
+            const int32_t tv = ok ? __ldg(a.v + i) : 0;
+            const float tr = ok ? __ldg(a.r + i) : 0.f;
+            const int cnt = (int)(end - base < 32 ? end - base : 32);
+            if (a.count_updates) done += (lane == 0) ? cnt : 0;
+#pragma unroll 1
+            for (int j0 = 0; j0 < 32 / G; j0 += D) {
+                int32_t su[D], sv[D];
+                float sr[D];
+                bool val[D];
+                RowRaw<SH> pr[D], qr[D];
+#pragma unroll
+                for (int d = 0; d < D; d++) {
+                    const int s = (j0 + d) * G + grp;
+                    su[d] = __shfl_sync(0xffffffffu, tu, s);
+                    sv[d] = __shfl_sync(0xffffffffu, tv, s);
+                    sr[d] = __shfl_sync(0xffffffffu, tr, s);
+                    val[d] = s < cnt;
+                }
+#pragma unroll
+                for (int d = 0; d < D; d++) {
+                    load_row<SH>(a.P, su[d], k, sub, val[d], pr[d]);
+                    load_row<SH>(a.Q, sv[d], k, sub, val[d], qr[d]);
+                }
+#pragma unroll
+                for (int d = 0; d < D; d++) {
+                    float p[SH::E], q[SH::E];
+                    widen_row<SH>(pr[d], p);
+                    widen_row<SH>(qr[d], q);
+                    const float err = sr[d] - group_dot<SH>(p, q);
+                    if (val[d] && !isfinite(err)) bad = 1;
+                    sgd_step<SH>(p, q, err, a.eta, a.lam);
+                    narrow_row<SH>(p, pr[d]);
+                    narrow_row<SH>(q, qr[d]);
+                    store_row<SH>(a.P, su[d], k, sub, val[d], pr[d]);
+                    store_row<SH>(a.Q, sv[d], k, sub, val[d], qr[d]);
+                }
+            }
+        }
+    }
+    if (bad) a.scratch->diverged = 1;
+    if (a.count_updates && lane == 0 && done) atomicAdd(&a.scratch->updates, done);
+}
+
+template <class SH, int D>
+static cudaError_t hogwild_launch(const UpdateArgs &a, int workers, cudaStream_t st, int *used) {
+    int dev = 0, sms = 0, per_sm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_hogwild<SH, D>, kBlock, 0);
+    if (per_sm < 1) per_sm = 1;
+    const int slots_per_warp = SH::G * D;
+    int64_t warps = (int64_t)sms * per_sm * kWarpsPerBlock;
+    if (workers > 0) warps = std::min<int64_t>(warps, (workers + slots_per_warp - 1) / slots_per_warp);
+    const int64_t chunks = (a.n + a.batch_f - 1) / a.batch_f;
+    warps = std::max<int64_t>(1, std::min<int64_t>(warps, chunks));
+    const int blocks = (int)((warps + kWarpsPerBlock - 1) / kWarpsPerBlock);
+    if (used) *used = (int)(warps * slots_per_warp);
+    UpdateArgs args = a;
+    args.active_warps = (int)warps;
+    k_hogwild<SH, D><<<blocks, kBlock, 0, st>>>(args);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_hogwild(const ShapeId &sh, const UpdateArgs &a, int workers, int variant, cudaStream_t st,
+                           int *workers_used) {
+    const int D = (variant >> 4) & 0xF;  // bits 4..7 select samples in flight per group (0 = default)
+    return dispatch_shape(sh, [&](auto tag) -> cudaError_t {
+        using SH = decltype(tag);
+        constexpr int L = SH::L;
+        if constexpr (SH::FULL) {
+            if (D == 4 && L % 4 == 0) return hogwild_launch<SH, (L % 4 == 0 ? 4 : 1)>(a, workers, st, workers_used);
+            if (D != 1 && L % 2 == 0) return hogwild_launch<SH, (L % 2 == 0 ? 2 : 1)>(a, workers, st, workers_used);
+        }
+        return hogwild_launch<SH, 1>(a, workers, st, workers_used);
+    });
+}
+
+// ------------------------------------------------------- deterministic waves
+// All CTAs are co-resident (cooperative launch); between waves a sense-free
+// generation barrier with gpu-scope fences orders every P/Q store of wave w
+// before any load of wave w+1 (loads are ld.global.cg, so L1 is never read).
+__device__ __forceinline__ void grid_barrier(DevScratch *s, unsigned nblocks) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        volatile unsigned *gen = &s->bar_gen;
+        const unsigned g = *gen;
+        __threadfence();
+        if (atomicAdd(&s->bar_count, 1u) == nblocks - 1) {
+            s->bar_count = 0;
+            __threadfence();
+            atomicExch(&s->bar_gen, g + 1);
+        } else {
+            while (*gen == g) __nanosleep(20);
+        }
+        __threadfence();
+    }
+    __syncthreads();
+}
+
+template <class SH>
+__global__ void __launch_bounds__(kBlock) k_waves(UpdateArgs a) {
+    constexpr int L = SH::L;
+    const int lane = threadIdx.x & 31, sub = lane % L;
+    const int k = SH::FULL ? SH::KMAX : a.k;
+    const int64_t groups = (int64_t)gridDim.x * kBlock / L;
+    const int64_t gid = ((int64_t)blockIdx.x * kBlock + threadIdx.x) / L;
+    int bad = 0;
+    unsigned long long done = 0;
+    for (int64_t w = 0; w < a.nwaves; w++) {
+        const int64_t lo = a.wave_off[w], hi = a.wave_off[w + 1];
+        // warp-uniform trip count so the full-warp shuffles stay converged
+        const int64_t warp_first = lo + (gid - (lane / L));
+        for (int64_t s0 = warp_first; s0 < hi; s0 += groups) {
+            const int64_t s = s0 + lane / L;
+            const bool val = s < hi;
+            const int32_t su = val ? __ldg(a.u + s) : 0;
+            const int32_t sv = val ? __ldg(a.v + s) : 0;
+            const float sr = val ? __ldg(a.r + s) : 0.f;
+            RowRaw<SH> pr, qr;
+            load_row<SH>(a.P, su, k, sub, val, pr);
+            load_row<SH>(a.Q, sv, k, sub, val, qr);
+            float p[SH::E], q[SH::E];
+            widen_row<SH>(pr, p);
+            widen_row<SH>(qr, q);
+            const float err = sr - group_dot<SH>(p, q);
+            if (val && !isfinite(err)) bad = 1;
+            sgd_step<SH>(p, q, err, a.eta, a.lam);
+            narrow_row<SH>(p, pr);
+            narrow_row<SH>(q, qr);
+            store_row<SH>(a.P, su, k, sub, val, pr);
+            store_row<SH>(a.Q, sv, k, sub, val, qr);
+            if (val && sub == 0) done++;
+        }
+        grid_barrier(a.scratch, gridDim.x);
+    }
+    if (bad) a.scratch->diverged = 1;
+    if (a.count_updates && done) atomicAdd(&a.scratch->updates, done);
+}
+
+cudaError_t launch_waves(const ShapeId &sh, const UpdateArgs &a, cudaStream_t st, int *launches) {
+    return dispatch_shape(sh, [&](auto tag) -> cudaError_t {
+        using SH = decltype(tag);
+        int dev = 0, sms = 0, per_sm = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_waves<SH>, kBlock, 0);
+        if (per_sm < 1) return cudaErrorLaunchOutOfResources;
+        // the largest wave decides how many groups are useful
+        int blocks = sms * std::min(per_sm, 4);
+        UpdateArgs args = a;
+        void *kargs[] = {&args};
+        if (launches) *launches = 1;
+        return cudaLaunchCooperativeKernel((const void *)k_waves<SH>, dim3(blocks), dim3(kBlock), kargs, 0, st);
+    });
+}
+
+// -------------------------------------------------------------------- RMSE --
+static constexpr int kRmseBlocks = 148 * 4;
+int rmse_parts() { return kRmseBlocks; }
+
+template <class SH>
+__global__ void __launch_bounds__(kBlock) k_rmse(const int32_t *u, const int32_t *v, const float *r, int64_t n,
+                                                 const void *P, const void *Q, int kk, double *partials) {
+    constexpr int L = SH::L;
+    const int lane = threadIdx.x & 31, sub = lane % L;
+    const int k = SH::FULL ? SH::KMAX : kk;
+    const int64_t groups = (int64_t)gridDim.x * kBlock / L;
+    const int64_t gid = ((int64_t)blockIdx.x * kBlock + threadIdx.x) / L;
+    double acc = 0.0;
+    const int64_t warp_first = gid - lane / L;
+    for (int64_t s0 = warp_first; s0 < n; s0 += groups) {
+        const int64_t s = s0 + lane / L;
+        const bool val = s < n;
+        const int32_t su = val ? __ldg(u + s) : 0;
+        const int32_t sv = val ? __ldg(v + s) : 0;
+        const float sr = val ? __ldg(r + s) : 0.f;
+        RowRaw<SH> pr, qr;
+        load_row<SH>(P, su, k, sub, val, pr);
+        load_row<SH>(Q, sv, k, sub, val, qr);
+        float p[SH::E], q[SH::E];
+        widen_row<SH>(pr, p);
+        widen_row<SH>(qr, q);
+        const float dot = group_dot<SH>(p, q);
+        if (val && sub == 0) {
+            const double e = (double)sr - (double)dot;
+            acc += e * e;
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    __shared__ double ws[kWarpsPerBlock];
+    if (lane == 0) ws[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double s = 0.0;
+        for (int i = 0; i < kWarpsPerBlock; i++) s += ws[i];
+        partials[blockIdx.x] = s;
+    }
+}
+
+__global__ void k_sum_partials(const double *partials, int n, int64_t count, double *out) {
+    __shared__ double sh[256];
+    double s = 0.0;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) s += partials[i];
+    sh[threadIdx.x] = s;
+    __syncthreads();
+    for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+        if ((int)threadIdx.x < o) sh[threadIdx.x] += sh[threadIdx.x + o];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) out[0] = sqrt(sh[0] / (double)count);
+}
+
+cudaError_t launch_rmse(const ShapeId &sh, const int32_t *u, const int32_t *v, const float *r, int64_t n,
+                        const void *P, const void *Q, int k, double *partials, int nparts, double *out,
+                        cudaStream_t st) {
+    cudaError_t e = dispatch_shape(sh, [&](auto tag) -> cudaError_t {
+        using SH = decltype(tag);
+        k_rmse<SH><<<nparts, kBlock, 0, st>>>(u, v, r, n, P, Q, k, partials);
+        return cudaGetLastError();
+    });
+    if (e != cudaSuccess) return e;
+    k_sum_partials<<<1, 256, 0, st>>>(partials, nparts, n, out);
+    return cudaGetLastError();
+}
+
+// -------------------------------------------------------------------- init --
+// A-7: X[row][col] = (float)(h >> 40) * 2^-24 * (float)(1/sqrt(k)),
+// h = splitmix64(seed ^ (tag << 60) ^ (row*k + col)), rounded to storage.
+__device__ __forceinline__ void store_scalar(void *X, int storage, int64_t i, float x) {
+    if (storage == kF32) reinterpret_cast<float *>(X)[i] = x;
+    else if (storage == kF16) reinterpret_cast<__half *>(X)[i] = __float2half_rn(x);
+    else reinterpret_cast<__nv_bfloat16 *>(X)[i] = __float2bfloat16_rn(x);
+}
+__device__ __forceinline__ float load_scalar(const void *X, int storage, int64_t i) {
+    if (storage == kF32) return reinterpret_cast<const float *>(X)[i];
+    if (storage == kF16) return __half2float(reinterpret_cast<const __half *>(X)[i]);
+    return __bfloat162float(reinterpret_cast<const __nv_bfloat16 *>(X)[i]);
+}
+
+__global__ void k_init(void *X, int64_t elem0, int64_t count, uint64_t seed, uint32_t tag, float scale, int storage) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x) {
+        const uint64_t h = splitmix64(seed ^ ((uint64_t)tag << 60) ^ (uint64_t)(elem0 + i));
+        const float unit = __fmul_rn((float)(h >> 40), 0x1.0p-24f);
+        store_scalar(X, storage, i, __fmul_rn(unit, scale));
+    }
+}
+
+cudaError_t launch_init_offset(int storage, void *X, int64_t elem0, int64_t count, int k, uint64_t seed, uint32_t tag,
+                               cudaStream_t st) {
+    const float scale = (float)(1.0 / sqrt((double)k));
+    const int blocks = (int)std::min<int64_t>((count + 255) / 256, 148 * 32);
+    k_init<<<std::max(blocks, 1), 256, 0, st>>>(X, elem0, count, seed, tag, scale, storage);
+    return cudaGetLastError();
+}
+
+__global__ void k_from_f32(void *X, const float *src, int64_t count, int storage) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x)
+        store_scalar(X, storage, i, src[i]);
+}
+__global__ void k_to_f32(const void *X, float *dst, int64_t count, int storage) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += (int64_t)gridDim.x * blockDim.x)
+        dst[i] = load_scalar(X, storage, i);
+}
+cudaError_t launch_from_f32(int storage, void *X, const float *src, int64_t count, cudaStream_t st) {
+    const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((count + 255) / 256, 148 * 32));
+    k_from_f32<<<blocks, 256, 0, st>>>(X, src, count, storage);
+    return cudaGetLastError();
+}
+cudaError_t launch_to_f32(int storage, const void *X, float *dst, int64_t count, cudaStream_t st) {
+    const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((count + 255) / 256, 148 * 32));
+    k_to_f32<<<blocks, 256, 0, st>>>(X, dst, count, storage);
+    return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------- validate --
+__global__ void k_validate(const int32_t *u, const int32_t *v, const float *r, int64_t n, int64_t row_lo,
+                           int64_t row_hi, int64_t n_cols, DevScratch *s) {
+    unsigned long long bad = 0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t a = u[i], b = v[i];
+        const float x = r[i];
+        bad += (a < row_lo || a >= row_hi || b < 0 || b >= n_cols || !isfinite(x)) ? 1 : 0;
+    }
+    for (int o = 16; o > 0; o >>= 1) bad += __shfl_xor_sync(0xffffffffu, bad, o);
+    if ((threadIdx.x & 31) == 0 && bad) atomicAdd(&s->bad, bad);
+}
+cudaError_t launch_validate_rows(const int32_t *u, const int32_t *v, const float *r, int64_t n, int64_t row_lo,
+                                 int64_t row_hi, int64_t n_cols, DevScratch *scratch, cudaStream_t st) {
+    const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 148 * 16));
+    k_validate<<<blocks, 256, 0, st>>>(u, v, r, n, row_lo, row_hi, n_cols, scratch);
+    return cudaGetLastError();
+}
+
+__global__ void k_rebase(int32_t *u, int64_t n, int32_t off) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        u[i] -= off;
+}
+cudaError_t launch_rebase(int32_t *u, int64_t n, int32_t off, cudaStream_t st) {
+    const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 148 * 16));
+    k_rebase<<<blocks, 256, 0, st>>>(u, n, off);
+    return cudaGetLastError();
+}
+
+// ----------------------------------------------------------------- shuffle --
+// A-8: order samples by key splitmix64(seed ^ i) (distinct for distinct i, as
+// splitmix64 is a bijection), ties impossible; perm[j] = original index.
+__global__ void k_shuffle_keys(uint64_t *keys, uint32_t *idx, int64_t n, uint64_t seed) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        keys[i] = splitmix64(seed ^ (uint64_t)i);
+        idx[i] = (uint32_t)i;
+    }
+}
+__global__ void k_gather(const int32_t *u_in, const int32_t *v_in, const float *r_in, const uint32_t *idx, int64_t n,
+                         int32_t *u_out, int32_t *v_out, float *r_out) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t j = idx[i];
+        u_out[i] = u_in[j];
+        v_out[i] = v_in[j];
+        r_out[i] = r_in[j];
+    }
+}
+cudaError_t launch_gather(const int32_t *u_in, const int32_t *v_in, const float *r_in, const uint32_t *idx, int64_t n,
+                          int32_t *u_out, int32_t *v_out, float *r_out, cudaStream_t st) {
+    const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 148 * 16));
+    k_gather<<<blocks, 256, 0, st>>>(u_in, v_in, r_in, idx, n, u_out, v_out, r_out);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_shuffle(const int32_t *u_in, const int32_t *v_in, const float *r_in, int64_t n, uint64_t seed,
+                           int32_t *u_out, int32_t *v_out, float *r_out, uint32_t *perm_out, cudaStream_t st) {
+    if (n > (int64_t)0xFFFFFFFFll) return cudaErrorInvalidValue;
+    uint64_t *k0 = nullptr, *k1 = nullptr;
+    uint32_t *i0 = nullptr;
+    void *tmp = nullptr;
+    size_t tmp_bytes = 0;
+    cudaError_t e;
+#define MF_TRY(x) do { e = (x); if (e != cudaSuccess) goto done; } while (0)
+    MF_TRY(cudaMallocAsync(&k0, sizeof(uint64_t) * n, st));
+    MF_TRY(cudaMallocAsync(&k1, sizeof(uint64_t) * n, st));
+    MF_TRY(cudaMallocAsync(&i0, sizeof(uint32_t) * n, st));
+    {
+        const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 148 * 16));
+        k_shuffle_keys<<<blocks, 256, 0, st>>>(k0, i0, n, seed);
+        MF_TRY(cudaGetLastError());
+    }
+    MF_TRY(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, k0, k1, i0, perm_out, n, 0, 64, st));
+    MF_TRY(cudaMallocAsync(&tmp, tmp_bytes, st));
+    MF_TRY(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, k0, k1, i0, perm_out, n, 0, 64, st));
+    MF_TRY(launch_gather(u_in, v_in, r_in, perm_out, n, u_out, v_out, r_out, st));
+done:
+    if (tmp) cudaFreeAsync(tmp, st);
+    if (k0) cudaFreeAsync(k0, st);
+    if (k1) cudaFreeAsync(k1, st);
+    if (i0) cudaFreeAsync(i0, st);
+#undef MF_TRY
+    return e;
+}
+
+}  // namespace mf

@@ -1,0 +1,70 @@
+// mf_kernels.cuh -- kernel argument blocks and host launch entry points
+// shared between the host API (mf_api.cu) and the kernel translation units.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <cstdint>
+
+namespace mf {
+
+enum StorageKind { kF32 = 0, kF16 = 1, kBF16 = 2 };
+
+// device scratch words reset at the start of every epoch
+struct DevScratch {
+    unsigned long long chunk;     // batch-Hogwild! chunk claim counter
+    unsigned long long updates;   // exactly-once counter (MF_OPT_COUNT_UPDATES)
+    int diverged;                 // set when any err is non-finite
+    unsigned bar_count;           // grid barrier arrivals
+    unsigned bar_gen;             // grid barrier generation
+    int pad;
+    unsigned long long bad;       // validation: out-of-range / non-finite count
+};
+
+struct UpdateArgs {
+    const int32_t *u;
+    const int32_t *v;
+    const float *r;
+    int64_t n;          // samples (or end of range)
+    void *P;
+    void *Q;
+    int k;
+    float eta;
+    float lam;
+    int batch_f;        // samples per chunk (multiple of 32)
+    int count_updates;
+    DevScratch *scratch;
+    const int64_t *wave_off;  // deterministic: wave offsets (nwaves + 1)
+    int64_t nwaves;
+    int active_warps;   // batch-Hogwild!: warps beyond this exit at once (exact worker count)
+};
+
+// Kernel-shape choice for (k, storage); filled by select_shape().
+struct ShapeId {
+    int storage, L, V, VB, full;
+};
+
+// launchers (return cudaError_t; grid sizing inside)
+cudaError_t launch_hogwild(const ShapeId &sh, const UpdateArgs &a, int workers, int variant, cudaStream_t st,
+                           int *workers_used);
+cudaError_t launch_waves(const ShapeId &sh, const UpdateArgs &a, cudaStream_t st, int *launches);
+cudaError_t launch_rmse(const ShapeId &sh, const int32_t *u, const int32_t *v, const float *r, int64_t n,
+                        const void *P, const void *Q, int k, double *partials, int nparts, double *out,
+                        cudaStream_t st);
+cudaError_t launch_init_offset(int storage, void *X, int64_t elem0, int64_t count, int k, uint64_t seed, uint32_t tag,
+                               cudaStream_t st);
+cudaError_t launch_init_rows(int storage, void *X, int64_t row0, int64_t rows, int k, uint64_t seed, uint32_t tag,
+                             cudaStream_t st);
+cudaError_t launch_from_f32(int storage, void *X, const float *src, int64_t count, cudaStream_t st);
+cudaError_t launch_to_f32(int storage, const void *X, float *dst, int64_t count, cudaStream_t st);
+cudaError_t launch_validate_rows(const int32_t *u, const int32_t *v, const float *r, int64_t n, int64_t row_lo,
+                                 int64_t row_hi, int64_t n_cols, DevScratch *scratch, cudaStream_t st);
+cudaError_t launch_rebase(int32_t *u, int64_t n, int32_t off, cudaStream_t st);
+cudaError_t launch_shuffle(const int32_t *u_in, const int32_t *v_in, const float *r_in, int64_t n, uint64_t seed,
+                           int32_t *u_out, int32_t *v_out, float *r_out, uint32_t *perm_out, cudaStream_t st);
+cudaError_t launch_gather(const int32_t *u_in, const int32_t *v_in, const float *r_in, const uint32_t *idx, int64_t n,
+                          int32_t *u_out, int32_t *v_out, float *r_out, cudaStream_t st);
+
+ShapeId select_shape(int k, int storage, int variant);
+int rmse_parts();
+
+}  // namespace mf

@@ -1,0 +1,254 @@
+// sgd_core.cuh -- device-side building blocks of one SGD update (sm_100a).
+//
+// One rating r_uv is handled by a GROUP of L consecutive lanes of a warp
+// (L = 4..32, sized by k and the storage width; PAPER.md:188 used a fixed
+// 32-thread worker).  Lane `sub` of the group owns V vectors of VB bytes of
+// each of p_u and q_v; vector j of lane sub covers elements
+//     d = (j*L + sub)*EPV ... +EPV-1,        EPV = VB / sizeof(storage)
+// so every load/store instruction of the group touches one contiguous
+// L*VB-byte span of the row (coalesced).
+//
+// Per update (§2.2):
+//   dot  = sum_d p[d] q[d]       fp32 FMA per lane, then __shfl_xor_sync tree over
+//                                the L lanes ("warp shuffle")
+//   err  = r - dot
+//   p'   = p + eta (err q - lambda p),  q' = q + eta (err p - lambda q)
+//          both from the snapshot p, q held in registers (A-1);
+//          fp32 math, storage fp32 / fp16 / bf16 rounded to nearest even
+//          (A-13).
+//
+// P and Q are read with ld.global.cg (L2, not L1): they are written
+// concurrently by other SMs, so they must never go through the
+// non-coherent read-only path (__ldg is only for R).
+#pragma once
+
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+#include <cstdint>
+
+#include "mf_kernels.cuh"
+
+namespace mf {
+
+
+
+// ---------------------------------------------------------------- vectors --
+template <int VB>
+struct Vec;  // VB bytes held in NW 32-bit words
+template <>
+struct Vec<16> {
+    static constexpr int NW = 4;
+    static __device__ __forceinline__ void ld(const void *p, uint32_t (&w)[4]) {
+        uint4 x = __ldcg(reinterpret_cast<const uint4 *>(p));
+        w[0] = x.x; w[1] = x.y; w[2] = x.z; w[3] = x.w;
+    }
+    static __device__ __forceinline__ void st(void *p, const uint32_t (&w)[4]) {
+        __stcg(reinterpret_cast<uint4 *>(p), make_uint4(w[0], w[1], w[2], w[3]));
+    }
+};
+template <>
+struct Vec<8> {
+    static constexpr int NW = 2;
+    static __device__ __forceinline__ void ld(const void *p, uint32_t (&w)[2]) {
+        uint2 x = __ldcg(reinterpret_cast<const uint2 *>(p));
+        w[0] = x.x; w[1] = x.y;
+    }
+    static __device__ __forceinline__ void st(void *p, const uint32_t (&w)[2]) {
+        __stcg(reinterpret_cast<uint2 *>(p), make_uint2(w[0], w[1]));
+    }
+};
+template <>
+struct Vec<4> {
+    static constexpr int NW = 1;
+    static __device__ __forceinline__ void ld(const void *p, uint32_t (&w)[1]) {
+        w[0] = __ldcg(reinterpret_cast<const unsigned int *>(p));
+    }
+    static __device__ __forceinline__ void st(void *p, const uint32_t (&w)[1]) {
+        __stcg(reinterpret_cast<unsigned int *>(p), w[0]);
+    }
+};
+template <>
+struct Vec<2> {  // one 16-bit element in the low half of w[0]
+    static constexpr int NW = 1;
+    static __device__ __forceinline__ void ld(const void *p, uint32_t (&w)[1]) {
+        w[0] = __ldcg(reinterpret_cast<const unsigned short *>(p));
+    }
+    static __device__ __forceinline__ void st(void *p, const uint32_t (&w)[1]) {
+        __stcg(reinterpret_cast<unsigned short *>(p), (unsigned short)(w[0] & 0xFFFFu));
+    }
+};
+
+// ---------------------------------------------------------------- storage --
+template <int S>
+struct Storage;
+template <>
+struct Storage<kF32> {
+    static constexpr int BYTES = 4;
+    template <int NW>
+    static __device__ __forceinline__ void widen(const uint32_t (&w)[NW], float *x, int n) {
+#pragma unroll
+        for (int i = 0; i < NW; i++) x[i] = __uint_as_float(w[i]);
+    }
+    template <int NW>
+    static __device__ __forceinline__ void narrow(const float *x, uint32_t (&w)[NW], int n) {
+#pragma unroll
+        for (int i = 0; i < NW; i++) w[i] = __float_as_uint(x[i]);
+    }
+};
+template <>
+struct Storage<kF16> {
+    static constexpr int BYTES = 2;
+    template <int NW>
+    static __device__ __forceinline__ void widen(const uint32_t (&w)[NW], float *x, int n) {
+        if (n == 1) {
+            x[0] = __half2float(__ushort_as_half((unsigned short)(w[0] & 0xFFFFu)));
+            return;
+        }
+#pragma unroll
+        for (int i = 0; i < NW; i++) {
+            __half2 h = *reinterpret_cast<const __half2 *>(&w[i]);
+            float2 f = __half22float2(h);
+            x[2 * i] = f.x;
+            x[2 * i + 1] = f.y;
+        }
+    }
+    template <int NW>
+    static __device__ __forceinline__ void narrow(const float *x, uint32_t (&w)[NW], int n) {
+        if (n == 1) {
+            w[0] = __half_as_ushort(__float2half_rn(x[0]));
+            return;
+        }
+#pragma unroll
+        for (int i = 0; i < NW; i++) {
+            __half2 h = __floats2half2_rn(x[2 * i], x[2 * i + 1]);
+            w[i] = *reinterpret_cast<uint32_t *>(&h);
+        }
+    }
+};
+template <>
+struct Storage<kBF16> {
+    static constexpr int BYTES = 2;
+    template <int NW>
+    static __device__ __forceinline__ void widen(const uint32_t (&w)[NW], float *x, int n) {
+        if (n == 1) {
+            x[0] = __uint_as_float(w[0] << 16);
+            return;
+        }
+#pragma unroll
+        for (int i = 0; i < NW; i++) {
+            x[2 * i] = __uint_as_float(w[i] << 16);
+            x[2 * i + 1] = __uint_as_float(w[i] & 0xFFFF0000u);
+        }
+    }
+    template <int NW>
+    static __device__ __forceinline__ void narrow(const float *x, uint32_t (&w)[NW], int n) {
+        if (n == 1) {
+            w[0] = __bfloat16_as_ushort(__float2bfloat16_rn(x[0]));
+            return;
+        }
+#pragma unroll
+        for (int i = 0; i < NW; i++) {
+            __nv_bfloat162 h = __floats2bfloat162_rn(x[2 * i], x[2 * i + 1]);
+            w[i] = *reinterpret_cast<uint32_t *>(&h);
+        }
+    }
+};
+
+// ------------------------------------------------------------- group shape --
+// S storage kind, L lanes per rating, V vectors per lane, VB bytes per vector,
+// FULL: k == KMAX exactly (no masking).
+template <int S_, int L_, int V_, int VB_, bool FULL_>
+struct Shape {
+    static constexpr int S = S_, L = L_, V = V_, VB = VB_;
+    static constexpr bool FULL = FULL_;
+    static constexpr int BYTES = Storage<S>::BYTES;
+    static constexpr int EPV = VB / BYTES;  // elements per vector
+    static constexpr int NW = Vec<VB>::NW;  // 32-bit words per vector
+    static constexpr int E = V * EPV;       // elements per lane
+    static constexpr int KMAX = L * E;      // largest k this shape covers
+    static constexpr int G = 32 / L;        // groups (concurrent ratings) per warp
+    static_assert(32 % L == 0, "L must divide 32");
+    static_assert(EPV >= 1, "vector narrower than one element");
+};
+
+// One lane's slice of a feature row, raw storage words.
+template <class SH>
+struct RowRaw {
+    uint32_t w[SH::V][SH::NW];
+};
+
+// byte offset of vector j of lane `sub` inside a row
+template <class SH>
+__device__ __forceinline__ int64_t vec_elem(int j, int sub) {
+    return (int64_t)(j * SH::L + sub) * SH::EPV;
+}
+
+template <class SH>
+__device__ __forceinline__ void load_row(const void *base, int64_t row, int k, int sub, bool valid,
+                                         RowRaw<SH> &out) {
+    const char *rp = reinterpret_cast<const char *>(base) + row * (int64_t)k * SH::BYTES;
+#pragma unroll
+    for (int j = 0; j < SH::V; j++) {
+        const int64_t e = vec_elem<SH>(j, sub);
+        if (valid && (SH::FULL || e < k)) {
+            Vec<SH::VB>::ld(rp + e * SH::BYTES, out.w[j]);
+        } else {
+#pragma unroll
+            for (int i = 0; i < SH::NW; i++) out.w[j][i] = 0u;
+        }
+    }
+}
+
+template <class SH>
+__device__ __forceinline__ void store_row(void *base, int64_t row, int k, int sub, bool valid, const RowRaw<SH> &in) {
+    char *rp = reinterpret_cast<char *>(base) + row * (int64_t)k * SH::BYTES;
+#pragma unroll
+    for (int j = 0; j < SH::V; j++) {
+        const int64_t e = vec_elem<SH>(j, sub);
+        if (valid && (SH::FULL || e < k)) Vec<SH::VB>::st(rp + e * SH::BYTES, in.w[j]);
+    }
+}
+
+template <class SH>
+__device__ __forceinline__ void widen_row(const RowRaw<SH> &in, float (&x)[SH::E]) {
+#pragma unroll
+    for (int j = 0; j < SH::V; j++) Storage<SH::S>::template widen<SH::NW>(in.w[j], &x[j * SH::EPV], SH::EPV);
+}
+
+template <class SH>
+__device__ __forceinline__ void narrow_row(const float (&x)[SH::E], RowRaw<SH> &out) {
+#pragma unroll
+    for (int j = 0; j < SH::V; j++) Storage<SH::S>::template narrow<SH::NW>(&x[j * SH::EPV], out.w[j], SH::EPV);
+}
+
+// fp32 partial dot of this lane, then xor-butterfly over the L lanes of the
+// group.  Every lane of the warp must call it (full-warp shuffles).
+template <class SH>
+__device__ __forceinline__ float group_dot(const float (&p)[SH::E], const float (&q)[SH::E]) {
+    float s = 0.f;
+#pragma unroll
+    for (int e = 0; e < SH::E; e++) s = fmaf(p[e], q[e], s);
+#pragma unroll
+    for (int o = SH::L / 2; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    return s;
+}
+
+// p' = p + eta (err q - lambda p), q' = q + eta (err p - lambda q), snapshot semantics.
+template <class SH>
+__device__ __forceinline__ void sgd_step(float (&p)[SH::E], float (&q)[SH::E], float err, float eta, float lam) {
+#pragma unroll
+    for (int e = 0; e < SH::E; e++) {
+        const float pe = p[e], qe = q[e];
+        p[e] = pe + eta * (err * qe - lam * pe);
+        q[e] = qe + eta * (err * pe - lam * qe);
+    }
+}
+
+__device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
+    uint64_t z = x + 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+
+}  // namespace mf

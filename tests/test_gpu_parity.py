@@ -1,0 +1,251 @@
+"""GPU path (libmf.so through the C ABI) against the CPU oracle.  -m gpu.
+
+Tolerances (readings A-16 and §6): deterministic mode after one
+epoch, per matrix ||A_gpu - A_ref||_F / ||A_ref||_F <= 1e-5 (fp32), 2e-3
+(fp16), 1.6e-2 (bf16).  RMSE kernel: relative 1e-5 (fp32 dot vs the oracle's
+fp64 dot).  Every schedule's test RMSE after E epochs within 0.5% of the
+oracle's on the same shuffled order (north star).  Integer work (order,
+counts, init bits) is bit-exact.
+"""
+import numpy as np
+import pytest
+
+import datagen
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+TOL = {0: 1e-5, 1: 2e-3, 2: 1.6e-2}
+ORC = {0: oracle.F32, 1: oracle.F16, 2: oracle.BF16}
+
+
+def frob(a, b):
+    return float(np.linalg.norm(a.astype(np.float64) - b) / max(np.linalg.norm(b.astype(np.float64)), 1e-300))
+
+
+@pytest.fixture(scope="module")
+def mfmod():
+    from paper_1610_05838_b200 import mf
+    return mf
+
+
+def _gpu(mfmod, cfg, storage=0, **opts):
+    return mfmod.MF(cfg.m, cfg.n, cfg.k, cfg.alpha, cfg.lam, cfg.seed_init, storage=storage, beta=cfg.beta,
+                    seed_shuffle=cfg.seed_shuffle, **opts)
+
+
+@pytest.fixture(scope="module")
+def c1():
+    cfg = datagen.CONFIGS["C1"]
+    return cfg, datagen.make(cfg)
+
+
+# ------------------------------------------------------------ bit-exact setup
+@pytest.mark.parametrize("storage", [0, 1, 2])
+def test_init_bits_match_oracle(mfmod, storage):
+    m_, n_, k = 37, 23, 24
+    with mfmod.MF(m_, n_, k, 0.1, 0.0, 99, storage=storage) as g:
+        P, Q = g.factors()
+    Pr = oracle.widen(oracle.init(99, m_, k, 0, ORC[storage]), ORC[storage])
+    Qr = oracle.widen(oracle.init(99, n_, k, 1, ORC[storage]), ORC[storage])
+    np.testing.assert_array_equal(P, Pr)
+    np.testing.assert_array_equal(Q, Qr)
+
+
+def test_shuffle_order_matches_oracle(mfmod, c1):
+    cfg, ((u, v, r), _) = c1
+    with _gpu(mfmod, cfg) as g:
+        g.load(u, v, r)
+        np.testing.assert_array_equal(g.order(), oracle.shuffle_perm(cfg.seed_shuffle, len(u)))
+
+
+# ------------------------------------------------------ P-1 worked example --
+@pytest.mark.parametrize("storage", [0, 1])
+@pytest.mark.parametrize("schedule", ["deterministic", "hogwild", "wavefront"])
+def test_worked_example_exact_on_gpu(mfmod, storage, schedule):
+    """tests/golden/p1_worked_example.json: exact (dyadic) in fp32 and fp16 under any dot order."""
+    import json
+    import os
+    from fractions import Fraction as F
+    g = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "p1_worked_example.json")))
+    fl = lambda rows: np.array([[float(F(x)) for x in row] for row in rows], np.float32)  # noqa: E731
+    with mfmod.MF(4, 4, 2, 0.25, 0.5, 0, storage=storage, shuffle=0, workers=1, wave_rows=1, wave_cols=1) as m:
+        m.set_factors(fl(g["P0"]), fl(g["Q0"]))
+        u = np.array([s[0] for s in g["samples"]], np.int32)
+        v = np.array([s[1] for s in g["samples"]], np.int32)
+        r = np.array([float(F(s[2])) for s in g["samples"]], np.float32)
+        m.load(u, v, r)
+        m.epoch(schedule)
+        P, Q = m.factors()
+        np.testing.assert_array_equal(P, fl(g["P_final"]))
+        np.testing.assert_array_equal(Q, fl(g["Q_final"]))
+        tu = np.array([t[0] for t in g["test"]], np.int32)
+        tv = np.array([t[1] for t in g["test"]], np.int32)
+        assert m.rmse(tu, tv, np.ones(2, np.float32)) == pytest.approx(np.sqrt(1 / 8), rel=1e-12)
+
+
+# ------------------------------------------------------ deterministic mode --
+@pytest.mark.parametrize("storage", [0, 1, 2])
+def test_c1_deterministic_one_epoch(mfmod, c1, storage):
+    cfg, ((u, v, r), _) = c1
+    order = oracle.shuffle_perm(cfg.seed_shuffle, len(u))
+    ref = oracle.Model(cfg.m, cfg.n, cfg.k, ORC[storage], seed=cfg.seed_init)
+    assert ref.epoch(u, v, r, oracle.eta(cfg.alpha, cfg.beta, 0), cfg.lam, order) == 0
+    Pr, Qr = ref.factors_f32()
+    with _gpu(mfmod, cfg, storage) as g:
+        g.load(u, v, r)
+        g.epoch("deterministic")
+        P, Q = g.factors()
+    assert frob(P, Pr) <= TOL[storage] and frob(Q, Qr) <= TOL[storage], (frob(P, Pr), frob(Q, Qr))
+
+
+def test_c1_deterministic_bit_reproducible_and_multi_epoch(mfmod, c1):
+    cfg, ((u, v, r), (tu, tv, tr)) = c1
+    outs = []
+    for _ in range(2):
+        with _gpu(mfmod, cfg) as g:
+            g.load(u, v, r)
+            for _t in range(3):
+                g.epoch("deterministic")
+            outs.append(g.factors() + (g.rmse(tu, tv, tr),))
+    np.testing.assert_array_equal(outs[0][0], outs[1][0])
+    np.testing.assert_array_equal(outs[0][1], outs[1][1])
+    order = oracle.shuffle_perm(cfg.seed_shuffle, len(u))
+    ref, trace = oracle.train(cfg.m, cfg.n, cfg.k, oracle.F32, cfg.seed_init, u, v, r, cfg.alpha, cfg.beta,
+                              cfg.lam, 3, order=order, test=(tu, tv, tr))
+    assert frob(outs[0][0], ref.P) <= 3e-5 and frob(outs[0][1], ref.Q) <= 3e-5
+    assert outs[0][2] == pytest.approx(trace[-1], rel=1e-5)
+
+
+@pytest.mark.parametrize("k", [2, 7, 33, 64, 100, 128, 256])
+@pytest.mark.parametrize("storage", [0, 1])
+def test_deterministic_k_sweep_ragged(mfmod, k, storage):
+    """Generic (masked) and fast (vectorised) shapes; N not a multiple of 32 or 256."""
+    m_, n_, N = 301, 97, 12_345
+    u, v, r = datagen.planted_coo(21, m_, n_, 8, 0.1, N)
+    order = oracle.shuffle_perm(5, N)
+    ref = oracle.Model(m_, n_, k, ORC[storage], seed=13)
+    ref.epoch(u, v, r, 0.02, 0.03, order)
+    Pr, Qr = ref.factors_f32()
+    with mfmod.MF(m_, n_, k, 0.02, 0.03, 13, storage=storage, seed_shuffle=5) as g:
+        g.load(u, v, r)
+        g.epoch("deterministic")
+        P, Q = g.factors()
+    assert frob(P, Pr) <= TOL[storage] and frob(Q, Qr) <= TOL[storage], (frob(P, Pr), frob(Q, Qr))
+
+
+@pytest.mark.parametrize("storage", [0, 1])
+def test_netflix_slice_deterministic(mfmod, storage):
+    """C2-1pct (Netflix degrees, k=128): ~8k waves of ~120 samples; fast vectorised shape."""
+    cfg = datagen.CONFIGS["C2-1pct"]
+    (u, v, r), (tu, tv, tr) = datagen.make(cfg)
+    order = oracle.shuffle_perm(cfg.seed_shuffle, len(u))
+    ref = oracle.Model(cfg.m, cfg.n, cfg.k, ORC[storage], seed=cfg.seed_init)
+    ref.epoch(u, v, r, oracle.eta(cfg.alpha, cfg.beta, 0), cfg.lam, order)
+    Pr, Qr = ref.factors_f32()
+    with _gpu(mfmod, cfg, storage) as g:
+        g.load(u, v, r)
+        nw = mfmod.mf_wave_count(g.h)
+        _, nw_ref = oracle.waves(cfg.m, cfg.n, u, v, order)
+        assert nw == nw_ref
+        g.epoch("deterministic")
+        P, Q = g.factors()
+        rg = g.rmse(tu, tv, tr)
+    assert frob(P, Pr) <= TOL[storage] and frob(Q, Qr) <= TOL[storage], (frob(P, Pr), frob(Q, Qr))
+    assert rg == pytest.approx(ref.rmse(tu, tv, tr), rel=TOL[storage])
+
+
+# -------------------------------------------------------------------- RMSE --
+@pytest.mark.parametrize("storage", [0, 1, 2])
+def test_rmse_kernel_matches_oracle(mfmod, storage):
+    rng = np.random.default_rng(8)
+    m_, n_, k, N = 500, 300, 128, 100_003
+    P = rng.normal(size=(m_, k)).astype(np.float32) * 0.1
+    Q = rng.normal(size=(n_, k)).astype(np.float32) * 0.1
+    u = rng.integers(0, m_, N).astype(np.int32)
+    v = rng.integers(0, n_, N).astype(np.int32)
+    r = rng.normal(size=N).astype(np.float32)
+    with mfmod.MF(m_, n_, k, 0.1, 0.0, 1, storage=storage) as g:
+        g.set_factors(P, Q)
+        Pg, Qg = g.factors()
+        got = g.rmse(u, v, r)
+    ref = oracle.Model(m_, n_, k, oracle.F32, P=Pg, Q=Qg).rmse(u, v, r)
+    assert got == pytest.approx(ref, rel=1e-5)
+    if storage == 1:  # set_factors rounds RNE like the oracle's conversion
+        np.testing.assert_array_equal(Pg, P.astype(np.float16).astype(np.float32))
+
+
+# --------------------------------------------------------- batch-Hogwild! --
+@pytest.mark.parametrize("storage", [0, 1])
+def test_c1_hogwild_rmse_within_half_percent(mfmod, c1, storage):
+    cfg, ((u, v, r), test) = c1
+    order = oracle.shuffle_perm(cfg.seed_shuffle, len(u))
+    _, trace = oracle.train(cfg.m, cfg.n, cfg.k, ORC[storage], cfg.seed_init, u, v, r, cfg.alpha, cfg.beta,
+                            cfg.lam, cfg.epochs, order=order, test=test)
+    with _gpu(mfmod, cfg, storage, count_updates=1) as g:
+        g.load(u, v, r)
+        for _ in range(cfg.epochs):
+            st = g.epoch("hogwild")
+            assert st.updates == len(u)  # exactly once
+        got = g.rmse(*test)
+    assert abs(got - trace[-1]) <= 0.005 * trace[-1], (got, trace[-1])
+
+
+def test_netflix_slice_hogwild_many_workers(mfmod):
+    """C2-1pct, 10 epochs, explicit large worker count (c/n ~ 5): RMSE within 0.5% of serial."""
+    cfg = datagen.CONFIGS["C2-1pct"]
+    (u, v, r), test = datagen.make(cfg)
+    order = oracle.shuffle_perm(cfg.seed_shuffle, len(u))
+    E = 10
+    _, trace = oracle.train(cfg.m, cfg.n, cfg.k, oracle.F32, cfg.seed_init, u, v, r, cfg.alpha, cfg.beta, cfg.lam,
+                            E, order=order, test=test)
+    with _gpu(mfmod, cfg, count_updates=1) as g:
+        g.load(u, v, r)
+        for _ in range(E):
+            st = g.epoch("hogwild")
+            assert st.updates == len(u)
+        got = g.rmse(*test)
+    assert abs(got - trace[-1]) <= 0.005 * trace[-1], (got, trace[-1])
+
+
+# ------------------------------------------------------------- edge cases --
+def test_errors_and_divergence(mfmod):
+    mf = mfmod
+    with mf.MF(10, 8, 4, 0.1, 0.0, 1) as g:
+        with pytest.raises(mf.MFError) as e:
+            g.epoch("hogwild")
+        assert e.value.status == mf.MF_ESTATE
+        with pytest.raises(mf.MFError) as e:
+            g.load(np.array([0, 10], np.int32), np.array([0, 1], np.int32), np.ones(2, np.float32))
+        assert e.value.status == mf.MF_EINVAL
+        with pytest.raises(mf.MFError) as e:
+            g.load(np.array([0], np.int32), np.array([-1], np.int32), np.ones(1, np.float32))
+        assert e.value.status == mf.MF_EINVAL
+        with pytest.raises(mf.MFError) as e:
+            g.load(np.array([0], np.int32), np.array([0], np.int32), np.array([np.nan], np.float32))
+        assert e.value.status == mf.MF_EINVAL
+        with pytest.raises(mf.MFError) as e:
+            g.rmse(np.zeros(0, np.int32), np.zeros(0, np.int32), np.zeros(0, np.float32))
+        assert e.value.status == mf.MF_EINVAL
+        g.load(np.array([3], np.int32), np.array([2], np.int32), np.ones(1, np.float32))  # N = 1
+        g.set_factors(np.full((10, 4), 1e30, np.float32), np.full((8, 4), 1e30, np.float32))
+        for sched in ("hogwild", "deterministic"):
+            with pytest.raises(mf.MFError) as e:
+                g.epoch(sched)
+            assert e.value.status == mf.MF_EDIVERGED
+
+
+def test_device_pointers_accepted(mfmod, c1):
+    """Inputs already in HBM (torch CUDA tensors) give the same order and result as host arrays."""
+    import torch
+    cfg, ((u, v, r), test) = c1
+    outs = []
+    for dev in (False, True):
+        with _gpu(mfmod, cfg) as g:
+            if dev:
+                g.load(torch.from_numpy(u).cuda(), torch.from_numpy(v).cuda(), torch.from_numpy(r).cuda())
+            else:
+                g.load(u, v, r)
+            g.epoch("deterministic")
+            outs.append(g.factors())
+    np.testing.assert_array_equal(outs[0][0], outs[1][0])
