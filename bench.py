@@ -1,0 +1,299 @@
+"""Benchmark: SGD updates/s of the batch-Hogwild! epoch (PAPER.md:207 metric) on the Netflix-shaped
+synthetic workload (BASELINE.json configs[1]), k = 128, on one B200 (or G B200s, partitioned).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--storage f16|f32|bf16] [--config C2] [--schedule hogwild]
+
+One step = one epoch of the hot path over the whole training set (N = 99,072,112 updates) followed by
+the test-RMSE evaluation, both in libmf.so's kernels.  Prints ONE JSON line (rank 0).
+`value` is device-timed with inputs resident in HBM; `e2e` repeats the step through the public C ABI
+from pinned HOST buffers (mf_load_coo H2D + validation + A-8 shuffle, mf_epoch, mf_rmse, result D2H).
+`--impl reference` times the CPU oracle (the only reference this paper-only task has) on a bounded
+sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+import datagen  # noqa: E402
+
+HBM_FALLBACK_GBS = 6650.0  # B200_PROFILING.md fallback, used only if MEASURED_PEAKS.json is absent
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return HBM_FALLBACK_GBS, "fallback"
+
+
+def b_alg(k, storage):
+    """algorithmic bytes per update = 12 (triple) + 2kb (read p, q) + 2kb (write p, q)."""
+    b = 4 if storage == "f32" else 2
+    return 12 + 4 * k * b
+
+
+class Clocks:
+    """nvidia-smi sampler running during the timed region (B200_PROFILING.md clocks line)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index, self.rows, self.proc = index, [], None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        time.sleep(0.25)
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        time.sleep(0.15)
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        reasons = set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in self.rows:
+            for nm, val in zip(names, r[5:9]):
+                if val.lower().startswith("active"):
+                    reasons.add(nm)
+        loaded = sorted(sm)[len(sm) // 2:] if sm else []
+        return {"sm_mhz": statistics.median(loaded) if loaded else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(self.rows)}
+
+
+def load_traffic(storage, cfgname):
+    """ncu dram bytes per launch of the update kernel, from the committed profile summary (or None)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as f:
+            d = json.load(f)
+        return d["kernels"][f"{cfgname}/{storage}"]["dram_bytes_per_launch"]
+    except Exception:
+        return None
+
+
+# ----------------------------------------------------------------- reference
+def run_reference(a, cfg):
+    """The oracle as it stands (serial C++, 1 core) on a bounded sample of the same workload."""
+    import oracle
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    st = oracle.STORAGE_NAME[a.storage]
+    (u, v, r), test = datagen.make(cfg)
+    sample = a.ref_sample
+    m = oracle.Model(cfg.m, cfg.n, cfg.k, st, seed=cfg.seed_init)
+    eta = oracle.eta(cfg.alpha, cfg.beta, 0)
+    times = []
+    for i in range(a.warmup + a.steps):
+        lo = (i * sample) % (len(u) - sample)
+        t0 = time.perf_counter()
+        m.epoch(u[lo:lo + sample], v[lo:lo + sample], r[lo:lo + sample], eta, cfg.lam)
+        dt = time.perf_counter() - t0
+        if i >= a.warmup:
+            times.append(dt)
+    tot = sum(times)
+    val = a.steps * sample / tot
+    out = {"metric": "sgd_updates_per_sec", "value": val, "unit": "updates/s", "n_gpus": a.gpus,
+           "steps": a.steps, "warmup": a.warmup, "ms_per_step": 1e3 * tot / a.steps, "higher_is_better": True,
+           "scaling": "weak", "vs_baseline": None, "dtype": "f32", "storage": a.storage, "data": "synthetic",
+           "impl": "reference",
+           "config": {"workload": f"{cfg.name} (Netflix-shaped, Table 2) m={cfg.m} n={cfg.n} k={cfg.k}",
+                      "schedule": "serial", "sample_per_step": sample},
+           "cpu_baseline": {"value": val, "unit": "updates/s", "cores": 1, "kind": "oracle",
+                            "sample": f"{sample} consecutive shuffled samples of {cfg.name} per step, full-size P/Q"},
+           "e2e": {"value": val, "unit": "updates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+def cpu_baseline(cfg, storage, u, v, r, budget_s=12.0):
+    """Oracle updates/s on a bounded sample (full-size factors), 1 core."""
+    import oracle
+    st = oracle.STORAGE_NAME[storage]
+    m = oracle.Model(cfg.m, cfg.n, cfg.k, st, seed=cfg.seed_init)
+    eta = oracle.eta(cfg.alpha, cfg.beta, 0)
+    n, done, t_all = 100_000, 0, 0.0
+    while t_all < budget_s and done + n <= len(u):
+        t0 = time.perf_counter()
+        m.epoch(u[done:done + n], v[done:done + n], r[done:done + n], eta, cfg.lam)
+        t_all += time.perf_counter() - t0
+        done += n
+    return {"value": done / t_all, "unit": "updates/s", "cores": 1, "kind": "oracle",
+            "sample": f"first {done} samples of {cfg.name} in stored order, full-size P/Q, {storage} storage, "
+                      f"{t_all:.1f} s"}
+
+
+# ---------------------------------------------------------------------- ours
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--storage", default="f16", choices=["f16", "f32", "bf16"])
+    ap.add_argument("--config", default="C2")
+    ap.add_argument("--schedule", default="hogwild", choices=["hogwild", "wavefront", "deterministic"])
+    ap.add_argument("--workers", type=int, default=0)
+    ap.add_argument("--variant", type=int, default=-1)
+    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--ref-sample", type=int, default=1_000_000)
+    a = ap.parse_args()
+    a.warmup = max(a.warmup, 3)
+    cfg = datagen.CONFIGS[a.config]
+
+    if a.impl == "reference":
+        return run_reference(a, cfg)
+
+    import torch
+    import torch.distributed as dist
+    from paper_1610_05838_b200 import mf
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        return run_partitioned(a, cfg, rank, world, local)
+    torch.cuda.set_device(local)
+    stream = torch.cuda.current_stream()
+
+    (u, v, r), (tu, tv, tr) = datagen.make(cfg)
+    N = len(u)
+    variant = a.variant if a.variant >= 0 else (16 if a.storage != "f32" else 0)
+    g = mf.MF(cfg.m, cfg.n, cfg.k, cfg.alpha, cfg.lam, cfg.seed_init, storage=a.storage, beta=cfg.beta,
+              seed_shuffle=cfg.seed_shuffle, device=local, stream=stream.cuda_stream, variant=variant,
+              workers=a.workers)
+    # inputs resident in HBM (torch tensors as device memory), loaded through the C ABI
+    du, dv, dr = (torch.from_numpy(x).cuda() for x in (u, v, r))
+    dtu, dtv, dtr = (torch.from_numpy(x).cuda() for x in (tu, tv, tr))
+    g.load(du, dv, dr)
+
+    def step():
+        st = g.epoch(a.schedule)
+        rm = g.rmse(dtu, dtv, dtr)
+        return st, rm
+
+    for _ in range(a.warmup):
+        step()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    kern, launches, rmses, workers = [], 0, [], 0
+    with Clocks(local) as clk:
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for _ in range(a.steps):
+            st, rm = step()
+            kern.append(st.kernel_seconds)
+            launches += st.launches + 3  # + validate, rmse, final-sum kernels of mf_rmse
+            rmses.append(rm)
+            workers = st.workers
+        e1.record(stream)
+        torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / a.steps
+    value = N / (ms * 1e-3)
+
+    # roofline of the dominant kernel (the update kernel): algorithmic bytes / its event-timed duration
+    peak, peak_kind = peaks()
+    k_s = statistics.mean(kern)
+    B = b_alg(cfg.k, a.storage)
+    achieved = B * N / k_s / 1e9
+    traffic = load_traffic(a.storage, cfg.name)
+    roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+            "traffic": traffic, "peak_kind": peak_kind, "kernel": "k_hogwild" if a.schedule == "hogwild" else
+            "k_" + a.schedule, "kernel_ms": k_s * 1e3, "kernel_share_of_step": k_s * 1e3 / ms,
+            "bytes_per_update_alg": B, "updates_per_launch": N,
+            "note": "frac > 1 is possible: Q (n*k*b = %.1f MB) stays L2-resident, so HBM carries ~12+2kb B/update"
+                    % (cfg.n * cfg.k * (4 if a.storage == "f32" else 2) / 1e6)}
+    g.close()
+
+    # end to end through the public API from pinned host buffers
+    hu, hv, hr = (torch.from_numpy(x).pin_memory() for x in (u, v, r))
+    htu, htv, htr = (torch.from_numpy(x).pin_memory() for x in (tu, tv, tr))
+    ge = mf.MF(cfg.m, cfg.n, cfg.k, cfg.alpha, cfg.lam, cfg.seed_init, storage=a.storage, beta=cfg.beta,
+               seed_shuffle=cfg.seed_shuffle, device=local, stream=stream.cuda_stream, variant=variant,
+               workers=a.workers)
+
+    def e2e_step():
+        ge.load(hu, hv, hr)      # H2D + device validation + A-8 shuffle
+        ge.epoch(a.schedule)
+        return ge.rmse(htu, htv, htr)  # H2D of the test set, RMSE kernels, D2H of the result
+
+    e2e_step()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    e0.record(stream)
+    for _ in range(a.e2e_steps):
+        e2e_step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = e0.elapsed_time(e1) / a.e2e_steps
+    wall_ms = (time.perf_counter() - t0) * 1e3 / a.e2e_steps
+    ge.close()
+    h2d = 12 * N + 12 * len(tu)
+
+    cpu = None if a.no_cpu else cpu_baseline(cfg, a.storage, u, v, r)
+    out = {
+        "metric": "sgd_updates_per_sec", "value": value, "unit": "updates/s", "n_gpus": 1, "steps": a.steps,
+        "warmup": a.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f32", "storage": a.storage, "data": "synthetic",
+        "config": {"workload": f"{cfg.name}: Netflix-shaped (PAPER.md Table 2) m={cfg.m} n={cfg.n} "
+                               f"N={N} k={cfg.k}, planted rank-8 synthetic ratings",
+                   "schedule": a.schedule, "storage": a.storage, "workers": workers, "batch_f": 256,
+                   "alpha": cfg.alpha, "beta": cfg.beta, "lambda": cfg.lam,
+                   "l2": "inputs larger than L2 (R %.2f GB, P %.0f MB); no flush" % (12 * N / 1e9,
+                         cfg.m * cfg.k * (4 if a.storage == 'f32' else 2) / 1e6),
+                   "step": "mf_epoch (N updates) + mf_rmse (test set)"},
+        "test_rmse": rmses[-1],
+        "roofline": roof,
+        "cpu_baseline": cpu,
+        "e2e": {"value": N / (e2e_ms * 1e-3), "unit": "updates/s", "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": 8, "ms_per_step": e2e_ms, "wall_ms_per_step": wall_ms,
+                "includes": "H2D of R + test set from pinned host, validation, A-8 shuffle, epoch, RMSE"},
+        "gpu_launches": launches,
+        "clocks": clk.summary(),
+    }
+    print(json.dumps(out), flush=True)
+
+
+def run_partitioned(a, cfg, rank, world, local):
+    raise SystemExit("partitioned multi-GPU bench: see run_partitioned (not yet built)")
+
+
+if __name__ == "__main__":
+    main()

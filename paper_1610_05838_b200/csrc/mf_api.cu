@@ -505,7 +505,7 @@ extern "C" int mf_epoch(mf_ctx *ctx, int schedule, mf_epoch_stats *stats) {
     CK(cudaEventRecord(ctx->events[0], st));
     CK(cudaMemsetAsync(ctx->scratch, 0, sizeof(DevScratch), st));
     UpdateArgs a = ctx->update_args(eta);
-    int launches = 2, used = 0;
+    int launches = 1, used = 0;
     CK(cudaEventRecord(ctx->events[1], st));
     if (schedule == MF_SCHED_HOGWILD) {
         const int w = ctx->workers > 0 ? ctx->workers : ctx->auto_workers();
@@ -522,7 +522,7 @@ extern "C" int mf_epoch(mf_ctx *ctx, int schedule, mf_epoch_stats *stats) {
     } else {  // wavefront
         int l = 0;
         RC(ctx->run_wavefront(sh, a, &l, &used));
-        launches += l - 1;
+        launches = l;
     }
     CK(cudaEventRecord(ctx->events[2], st));
     return ctx->finish_epoch(schedule, eta, launches, used, stats);

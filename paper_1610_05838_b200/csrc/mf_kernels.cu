@@ -74,7 +74,12 @@ ShapeId select_shape(int k, int storage, int variant) {
         if (k == 64) return {storage, 8, 1, 16, 1};
         if (k == 256) return {storage, 32, 1, 16, 1};
     }
-    // generic: L = 32, VB = 4 bytes (or 2 for odd k with 16-bit storage), V vectors per lane
+    return select_generic_shape(k, storage);
+}
+
+// generic: L = 32, VB = 4 bytes (or 2 for odd k with 16-bit storage), V vectors per lane
+ShapeId select_generic_shape(int k, int storage) {
+    const int bytes = storage == kF32 ? 4 : 2;
     const int vb = (bytes == 2 && (k % 2)) ? 2 : 4;
     const int epv = vb / bytes;
     const int per_lane = (k + 32 * epv - 1) / (32 * epv);
@@ -98,7 +103,12 @@ __global__ void __launch_bounds__(kBlock) k_hogwild(UpdateArgs a) {
     const int k = SH::FULL ? SH::KMAX : a.k;
     const int64_t N = a.n;
     const int f = a.batch_f;
-    if ((int)((blockIdx.x * kBlock + threadIdx.x) >> 5) >= a.active_warps) return;  // warp-uniform
+    const int64_t warp_id = (blockIdx.x * kBlock + threadIdx.x) >> 5;
+    // exact worker count: groups beyond a.active_groups idle; a warp with no active group exits
+    const int64_t gleft = (int64_t)a.active_groups - warp_id * G;
+    if (gleft <= 0) return;  // warp-uniform
+    const int gper = gleft < G ? (int)gleft : G;  // active groups in this warp
+    const int ntile = (32 + gper - 1) / gper;     // samples per group per 32-sample tile
     unsigned long long done = 0;
     int bad = 0;
 
@@ -118,18 +128,18 @@ __global__ void __launch_bounds__(kBlock) k_hogwild(UpdateArgs a) {
             const int cnt = (int)(end - base < 32 ? end - base : 32);
             if (a.count_updates) done += (lane == 0) ? cnt : 0;
 #pragma unroll 1
-            for (int j0 = 0; j0 < 32 / G; j0 += D) {
+            for (int j0 = 0; j0 < ntile; j0 += D) {
                 int32_t su[D], sv[D];
                 float sr[D];
                 bool val[D];
                 RowRaw<SH> pr[D], qr[D];
 #pragma unroll
                 for (int d = 0; d < D; d++) {
-                    const int s = (j0 + d) * G + grp;
+                    const int s = (j0 + d) * gper + grp;
                     su[d] = __shfl_sync(0xffffffffu, tu, s);
                     sv[d] = __shfl_sync(0xffffffffu, tv, s);
                     sr[d] = __shfl_sync(0xffffffffu, tr, s);
-                    val[d] = s < cnt;
+                    val[d] = grp < gper && s < cnt;
                 }
 #pragma unroll
                 for (int d = 0; d < D; d++) {
@@ -163,15 +173,16 @@ static cudaError_t hogwild_launch(const UpdateArgs &a, int workers, cudaStream_t
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_hogwild<SH, D>, kBlock, 0);
     if (per_sm < 1) per_sm = 1;
-    const int slots_per_warp = SH::G * D;
-    int64_t warps = (int64_t)sms * per_sm * kWarpsPerBlock;
-    if (workers > 0) warps = std::min<int64_t>(warps, (workers + slots_per_warp - 1) / slots_per_warp);
+    // workers = concurrent ratings = active groups x D
+    int64_t groups = (int64_t)sms * per_sm * kWarpsPerBlock * SH::G;
+    if (workers > 0) groups = std::min<int64_t>(groups, (workers + D - 1) / D);
     const int64_t chunks = (a.n + a.batch_f - 1) / a.batch_f;
-    warps = std::max<int64_t>(1, std::min<int64_t>(warps, chunks));
+    groups = std::max<int64_t>(1, std::min<int64_t>(groups, chunks * SH::G));
+    const int64_t warps = (groups + SH::G - 1) / SH::G;
     const int blocks = (int)((warps + kWarpsPerBlock - 1) / kWarpsPerBlock);
-    if (used) *used = (int)(warps * slots_per_warp);
+    if (used) *used = (int)(groups * D);
     UpdateArgs args = a;
-    args.active_warps = (int)warps;
+    args.active_groups = groups;
     k_hogwild<SH, D><<<blocks, kBlock, 0, st>>>(args);
     return cudaGetLastError();
 }
@@ -183,6 +194,7 @@ cudaError_t launch_hogwild(const ShapeId &sh, const UpdateArgs &a, int workers, 
         using SH = decltype(tag);
         constexpr int L = SH::L;
         if constexpr (SH::FULL) {
+            if (workers > 0 && workers < 64) return hogwild_launch<SH, 1>(a, workers, st, workers_used);
             if (D == 4 && L % 4 == 0) return hogwild_launch<SH, (L % 4 == 0 ? 4 : 1)>(a, workers, st, workers_used);
             if (D != 1 && L % 2 == 0) return hogwild_launch<SH, (L % 2 == 0 ? 2 : 1)>(a, workers, st, workers_used);
         }

@@ -35,7 +35,7 @@ struct UpdateArgs {
     DevScratch *scratch;
     const int64_t *wave_off;  // deterministic: wave offsets (nwaves + 1)
     int64_t nwaves;
-    int active_warps;   // batch-Hogwild!: warps beyond this exit at once (exact worker count)
+    int64_t active_groups;  // batch-Hogwild!: groups beyond this idle (exact worker count)
 };
 
 // Kernel-shape choice for (k, storage); filled by select_shape().
@@ -65,6 +65,7 @@ cudaError_t launch_gather(const int32_t *u_in, const int32_t *v_in, const float 
                           int32_t *u_out, int32_t *v_out, float *r_out, cudaStream_t st);
 
 ShapeId select_shape(int k, int storage, int variant);
+ShapeId select_generic_shape(int k, int storage);
 int rmse_parts();
 
 }  // namespace mf

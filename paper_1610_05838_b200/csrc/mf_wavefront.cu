@@ -1,13 +1,369 @@
-// mf_wavefront.cu -- wavefront-update schedule (§3.2.3).  [stub: filled in next]
-#include "mf_ctx.h"
+// mf_wavefront.cu -- wavefront-update schedule (§3.2.3, Fig. 8).
+//
+// R is bucketed into an s x c grid of blocks: s equal-width row bands (one per
+// worker) and c equal-width column groups, remainder to the last band/group
+// (SPEC.md:319).  The bucketing is a stable radix sort by block id, so each
+// block keeps the shuffled order.  Worker w (one warp) walks
+// its column sequence pi_w[0..c): for wave j it acquires the lock of column
+// pi_w[j] in the 1-D column lock array, processes block
+// (w, pi_w[j]) serially, and releases the lock (release-before-acquire, no
+// hold-and-wait: DESIGN.md A-9).  Default sequences are a randomized Latin
+// rectangle pi_w[j] = sigma((rho(w) + j) mod c), re-drawn per epoch; option
+// MF_OPT_WAVE_PERM=1 gives every worker an independent random permutation,
+// the paper's literal reading.
+//
+// Inside a block a worker keeps D samples in flight: rows of sample i+D are
+// loaded while sample i is computed, and a row written by one of the D
+// previous samples is forwarded from registers, so a block is still processed
+// exactly serially.  Lock acquire/release use gpu-scope atomics with fences;
+// P/Q loads are ld.global.cg (coherent at L2).
+#include <cub/device/device_radix_sort.cuh>
 
-int mf_ctx::build_wavefront() { return fail(MF_EINVAL, "wavefront schedule not built yet"); }
-int mf_ctx::run_wavefront(const mf::ShapeId &, const mf::UpdateArgs &, int *, int *) {
-    return fail(MF_EINVAL, "wavefront schedule not built yet");
+#include <algorithm>
+#include <cmath>
+#include <numeric>
+#include <vector>
+
+#include "mf_ctx.h"
+#include "sgd_core.cuh"
+
+using namespace mf;
+
+namespace {
+
+constexpr int kBlock = 256;
+
+uint64_t host_mix(uint64_t x) {
+    uint64_t z = x + 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
 }
-void mf_ctx::release_wavefront() {}
-extern "C" int mf_wavefront_trace(mf_ctx *ctx, int64_t *, int64_t, int64_t *count) {
-    if (!ctx || !count) return MF_EINVAL;
+
+// Fisher-Yates permutation of [0, n) driven by a counter hash stream
+void permutation(std::vector<int32_t> &out, int n, uint64_t key) {
+    out.resize(n);
+    std::iota(out.begin(), out.end(), 0);
+    for (int i = n - 1; i > 0; i--) {
+        const uint64_t h = host_mix(key ^ (uint64_t)i * 0xD1B54A32D192ED03ull);
+        const int j = (int)(h % (uint64_t)(i + 1));
+        std::swap(out[i], out[j]);
+    }
+}
+
+__global__ void k_block_keys(const int32_t *u, const int32_t *v, int64_t n, int64_t band_w, int64_t grp_w, int s,
+                             int c, uint32_t *keys, uint32_t *idx) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        int64_t b = u[i] / band_w, g = v[i] / grp_w;
+        b = b < s - 1 ? b : s - 1;
+        g = g < c - 1 ? g : c - 1;
+        keys[i] = (uint32_t)(b * c + g);
+        idx[i] = (uint32_t)i;
+    }
+}
+
+// offsets[b] = first sorted position with key >= b, for b in [0, nb]
+__global__ void k_block_offsets(const uint32_t *sorted_keys, int64_t n, int64_t nb, int64_t *off) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i <= n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t prev = i == 0 ? -1 : (int64_t)sorted_keys[i - 1];
+        const int64_t cur = i == n ? nb : (int64_t)sorted_keys[i];
+        for (int64_t b = prev + 1; b <= cur; b++) off[b] = i;
+    }
+}
+
+struct WfArgs {
+    const int32_t *u, *v;
+    const float *r;
+    const int64_t *off;   // s*c + 1
+    const int32_t *seq;   // latin: sigma[c] then rho[s]; random: s*c table
+    int32_t *locks;       // c
+    void *P, *Q;
+    int64_t *trace;       // optional, 4 per block
+    DevScratch *scratch;
+    int s, c, k, latin, count_updates;
+    float eta, lam;
+};
+
+__device__ __forceinline__ int64_t globaltimer() {
+    int64_t t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+
+template <class SH, int D>
+__global__ void __launch_bounds__(kBlock) k_wavefront(WfArgs a) {
+    static_assert(SH::L == 32, "wavefront worker is a full warp");
+    const int lane = threadIdx.x & 31;
+    const int w = (blockIdx.x * kBlock + threadIdx.x) >> 5;
+    if (w >= a.s) return;
+    const int k = SH::FULL ? SH::KMAX : a.k;
+    const int c = a.c;
+    int bad = 0;
+    unsigned long long done = 0;
+    for (int j = 0; j < c; j++) {
+        const int col = a.latin ? a.seq[(a.seq[c + w] + j) % c] : a.seq[(int64_t)w * c + j];
+        int32_t *lock = a.locks + col;
+        if (lane == 0)
+            while (atomicCAS(lock, 0, 1) != 0) __nanosleep(64);
+        __syncwarp();
+        __threadfence();  // acquire: the previous holder's stores are visible (loads are .cg)
+        const int64_t t0 = a.trace ? globaltimer() : 0;
+        const int64_t blk = (int64_t)w * c + col;
+        const int64_t lo = a.off[blk], hi = a.off[blk + 1];
+        done += (uint64_t)(hi - lo);
+
+        // ring of D prefetched samples, history of the D last written rows
+        int32_t ru[D], rv[D];
+        float rr[D];
+        RowRaw<SH> rp[D], rq[D];
+        int32_t hu[D], hv[D];
+        RowRaw<SH> hp[D], hq[D];
+#pragma unroll
+        for (int d = 0; d < D; d++) {
+            hu[d] = -1;
+            hv[d] = -1;
+            const int64_t i = lo + d;
+            const bool ok = i < hi;
+            ru[d] = ok ? __ldg(a.u + i) : 0;
+            rv[d] = ok ? __ldg(a.v + i) : 0;
+            rr[d] = ok ? __ldg(a.r + i) : 0.f;
+            load_row<SH>(a.P, ru[d], k, lane, ok, rp[d]);
+            load_row<SH>(a.Q, rv[d], k, lane, ok, rq[d]);
+        }
+        for (int64_t base = lo; base < hi; base += D) {
+#pragma unroll
+            for (int d = 0; d < D; d++) {
+                const int64_t i = base + d;
+                if (i < hi) {  // warp-uniform
+                    RowRaw<SH> pr = rp[d], qr = rq[d];
+                    // forward rows written since this sample's loads were issued (oldest first)
+#pragma unroll
+                    for (int t = 0; t < D; t++) {
+                        const int h = (d + t) % D;
+                        if (hu[h] == ru[d]) pr = hp[h];
+                        if (hv[h] == rv[d]) qr = hq[h];
+                    }
+                    float p[SH::E], q[SH::E];
+                    widen_row<SH>(pr, p);
+                    widen_row<SH>(qr, q);
+                    const float err = rr[d] - group_dot<SH>(p, q);
+                    if (!isfinite(err)) bad = 1;
+                    sgd_step<SH>(p, q, err, a.eta, a.lam);
+                    narrow_row<SH>(p, pr);
+                    narrow_row<SH>(q, qr);
+                    store_row<SH>(a.P, ru[d], k, lane, true, pr);
+                    store_row<SH>(a.Q, rv[d], k, lane, true, qr);
+                    hu[d] = ru[d];
+                    hv[d] = rv[d];
+                    hp[d] = pr;
+                    hq[d] = qr;
+                    // refill this slot with sample i + D
+                    const int64_t nx = i + D;
+                    const bool ok = nx < hi;
+                    ru[d] = ok ? __ldg(a.u + nx) : 0;
+                    rv[d] = ok ? __ldg(a.v + nx) : 0;
+                    rr[d] = ok ? __ldg(a.r + nx) : 0.f;
+                    load_row<SH>(a.P, ru[d], k, lane, ok, rp[d]);
+                    load_row<SH>(a.Q, rv[d], k, lane, ok, rq[d]);
+                }
+            }
+        }
+        if (a.trace && lane == 0) {
+            int64_t *tr = a.trace + 4 * blk;
+            tr[0] = w;
+            tr[1] = blk;
+            tr[2] = t0;
+            tr[3] = globaltimer();
+        }
+        __threadfence();  // release: every lane's stores of this block before the unlock
+        __syncwarp();
+        if (lane == 0) atomicExch(lock, 0);
+    }
+    if (bad && lane == 0) a.scratch->diverged = 1;
+    if (a.count_updates && lane == 0 && done) atomicAdd(&a.scratch->updates, done);
+}
+
+ShapeId warp_shape(int k, int storage) {
+    if (storage == kF32) {
+        if (k == 128) return {storage, 32, 1, 16, 1};
+        if (k == 256) return {storage, 32, 2, 16, 1};
+    } else {
+        if (k == 128) return {storage, 32, 1, 8, 1};
+        if (k == 256) return {storage, 32, 1, 16, 1};
+    }
+    return select_generic_shape(k, storage);  // L = 32, masked
+}
+
+template <class F>
+cudaError_t dispatch_warp_shape(const ShapeId &s, F &&f) {
+#define MF_WCASE(S_, V_, VB_, FULL_)                                                               \
+    if (s.storage == S_ && s.L == 32 && s.V == V_ && s.VB == VB_ && s.full == FULL_)              \
+        return f(Shape<S_, 32, V_, VB_, (bool)FULL_>{});
+    MF_WCASE(kF32, 1, 16, 1) MF_WCASE(kF32, 2, 16, 1) MF_WCASE(kF16, 1, 8, 1) MF_WCASE(kF16, 1, 16, 1)
+    MF_WCASE(kBF16, 1, 8, 1) MF_WCASE(kBF16, 1, 16, 1)
+    MF_WCASE(kF32, 1, 4, 0) MF_WCASE(kF32, 4, 4, 0) MF_WCASE(kF32, 16, 4, 0) MF_WCASE(kF32, 32, 4, 0)
+    MF_WCASE(kF16, 1, 4, 0) MF_WCASE(kF16, 4, 4, 0) MF_WCASE(kF16, 16, 4, 0)
+    MF_WCASE(kF16, 1, 2, 0) MF_WCASE(kF16, 4, 2, 0) MF_WCASE(kF16, 16, 2, 0) MF_WCASE(kF16, 32, 2, 0)
+    MF_WCASE(kBF16, 1, 4, 0) MF_WCASE(kBF16, 4, 4, 0) MF_WCASE(kBF16, 16, 4, 0)
+    MF_WCASE(kBF16, 1, 2, 0) MF_WCASE(kBF16, 4, 2, 0) MF_WCASE(kBF16, 16, 2, 0) MF_WCASE(kBF16, 32, 2, 0)
+#undef MF_WCASE
+    return cudaErrorInvalidValue;
+}
+
+}  // namespace
+
+#define CK(expr)                                   \
+    do {                                           \
+        int _rc = cuda((expr), #expr);             \
+        if (_rc != MF_OK) return _rc;              \
+    } while (0)
+
+void mf_ctx::release_wavefront() {
+    for (void *p : {(void *)fu, (void *)fv, (void *)fr, (void *)wf_off, (void *)wf_locks, (void *)wf_seq,
+                    (void *)wf_trace})
+        if (p) cudaFree(p);
+    fu = fv = nullptr;
+    fr = nullptr;
+    wf_off = nullptr;
+    wf_locks = wf_seq = nullptr;
+    wf_trace = nullptr;
+    wf_trace_n = 0;
+    wf_valid = false;
+}
+
+// Auto sizing: ~8 workers per SM, c = 2s column blocks, but
+// keep >= ~100 samples per block and s <= m, c <= n.
+int mf_ctx::build_wavefront() {
+    if (wf_valid) return MF_OK;
+    release_wavefront();
+    const int64_t rows = p_rows();
+    int s = wave_rows, c = wave_cols;
+    if (s <= 0) {
+        const double by_blocks = std::sqrt((double)N / 200.0);
+        s = (int)std::max<double>(1.0, std::min<double>({(double)num_sms * 8, by_blocks, (double)rows}));
+    }
+    if (c <= 0) c = (int)std::min<int64_t>(2 * (int64_t)s, n);
+    if (s > rows || c > n || s < 1 || c < s)
+        return fail(MF_EINVAL, "wavefront needs 1 <= s <= c, s <= m, c <= n (s=%d c=%d)", s, c);
+    if ((int64_t)s * c >= (1ll << 32)) return fail(MF_EINVAL, "wavefront grid s*c too large");
+    cudaStream_t st = stream();
+    const int64_t nb = (int64_t)s * c;
+    uint32_t *k0 = nullptr, *k1 = nullptr, *i0 = nullptr, *i1 = nullptr;
+    void *tmp = nullptr;
+    size_t tmp_bytes = 0;
+    CK(cudaMalloc((void **)&fu, sizeof(int32_t) * N));
+    CK(cudaMalloc((void **)&fv, sizeof(int32_t) * N));
+    CK(cudaMalloc((void **)&fr, sizeof(float) * N));
+    CK(cudaMalloc((void **)&wf_off, sizeof(int64_t) * (nb + 1)));
+    CK(cudaMalloc((void **)&wf_locks, sizeof(int32_t) * c));
+    CK(cudaMallocAsync((void **)&k0, sizeof(uint32_t) * N, st));
+    CK(cudaMallocAsync((void **)&k1, sizeof(uint32_t) * N, st));
+    CK(cudaMallocAsync((void **)&i0, sizeof(uint32_t) * N, st));
+    CK(cudaMallocAsync((void **)&i1, sizeof(uint32_t) * N, st));
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((N + 255) / 256, 148 * 16));
+    k_block_keys<<<grid, 256, 0, st>>>(u, v, N, std::max<int64_t>(1, rows / s), std::max<int64_t>(1, n / c), s, c, k0,
+                                       i0);
+    CK(cudaGetLastError());
+    int bits = 1;
+    while (bits < 32 && (1ull << bits) < (uint64_t)nb) bits++;
+    CK(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, k0, k1, i0, i1, N, 0, bits, st));
+    CK(cudaMallocAsync(&tmp, tmp_bytes, st));
+    CK(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, k0, k1, i0, i1, N, 0, bits, st));  // stable
+    k_block_offsets<<<grid, 256, 0, st>>>(k1, N, nb, wf_off);
+    CK(cudaGetLastError());
+    CK(launch_gather(u, v, r, i1, N, fu, fv, fr, st));
+    CK(cudaFreeAsync(tmp, st));
+    CK(cudaFreeAsync(k0, st));
+    CK(cudaFreeAsync(k1, st));
+    CK(cudaFreeAsync(i0, st));
+    CK(cudaFreeAsync(i1, st));
+    CK(cudaMemsetAsync(wf_locks, 0, sizeof(int32_t) * c, st));
+    CK(cudaStreamSynchronize(st));
+    wf_s = s;
+    wf_c = c;
+    wf_valid = true;
+    return MF_OK;
+}
+
+int mf_ctx::run_wavefront(const ShapeId &, const UpdateArgs &ua, int *launches, int *workers_used) {
+    cudaStream_t st = stream();
+    const int s = wf_s, c = wf_c;
+    // column sequences for this epoch (host, counter-hash Fisher-Yates keyed by seed and epoch)
+    const uint64_t key = host_mix(seed_shuffle ^ 0x5eedull ^ ((uint64_t)epoch << 32));
+    std::vector<int32_t> seq;
+    if (wave_perm == 0) {
+        std::vector<int32_t> sigma, rho;
+        permutation(sigma, c, key);
+        permutation(rho, c, host_mix(key + 1));
+        seq = sigma;
+        seq.insert(seq.end(), rho.begin(), rho.begin() + s);
+    } else {
+        seq.resize((size_t)s * c);
+        std::vector<int32_t> pw;
+        for (int w = 0; w < s; w++) {
+            permutation(pw, c, host_mix(key + 2 + (uint64_t)w));
+            std::copy(pw.begin(), pw.end(), seq.begin() + (size_t)w * c);
+        }
+    }
+    if (wf_seq) cudaFree(wf_seq);
+    wf_seq = nullptr;
+    CK(cudaMalloc((void **)&wf_seq, sizeof(int32_t) * seq.size()));
+    CK(cudaMemcpyAsync(wf_seq, seq.data(), sizeof(int32_t) * seq.size(), cudaMemcpyHostToDevice, st));
+    const int64_t nb = (int64_t)s * c;
+    if (trace) {
+        if (wf_trace_n != nb) {
+            if (wf_trace) cudaFree(wf_trace);
+            wf_trace = nullptr;
+            CK(cudaMalloc((void **)&wf_trace, sizeof(int64_t) * 4 * nb));
+            wf_trace_n = nb;
+        }
+        CK(cudaMemsetAsync(wf_trace, 0xFF, sizeof(int64_t) * 4 * nb, st));
+    }
+    WfArgs a{};
+    a.u = fu;
+    a.v = fv;
+    a.r = fr;
+    a.off = wf_off;
+    a.seq = wf_seq;
+    a.locks = wf_locks;
+    a.P = P;
+    a.Q = Q;
+    a.trace = trace ? wf_trace : nullptr;
+    a.scratch = scratch;
+    a.s = s;
+    a.c = c;
+    a.k = k;
+    a.latin = wave_perm == 0;
+    a.count_updates = count_updates;
+    a.eta = ua.eta;
+    a.lam = ua.lam;
+    const ShapeId sh = warp_shape(k, storage);
+    const int blocks = (s * 32 + kBlock - 1) / kBlock;
+    CK(dispatch_warp_shape(sh, [&](auto tag) -> cudaError_t {
+        using SH = decltype(tag);
+        k_wavefront<SH, 2><<<blocks, kBlock, 0, st>>>(a);
+        return cudaGetLastError();
+    }));
+    *launches = 1;
+    *workers_used = s;
+    return MF_OK;
+}
+
+extern "C" int mf_wavefront_trace(mf_ctx *ctx, int64_t *records, int64_t cap, int64_t *count) {
+    if (!ctx || !count || (cap > 0 && !records)) return MF_EINVAL;
     *count = 0;
+    if (!ctx->wf_trace || ctx->wf_trace_n == 0) return MF_OK;
+    const int64_t nrec = std::min<int64_t>(cap, ctx->wf_trace_n);
+    std::vector<int64_t> h((size_t)(4 * ctx->wf_trace_n));
+    int rc = ctx->cuda(cudaMemcpy(h.data(), ctx->wf_trace, sizeof(int64_t) * h.size(), cudaMemcpyDeviceToHost),
+                       "trace copy");
+    if (rc != MF_OK) return rc;
+    int64_t o = 0;
+    for (int64_t b = 0; b < ctx->wf_trace_n && o < nrec; b++) {
+        if (h[(size_t)(4 * b)] < 0) continue;  // block not visited (never happens after a full epoch)
+        std::copy(h.begin() + 4 * b, h.begin() + 4 * b + 4, records + 4 * o);
+        o++;
+    }
+    *count = o;
     return MF_OK;
 }

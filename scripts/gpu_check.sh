@@ -1,0 +1,22 @@
+#!/bin/bash
+# One GPU round trip: smoke, gpu tests, bench, launch list, ncu capture of the update kernel.
+set -x
+mkdir -p gpurun_out
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,clocks.mem --format=csv > gpurun_out/gpu.txt
+python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1
+timeout ${TEST_TIMEOUT:-1200} python -m pytest tests -m gpu -q ${PYTEST_ARGS} > gpurun_out/pytest_gpu.log 2>&1
+tail -5 gpurun_out/pytest_gpu.log
+if [ -n "$BENCH" ]; then
+  timeout 600 python bench.py > gpurun_out/bench_f16.json 2> gpurun_out/bench_f16.err
+  timeout 600 python bench.py --storage f32 --no-cpu > gpurun_out/bench_f32.json 2> gpurun_out/bench_f32.err
+  cat gpurun_out/bench_f16.json gpurun_out/bench_f32.json
+fi
+if [ -n "$NCU" ]; then
+  timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
+     --log-file gpurun_out/launches.csv python bench.py --steps 3 --warmup 3 --no-cpu --e2e-steps 1 > gpurun_out/ncu_bench.log 2>&1
+  for st in f16 f32; do
+    timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_hogwild -s 4 -c 1 \
+       -o gpurun_out/prof_hogwild_$st -f python bench.py --storage $st --steps 1 --warmup 3 --no-cpu --e2e-steps 1 > gpurun_out/ncu_full_$st.log 2>&1
+  done
+fi
+ls gpurun_out

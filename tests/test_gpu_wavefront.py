@@ -1,0 +1,99 @@
+"""Wavefront-update schedule on the GPU.  -m gpu.
+
+Checks: exactly-once, the conflict audit (no two blocks of one
+column processed at overlapping times, SPEC.md:297-305 / S:555), every block
+visited once per epoch, and test RMSE within 0.5% of the serial
+oracle on the same shuffled order (north star).
+"""
+import numpy as np
+import pytest
+
+import datagen
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def mfmod():
+    from paper_1610_05838_b200 import mf
+    return mf
+
+
+def _audit(rec, s, c):
+    """rec rows: (worker, block, t_start, t_end). Returns number of column conflicts."""
+    assert len(rec) == s * c
+    blocks = rec[:, 1]
+    assert np.array_equal(np.sort(blocks), np.arange(s * c))  # each block exactly once
+    assert np.array_equal(rec[:, 0], blocks // c)             # block (w, col) done by worker w
+    conflicts = 0
+    col = blocks % c
+    for cc in range(c):
+        iv = rec[col == cc][:, 2:4]
+        iv = iv[np.argsort(iv[:, 0])]
+        conflicts += int(np.sum(iv[1:, 0] < iv[:-1, 1]))
+    return conflicts
+
+
+@pytest.mark.parametrize("perm", [0, 1])
+def test_wavefront_exactly_once_and_conflict_free(mfmod, perm):
+    cfg = datagen.CONFIGS["C1"]
+    (u, v, r), _ = datagen.make(cfg)
+    s, c = 8, 16
+    with mfmod.MF(cfg.m, cfg.n, cfg.k, cfg.alpha, cfg.lam, cfg.seed_init, beta=cfg.beta, wave_rows=s,
+                  wave_cols=c, wave_perm=perm, trace=1, count_updates=1) as g:
+        g.load(u, v, r)
+        for _ in range(3):
+            st = g.epoch("wavefront")
+            assert st.updates == len(u)
+            assert st.workers == s
+            rec = mfmod.mf_wavefront_trace(g.h, s * c + 10)
+            assert _audit(rec, s, c) == 0
+
+
+def test_wavefront_audit_at_scale(mfmod):
+    """Auto-sized grid (~8 workers/SM) on a Yahoo-shaped slice: still conflict-free."""
+    cfg = datagen.CONFIGS["C3-1pct"]
+    (u, v, r), _ = datagen.make(cfg)
+    with mfmod.MF(cfg.m, cfg.n, cfg.k, cfg.alpha, cfg.lam, cfg.seed_init, beta=cfg.beta, trace=1,
+                  count_updates=1) as g:
+        g.load(u, v, r)
+        st = g.epoch("wavefront")
+        assert st.updates == len(u)
+        s = st.workers
+        c = int(g.get(mfmod.MF_OPT_WAVE_COLS)) or 2 * s
+        rec = mfmod.mf_wavefront_trace(g.h, 10 ** 8)
+        assert _audit(rec, s, c) == 0
+
+
+@pytest.mark.parametrize("name,s,c,epochs", [("C1", 8, 16, 20), ("C3-1pct", 0, 0, 10)])
+def test_wavefront_rmse_within_half_percent(mfmod, name, s, c, epochs):
+    cfg = datagen.CONFIGS[name]
+    (u, v, r), test = datagen.make(cfg)
+    order = oracle.shuffle_perm(cfg.seed_shuffle, len(u))
+    _, trace = oracle.train(cfg.m, cfg.n, cfg.k, oracle.F32, cfg.seed_init, u, v, r, cfg.alpha, cfg.beta,
+                            cfg.lam, epochs, order=order, test=test)
+    with mfmod.MF(cfg.m, cfg.n, cfg.k, cfg.alpha, cfg.lam, cfg.seed_init, beta=cfg.beta, wave_rows=s,
+                  wave_cols=c, seed_shuffle=cfg.seed_shuffle) as g:
+        g.load(u, v, r)
+        for _ in range(epochs):
+            g.epoch("wavefront")
+        got = g.rmse(*test)
+    assert abs(got - trace[-1]) <= 0.005 * trace[-1], (got, trace[-1])
+
+
+def test_wavefront_single_worker_is_serial_block_order(mfmod):
+    """s = 1 worker: the epoch is serial SGD over the blocks in pi_0 order; with c = 1 it is exactly
+    serial SGD on the shuffled order (compare with the oracle, fp32 Frobenius 1e-5)."""
+    cfg = datagen.CONFIGS["C1"]
+    (u, v, r), _ = datagen.make(cfg)
+    order = oracle.shuffle_perm(cfg.seed_shuffle, len(u))
+    ref = oracle.Model(cfg.m, cfg.n, cfg.k, oracle.F32, seed=cfg.seed_init)
+    ref.epoch(u, v, r, oracle.eta(cfg.alpha, cfg.beta, 0), cfg.lam, order)
+    with mfmod.MF(cfg.m, cfg.n, cfg.k, cfg.alpha, cfg.lam, cfg.seed_init, beta=cfg.beta, wave_rows=1,
+                  wave_cols=1, seed_shuffle=cfg.seed_shuffle) as g:
+        g.load(u, v, r)
+        g.epoch("wavefront")
+        P, Q = g.factors()
+    assert np.linalg.norm(P - ref.P) / np.linalg.norm(ref.P) <= 1e-5
+    assert np.linalg.norm(Q - ref.Q) / np.linalg.norm(ref.Q) <= 1e-5
