@@ -1,0 +1,46 @@
+"""Write oracle golden traces (test RMSE per epoch) for full-size parity configs.
+
+Calls only oracle/ (and the shared input generator datagen/).  Output:
+tests/golden/<cfg>_<storage>_trace.json.  Usage:
+    python scripts/make_golden.py C2 f32 [epochs]
+The serial oracle runs at ~0.76 M updates/s (fp32) on one core, so C2 (99M samples) takes ~2 min
+per epoch; run it in the background on the dev container.
+"""
+import json
+import os
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import datagen  # noqa: E402
+import oracle  # noqa: E402
+
+
+def main():
+    name, storage = sys.argv[1], sys.argv[2]
+    cfg = datagen.CONFIGS[name]
+    epochs = int(sys.argv[3]) if len(sys.argv) > 3 else cfg.epochs
+    st = oracle.STORAGE_NAME[storage]
+    (u, v, r), test = datagen.make(cfg)
+    order = oracle.shuffle_perm(cfg.seed_shuffle, len(u))
+    m = oracle.Model(cfg.m, cfg.n, cfg.k, st, seed=cfg.seed_init)
+    out = os.path.join(ROOT, "tests", "golden", f"{name}_{storage}_trace.json")
+    rec = {"what": f"oracle test RMSE per epoch, serial SGD on the A-8 shuffled order (seed {cfg.seed_shuffle}), "
+                   f"init A-7 (seed {cfg.seed_init}), {storage} storage",
+           "written_by": "scripts/make_golden.py (calls only oracle/ and datagen/)",
+           "config": cfg.__dict__, "rmse": [], "seconds": []}
+    for t in range(epochs):
+        t0 = time.time()
+        rc = m.epoch(u, v, r, oracle.eta(cfg.alpha, cfg.beta, t), cfg.lam, order)
+        assert rc == 0, "oracle diverged"
+        rec["rmse"].append(m.rmse(*test))
+        rec["seconds"].append(time.time() - t0)
+        with open(out, "w") as f:
+            json.dump(rec, f, indent=1)
+        print(t, rec["rmse"][-1], rec["seconds"][-1], flush=True)
+
+
+if __name__ == "__main__":
+    main()
