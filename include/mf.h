@@ -135,9 +135,15 @@ int mf_attach_nccl(mf_ctx *ctx, const void *id128, int rank, int world);
 
 /* Host-only helpers of the partitioned schedule (no device needed):
  * row segment of rank g among G: [seg_begin, seg_end) = [floor(g*m/G), floor((g+1)*m/G));
- * column segment held by rank g in round r of epoch e (a Latin square). */
+ * column segment held by rank g in round r of epoch e: sigma_e(g, r) = pi_e((g + r) mod G), pi_e a
+ * per-epoch permutation drawn from `seed` (the context's shuffle seed) -- a Latin square, so the
+ * blocks of one round share no row or column segment. */
 int mf_segment(int64_t extent, int32_t parts, int32_t index, int64_t *begin, int64_t *end);
 int mf_round_segment(uint64_t seed, int32_t epoch, int32_t G, int32_t round, int32_t rank, int32_t *col_segment);
+/* Peers of partition `rank` for the Q exchange after round `round` of `epoch` (the last round hands over
+ * to round 0 of epoch+1): it sends its segment to *send_to and receives from *recv_from. */
+int mf_round_peers(uint64_t seed, int32_t epoch, int32_t G, int32_t round, int32_t rank, int32_t *send_to,
+                   int32_t *recv_from);
 
 /* Wavefront audit (MF_OPT_TRACE=1): copies up to cap records of 4 int64 (worker, block, t_start, t_end
  * in globaltimer ns) from the last wavefront epoch; *count = records written. */

@@ -328,7 +328,9 @@ extern "C" int mf_load_coo(mf_ctx *ctx, const int32_t *u, const int32_t *v, cons
         ctx->cap_n = nnz;
     }
     if (ctx->shuffle && !ctx->perm) RC(dev_alloc(ctx, &ctx->perm, nnz, "alloc perm"));
+    RC(ctx->gather_q());
     ctx->drop_layouts();
+    ctx->seg_valid = false;
     ctx->N = 0;
     const bool dev_src = is_device_ptr(u);
     const cudaMemcpyKind kind = dev_src ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
@@ -499,6 +501,10 @@ extern "C" int mf_epoch(mf_ctx *ctx, int schedule, mf_epoch_stats *stats) {
     if (schedule == MF_SCHED_DETERMINISTIC) RC(ctx->build_waves());
     if (schedule == MF_SCHED_WAVEFRONT) RC(ctx->build_wavefront());
     if (schedule == MF_SCHED_PARTITIONED) return ctx->epoch_partitioned(stats);
+    if (ctx->is_distributed())
+        return ctx->fail(MF_EINVAL, "with NCCL attached only MF_SCHED_PARTITIONED is available");
+    RC(ctx->gather_q());
+    ctx->seg_valid = false;
     cudaStream_t st = ctx->stream();
     const float eta = ctx->eta_at(ctx->epoch);
     const ShapeId sh = select_shape(ctx->k, ctx->storage, ctx->variant & 0xF);
@@ -534,6 +540,7 @@ extern "C" int mf_rmse(mf_ctx *ctx, const int32_t *u, const int32_t *v, const fl
     if (!u || !v || !r || nnz <= 0) return ctx->fail(MF_EINVAL, "mf_rmse: null pointer or nnz <= 0");
     RC(ctx->ensure_factors());
     CK(cudaSetDevice(ctx->device));
+    RC(ctx->gather_q());
     cudaStream_t st = ctx->stream();
     if (nnz > ctx->cap_t) {
         dev_free(&ctx->tu);
@@ -609,7 +616,7 @@ extern "C" int mf_get_factors(mf_ctx *ctx, float *P, float *Q) {
     if (!ctx) return MF_EINVAL;
     RC(ctx->ensure_factors());
     CK(cudaSetDevice(ctx->device));
-    if (ctx->is_distributed()) RC(ctx->gather_q());
+    RC(ctx->gather_q());
     if (P) RC(ctx->copy_out(ctx->P, ctx->p_rows() * ctx->k, P));
     if (Q) RC(ctx->copy_out(ctx->Q, ctx->n * ctx->k, Q));
     return MF_OK;
@@ -619,8 +626,11 @@ extern "C" int mf_set_factors(mf_ctx *ctx, const float *P, const float *Q) {
     if (!ctx) return MF_EINVAL;
     RC(ctx->ensure_factors());
     CK(cudaSetDevice(ctx->device));
+    RC(ctx->gather_q());
     if (P) RC(ctx->copy_in(ctx->P, ctx->p_rows() * ctx->k, P));
     if (Q) RC(ctx->copy_in(ctx->Q, ctx->n * ctx->k, Q));
+    ctx->full_valid = true;
+    ctx->seg_valid = false;
     return MF_OK;
 }
 

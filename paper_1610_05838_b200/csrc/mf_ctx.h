@@ -71,16 +71,20 @@ struct mf_ctx {
 
     // partitioned layout (mf_partition.cu)
     bool part_valid = false;
-    int part_G = 0;                  // logical partitions (loopback) or world size
-    int32_t *bu = nullptr, *bv = nullptr;
+    int part_G = 0;                  // partitions = world size (NCCL) or logical partitions (loopback)
+    int part_local = 0;              // partitions hosted by this context (1 with NCCL, G in loopback)
+    int32_t *bu = nullptr, *bv = nullptr;  // samples bucketed by (local partition, column segment); v segment-local
     float *br = nullptr;
-    int64_t *blk_off = nullptr;      // device copy of block offsets
-    std::vector<int64_t> h_blk_off;  // host copy
-    std::vector<int64_t> q_seg;      // column segment boundaries (G + 1)
-    void *q_buf[2] = {nullptr, nullptr};
+    std::vector<int64_t> h_blk_off;  // (part_local * G + 1) block offsets
+    int64_t seg_rows_max = 0;        // rows of the largest Q segment
+    std::vector<void *> q_cur, q_next;  // per hosted partition: the Q segment it holds / receive buffer
+    std::vector<int32_t> held;       // held[g] = Q segment held by partition g (all G, known everywhere)
+    bool full_valid = true;          // ctx->Q (full n x k) is current
+    bool seg_valid = false;          // q_cur buffers are current
     mf_nccl *nccl = nullptr;
     int rank = 0, world = 1;
     cudaStream_t comm_stream = nullptr;
+    void *gather_tmp = nullptr;
 
     // scratch for rmse / factors
     int32_t *tu = nullptr, *tv = nullptr;
@@ -116,6 +120,8 @@ struct mf_ctx {
 
     // mf_partition.cu
     int epoch_partitioned(mf_epoch_stats *stats);
+    int build_partition();
+    int exchange_segments(const std::vector<int32_t> &want);
     int rmse_partitioned(int64_t nnz, double *out);
     int gather_q();
     void release_partition();

@@ -325,7 +325,7 @@ __global__ void __launch_bounds__(kBlock) k_rmse(const int32_t *u, const int32_t
     }
 }
 
-__global__ void k_sum_partials(const double *partials, int n, int64_t count, double *out) {
+__global__ void k_sum_partials(const double *partials, int n, int64_t count, double *out, int do_sqrt) {
     __shared__ double sh[256];
     double s = 0.0;
     for (int i = threadIdx.x; i < n; i += blockDim.x) s += partials[i];
@@ -335,19 +335,19 @@ __global__ void k_sum_partials(const double *partials, int n, int64_t count, dou
         if ((int)threadIdx.x < o) sh[threadIdx.x] += sh[threadIdx.x + o];
         __syncthreads();
     }
-    if (threadIdx.x == 0) out[0] = sqrt(sh[0] / (double)count);
+    if (threadIdx.x == 0) out[0] = do_sqrt ? sqrt(sh[0] / (double)count) : sh[0];
 }
 
 cudaError_t launch_rmse(const ShapeId &sh, const int32_t *u, const int32_t *v, const float *r, int64_t n,
                         const void *P, const void *Q, int k, double *partials, int nparts, double *out,
-                        cudaStream_t st) {
+                        cudaStream_t st, int do_sqrt) {
     cudaError_t e = dispatch_shape(sh, [&](auto tag) -> cudaError_t {
         using SH = decltype(tag);
         k_rmse<SH><<<nparts, kBlock, 0, st>>>(u, v, r, n, P, Q, k, partials);
         return cudaGetLastError();
     });
     if (e != cudaSuccess) return e;
-    k_sum_partials<<<1, 256, 0, st>>>(partials, nparts, n, out);
+    k_sum_partials<<<1, 256, 0, st>>>(partials, nparts, n, out, do_sqrt);
     return cudaGetLastError();
 }
 

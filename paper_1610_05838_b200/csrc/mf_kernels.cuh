@@ -49,7 +49,7 @@ cudaError_t launch_hogwild(const ShapeId &sh, const UpdateArgs &a, int workers, 
 cudaError_t launch_waves(const ShapeId &sh, const UpdateArgs &a, cudaStream_t st, int *launches);
 cudaError_t launch_rmse(const ShapeId &sh, const int32_t *u, const int32_t *v, const float *r, int64_t n,
                         const void *P, const void *Q, int k, double *partials, int nparts, double *out,
-                        cudaStream_t st);
+                        cudaStream_t st, int do_sqrt = 1);
 cudaError_t launch_init_offset(int storage, void *X, int64_t elem0, int64_t count, int k, uint64_t seed, uint32_t tag,
                                cudaStream_t st);
 cudaError_t launch_init_rows(int storage, void *X, int64_t row0, int64_t rows, int k, uint64_t seed, uint32_t tag,

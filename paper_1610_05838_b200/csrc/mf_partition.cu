@@ -1,16 +1,394 @@
-// mf_partition.cu -- multi-GPU block partition with Q rotation (§4.1).  [stub]
-#include "mf_ctx.h"
+// mf_partition.cu -- multi-GPU block partition with Q-segment rotation (§4.1).
+//
+// The rating matrix is divided into G x G blocks: P into G row segments and Q into G column
+// segments (step 1 of P:294-300).  Partition g owns P segment g permanently and the samples of
+// row segment g, bucketed by column segment (a stable radix sort keeps the shuffled order inside
+// every block).  An epoch is G rounds; in round r partition g updates block (g, sigma_e(g, r)) with
+// sigma_e(g, r) = pi_e((g + r) mod G), pi_e a per-epoch random permutation, so the blocks of one
+// round never share a row or a column segment (a Latin square, P:129 / P:535) and every block is
+// processed once per epoch.  Between rounds each partition sends the Q segment it holds to the
+// partition that needs it next and receives its next segment: with NCCL (one process per GPU,
+// grouped ncclSend/ncclRecv over NVLink) or, for one-GPU testing, a loopback transport that runs
+// the G partitions on the same device and moves segments with device copies.  Unlike the paper
+// nothing goes through host memory.
+//
+// Inside a block the update is batch-Hogwild! (workers = max(1, N_local / 10^4), A-10),
+// or exactly serial with MF_OPT_WORKERS = 1 (used for parity).
+#include <cuda_runtime.h>
+#include <nccl.h>
 
-int mf_ctx::epoch_partitioned(mf_epoch_stats *) { return fail(MF_EINVAL, "partitioned schedule not built yet"); }
-int mf_ctx::rmse_partitioned(int64_t, double *) { return fail(MF_EINVAL, "partitioned schedule not built yet"); }
-int mf_ctx::gather_q() { return MF_OK; }
-void mf_ctx::release_partition() {}
-extern "C" int mf_nccl_unique_id(void *) { return MF_ENCCL; }
-extern "C" int mf_attach_nccl(mf_ctx *, const void *, int, int) { return MF_ENCCL; }
+#include <cub/device/device_radix_sort.cuh>
+
+#include <algorithm>
+#include <cstring>
+#include <vector>
+
+#include "mf_ctx.h"
+#include "mf_host_util.h"
+
+using namespace mf;
+
+struct mf_nccl {
+    ncclComm_t comm = nullptr;
+};
+
+namespace {
+
+// ---------------------------------------------------------------- schedule --
+void round_perm(std::vector<int32_t> &pi, uint64_t seed, int32_t epoch, int G) {
+    permutation(pi, G, host_mix(seed ^ 0xB10CB10Cull ^ ((uint64_t)(uint32_t)epoch << 32)));
+}
+int32_t sigma(const std::vector<int32_t> &pi, int G, int g, int r) { return pi[(g + r) % G]; }
+
+// segment index of x in [0, extent) split into `parts` (boundaries floor(i*extent/parts))
+__device__ __forceinline__ int seg_of(int64_t x, int64_t extent, int parts) {
+    int g = (int)((x * parts) / extent);
+    if (g + 1 <= parts - 1 && ((int64_t)(g + 1) * extent) / parts <= x) g++;
+    return g;
+}
+
+__global__ void k_part_keys(const int32_t *u, const int32_t *v, int64_t n, int64_t m_rows, int64_t n_cols, int G,
+                            int rows_split, uint32_t *keys, uint32_t *idx) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int rs = rows_split ? seg_of(u[i], m_rows, G) : 0;
+        keys[i] = (uint32_t)(rs * G + seg_of(v[i], n_cols, G));
+        idx[i] = (uint32_t)i;
+    }
+}
+
+// gather into block order; v becomes local to its column segment
+__global__ void k_part_gather(const int32_t *u, const int32_t *v, const float *r, const uint32_t *idx,
+                              const uint32_t *keys, int64_t n, int64_t n_cols, int G, int32_t *bu, int32_t *bv,
+                              float *br) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t j = idx[i];
+        const int cs = (int)(keys[i] % (uint32_t)G);
+        bu[i] = u[j];
+        bv[i] = v[j] - (int32_t)(((int64_t)cs * n_cols) / G);
+        br[i] = r[j];
+    }
+}
+
+__global__ void k_offsets(const uint32_t *sorted_keys, int64_t n, int64_t nb, int64_t *off) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i <= n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t prev = i == 0 ? -1 : (int64_t)sorted_keys[i - 1];
+        const int64_t cur = i == n ? nb : (int64_t)sorted_keys[i];
+        for (int64_t b = prev + 1; b <= cur; b++) off[b] = i;
+    }
+}
+
+int nccl_fail(mf_ctx *ctx, ncclResult_t r, const char *what) {
+    return ctx->fail(MF_ENCCL, "%s: %s", what, ncclGetErrorString(r));
+}
+
+}  // namespace
+
+#define CK(expr)                                   \
+    do {                                           \
+        int _rc = cuda((expr), #expr);             \
+        if (_rc != MF_OK) return _rc;              \
+    } while (0)
+#define NK(expr)                                                   \
+    do {                                                           \
+        ncclResult_t _r = (expr);                                  \
+        if (_r != ncclSuccess) return nccl_fail(this, _r, #expr);  \
+    } while (0)
+
+// ------------------------------------------------------------ host helpers --
 extern "C" int mf_segment(int64_t extent, int32_t parts, int32_t index, int64_t *b, int64_t *e) {
     if (extent < 0 || parts <= 0 || index < 0 || index >= parts || !b || !e) return MF_EINVAL;
-    *b = extent * index / parts;
-    *e = extent * (index + 1) / parts;
+    *b = seg_begin(extent, parts, index);
+    *e = seg_begin(extent, parts, index + 1);
     return MF_OK;
 }
-extern "C" int mf_round_segment(uint64_t, int32_t, int32_t, int32_t, int32_t, int32_t *) { return MF_EINVAL; }
+
+extern "C" int mf_round_segment(uint64_t seed, int32_t epoch, int32_t G, int32_t round, int32_t rank,
+                                int32_t *col_segment) {
+    if (G <= 0 || round < 0 || round >= G || rank < 0 || rank >= G || epoch < 0 || !col_segment) return MF_EINVAL;
+    std::vector<int32_t> pi;
+    round_perm(pi, seed, epoch, G);
+    *col_segment = sigma(pi, G, rank, round);
+    return MF_OK;
+}
+
+// peers of partition `rank` for the exchange that follows round `round` of `epoch` (the last round
+// hands over to round 0 of epoch + 1): it sends its segment to *send_to, receives from *recv_from.
+extern "C" int mf_round_peers(uint64_t seed, int32_t epoch, int32_t G, int32_t round, int32_t rank,
+                              int32_t *send_to, int32_t *recv_from) {
+    if (G <= 0 || round < 0 || round >= G || rank < 0 || rank >= G || epoch < 0 || !send_to || !recv_from)
+        return MF_EINVAL;
+    std::vector<int32_t> pi, pn;
+    round_perm(pi, seed, epoch, G);
+    if (round + 1 < G) pn = pi;
+    else round_perm(pn, seed, epoch + 1, G);
+    const int nr = (round + 1) % G;
+    std::vector<int32_t> held(G), want(G);
+    for (int g = 0; g < G; g++) {
+        held[g] = sigma(pi, G, g, round);
+        want[g] = sigma(pn, G, g, nr);
+    }
+    for (int h = 0; h < G; h++) {
+        if (want[h] == held[rank]) *send_to = h;
+        if (held[h] == want[rank]) *recv_from = h;
+    }
+    return MF_OK;
+}
+
+// ------------------------------------------------------------------ NCCL ----
+extern "C" int mf_nccl_unique_id(void *out128) {
+    if (!out128) return MF_EINVAL;
+    static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId is 128 bytes");
+    ncclUniqueId id;
+    if (ncclGetUniqueId(&id) != ncclSuccess) return MF_ENCCL;
+    std::memcpy(out128, &id, sizeof id);
+    return MF_OK;
+}
+
+extern "C" int mf_attach_nccl(mf_ctx *ctx, const void *id128, int rank, int world) {
+    if (!ctx || !id128 || world < 1 || rank < 0 || rank >= world) return MF_EINVAL;
+    if (ctx->P || ctx->N > 0 || ctx->nccl) return ctx->fail(MF_ESTATE, "mf_attach_nccl must precede loading and factors");
+    if (ctx->m < world || ctx->n < world) return ctx->fail(MF_EINVAL, "need m, n >= world");
+    int rc = ctx->ensure_device();
+    if (rc != MF_OK) return rc;
+    cudaSetDevice(ctx->device);
+    ncclUniqueId id;
+    std::memcpy(&id, id128, sizeof id);
+    mf_nccl *nc = new mf_nccl();
+    ncclResult_t r = ncclCommInitRank(&nc->comm, world, id, rank);
+    if (r != ncclSuccess) {
+        delete nc;
+        return ctx->fail(MF_ENCCL, "ncclCommInitRank: %s", ncclGetErrorString(r));
+    }
+    ctx->nccl = nc;
+    ctx->rank = rank;
+    ctx->world = world;
+    ctx->p_begin = seg_begin(ctx->m, world, rank);
+    ctx->p_end = seg_begin(ctx->m, world, rank + 1);
+    return MF_OK;
+}
+
+// ---------------------------------------------------------------- layout ----
+void mf_ctx::release_partition() {
+    for (void *p : {(void *)bu, (void *)bv, (void *)br, gather_tmp})
+        if (p) cudaFree(p);
+    bu = bv = nullptr;
+    br = nullptr;
+    gather_tmp = nullptr;
+    for (auto *vec : {&q_cur, &q_next})
+        for (void *p : *vec)
+            if (p) cudaFree(p);
+    q_cur.clear();
+    q_next.clear();
+    held.clear();
+    h_blk_off.clear();
+    seg_valid = false;
+    part_valid = false;
+    if (nccl) {
+        if (nccl->comm) ncclCommDestroy(nccl->comm);
+        delete nccl;
+        nccl = nullptr;
+    }
+}
+
+int mf_ctx::build_partition() {
+    if (part_valid) return MF_OK;
+    const int G = is_distributed() ? world : std::max(1, partitions);
+    if (G > n || G > p_rows() * (is_distributed() ? world : 1))
+        return fail(MF_EINVAL, "partitioned: G = %d exceeds the matrix dimensions", G);
+    const int local = is_distributed() ? 1 : G;
+    // free a previous layout's buffers (keep the NCCL comm)
+    for (void *p : {(void *)bu, (void *)bv, (void *)br})
+        if (p) cudaFree(p);
+    bu = bv = nullptr;
+    br = nullptr;
+    for (auto *vec : {&q_cur, &q_next})
+        for (void *p : *vec)
+            if (p) cudaFree(p);
+    q_cur.assign(local, nullptr);
+    q_next.assign(local, nullptr);
+    seg_valid = false;
+
+    cudaStream_t st = stream();
+    const int64_t nb = (int64_t)local * G;
+    uint32_t *k0 = nullptr, *k1 = nullptr, *i0 = nullptr, *i1 = nullptr;
+    int64_t *doff = nullptr;
+    void *tmp = nullptr;
+    size_t tmp_bytes = 0;
+    CK(cudaMalloc((void **)&bu, sizeof(int32_t) * std::max<int64_t>(N, 1)));
+    CK(cudaMalloc((void **)&bv, sizeof(int32_t) * std::max<int64_t>(N, 1)));
+    CK(cudaMalloc((void **)&br, sizeof(float) * std::max<int64_t>(N, 1)));
+    CK(cudaMallocAsync((void **)&k0, sizeof(uint32_t) * N, st));
+    CK(cudaMallocAsync((void **)&k1, sizeof(uint32_t) * N, st));
+    CK(cudaMallocAsync((void **)&i0, sizeof(uint32_t) * N, st));
+    CK(cudaMallocAsync((void **)&i1, sizeof(uint32_t) * N, st));
+    CK(cudaMallocAsync((void **)&doff, sizeof(int64_t) * (nb + 1), st));
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((N + 255) / 256, 148 * 16));
+    // loopback: rows are global, split into G segments; NCCL: u is already local to this rank's segment
+    k_part_keys<<<grid, 256, 0, st>>>(u, v, N, m, n, G, is_distributed() ? 0 : 1, k0, i0);
+    CK(cudaGetLastError());
+    int bits = 1;
+    while (bits < 32 && (1ull << bits) < (uint64_t)nb) bits++;
+    CK(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, k0, k1, i0, i1, N, 0, bits, st));
+    CK(cudaMallocAsync(&tmp, tmp_bytes, st));
+    CK(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, k0, k1, i0, i1, N, 0, bits, st));  // stable
+    k_part_gather<<<grid, 256, 0, st>>>(u, v, r, i1, k1, N, n, G, bu, bv, br);
+    CK(cudaGetLastError());
+    k_offsets<<<grid, 256, 0, st>>>(k1, N, nb, doff);
+    CK(cudaGetLastError());
+    h_blk_off.assign((size_t)nb + 1, 0);
+    CK(cudaMemcpyAsync(h_blk_off.data(), doff, sizeof(int64_t) * (nb + 1), cudaMemcpyDeviceToHost, st));
+    for (void *p : {(void *)tmp, (void *)k0, (void *)k1, (void *)i0, (void *)i1, (void *)doff}) CK(cudaFreeAsync(p, st));
+    CK(cudaStreamSynchronize(st));
+
+    seg_rows_max = 0;
+    for (int c = 0; c < G; c++) seg_rows_max = std::max(seg_rows_max, seg_begin(n, G, c + 1) - seg_begin(n, G, c));
+    const size_t bytes = (size_t)seg_rows_max * k * storage_bytes();
+    for (int g = 0; g < local; g++) {
+        CK(cudaMalloc(&q_cur[g], bytes));
+        CK(cudaMalloc(&q_next[g], bytes));
+    }
+    if (is_distributed() && !comm_stream) CK(cudaStreamCreateWithFlags(&comm_stream, cudaStreamNonBlocking));
+    part_G = G;
+    part_local = local;
+    held.assign(G, -1);
+    part_valid = true;
+    return MF_OK;
+}
+
+// Move segments so that partition g holds want[g]: g sends what it holds to the partition that wants
+// it and receives what it wants from the partition holding it (one send + one recv per partition).
+int mf_ctx::exchange_segments(const std::vector<int32_t> &want) {
+    const int G = part_G;
+    const size_t bytes = (size_t)seg_rows_max * k * storage_bytes();
+    cudaStream_t st = stream();
+    std::vector<int> dst(G), src(G);
+    for (int g = 0; g < G; g++)
+        for (int h = 0; h < G; h++) {
+            if (want[h] == held[g]) dst[g] = h;
+            if (held[h] == want[g]) src[g] = h;
+        }
+    if (is_distributed()) {
+        const int g = rank;
+        if (dst[g] != g) {
+            NK(ncclGroupStart());
+            NK(ncclSend(q_cur[0], bytes, ncclUint8, dst[g], nccl->comm, st));
+            NK(ncclRecv(q_next[0], bytes, ncclUint8, src[g], nccl->comm, st));
+            NK(ncclGroupEnd());
+            std::swap(q_cur[0], q_next[0]);
+        }
+    } else {
+        for (int g = 0; g < G; g++)
+            if (dst[g] != g) CK(cudaMemcpyAsync(q_next[dst[g]], q_cur[g], bytes, cudaMemcpyDeviceToDevice, st));
+        for (int g = 0; g < G; g++)
+            if (dst[g] != g) std::swap(q_cur[g], q_next[g]);
+    }
+    held = want;
+    return MF_OK;
+}
+
+// full Q -> segment buffers (partition g takes want[g])
+static int scatter_segments(mf_ctx *ctx, const std::vector<int32_t> &want) {
+    const int G = ctx->part_G;
+    const size_t rb = (size_t)ctx->k * ctx->storage_bytes();
+    for (int li = 0; li < ctx->part_local; li++) {
+        const int g = ctx->is_distributed() ? ctx->rank : li;
+        const int64_t b = seg_begin(ctx->n, G, want[g]), e = seg_begin(ctx->n, G, want[g] + 1);
+        int rc = ctx->cuda(cudaMemcpyAsync(ctx->q_cur[li], (char *)ctx->Q + b * rb, (e - b) * rb,
+                                           cudaMemcpyDeviceToDevice, ctx->stream()), "scatter Q");
+        if (rc != MF_OK) return rc;
+    }
+    ctx->held = want;
+    ctx->seg_valid = true;
+    return MF_OK;
+}
+
+// segment buffers -> full Q (collective with NCCL: all-gather of the held segments)
+int mf_ctx::gather_q() {
+    if (full_valid) return MF_OK;
+    if (!seg_valid) return fail(MF_ESTATE, "no valid copy of Q");
+    const int G = part_G;
+    const size_t rb = (size_t)k * storage_bytes();
+    const size_t bytes = (size_t)seg_rows_max * rb;
+    cudaStream_t st = stream();
+    if (is_distributed()) {
+        if (!gather_tmp) CK(cudaMalloc(&gather_tmp, bytes * G));
+        NK(ncclAllGather(q_cur[0], gather_tmp, bytes, ncclUint8, nccl->comm, st));
+        for (int h = 0; h < G; h++) {
+            const int64_t b = seg_begin(n, G, held[h]), e = seg_begin(n, G, held[h] + 1);
+            CK(cudaMemcpyAsync((char *)Q + b * rb, (char *)gather_tmp + h * bytes, (e - b) * rb,
+                               cudaMemcpyDeviceToDevice, st));
+        }
+    } else {
+        for (int g = 0; g < G; g++) {
+            const int64_t b = seg_begin(n, G, held[g]), e = seg_begin(n, G, held[g] + 1);
+            CK(cudaMemcpyAsync((char *)Q + b * rb, q_cur[g], (e - b) * rb, cudaMemcpyDeviceToDevice, st));
+        }
+    }
+    CK(cudaStreamSynchronize(st));
+    full_valid = true;
+    return MF_OK;
+}
+
+// ----------------------------------------------------------------- epoch ----
+int mf_ctx::epoch_partitioned(mf_epoch_stats *stats) {
+    if (!is_distributed() && partitions < 1) return fail(MF_EINVAL, "set MF_OPT_PARTITIONS or attach NCCL");
+    int rc = build_partition();
+    if (rc != MF_OK) return rc;
+    const int G = part_G;
+    cudaStream_t st = stream();
+    const float eta = eta_at(epoch);
+    std::vector<int32_t> pi, want(G);
+    round_perm(pi, seed_shuffle, epoch, G);
+    for (int g = 0; g < G; g++) want[g] = sigma(pi, G, g, 0);
+    CK(cudaEventRecord(events[0], st));
+    CK(cudaMemsetAsync(scratch, 0, sizeof(DevScratch), st));
+    if (!seg_valid) rc = scatter_segments(this, want);
+    else rc = exchange_segments(want);
+    if (rc != MF_OK) return rc;
+    full_valid = false;
+    const ShapeId sh = select_shape(k, storage, variant & 0xF);
+    int launches = 0, used_max = 0;
+    CK(cudaEventRecord(events[1], st));
+    for (int r = 0; r < G; r++) {
+        for (int li = 0; li < part_local; li++) {
+            const int g = is_distributed() ? rank : li;
+            const int c = sigma(pi, G, g, r);
+            const int64_t lo = h_blk_off[(size_t)li * G + c], hi = h_blk_off[(size_t)li * G + c + 1];
+            if (hi <= lo) continue;
+            UpdateArgs a = update_args(eta);
+            a.u = bu + lo;
+            a.v = bv + lo;
+            a.r = br + lo;
+            a.n = hi - lo;
+            a.Q = q_cur[li];
+            const int64_t n_local = h_blk_off[(size_t)(li + 1) * G] - h_blk_off[(size_t)li * G];
+            const int w = workers > 0 ? workers : (int)std::max<int64_t>(1, std::min<int64_t>(n_local / 10000, 1 << 30));
+            int used = 0;
+            CK(launch_hogwild(sh, a, w, variant, st, &used));
+            used_max = std::max(used_max, used);
+            launches++;
+        }
+        if (r + 1 < G) {
+            for (int g = 0; g < G; g++) want[g] = sigma(pi, G, g, r + 1);
+            rc = exchange_segments(want);
+            if (rc != MF_OK) return rc;
+        }
+    }
+    CK(cudaEventRecord(events[2], st));
+    return finish_epoch(MF_SCHED_PARTITIONED, eta, launches, used_max, stats);
+}
+
+int mf_ctx::rmse_partitioned(int64_t nnz, double *out) {
+    // caller (mf_rmse) validated the local test triples, rebased u and gathered Q
+    cudaStream_t st = stream();
+    const ShapeId sh = select_shape(k, storage, 0);
+    CK(launch_rmse(sh, tu, tv, tr, nnz, P, Q, k, partials, rmse_parts(), d_out, st, 0));
+    double cnt = (double)nnz;
+    CK(cudaMemcpyAsync(d_out + 1, &cnt, sizeof(double), cudaMemcpyHostToDevice, st));
+    NK(ncclAllReduce(d_out, d_out, 2, ncclFloat64, ncclSum, nccl->comm, st));
+    double h[2];
+    CK(cudaMemcpyAsync(h, d_out, sizeof h, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    *out = std::sqrt(h[0] / h[1]);
+    return MF_OK;
+}

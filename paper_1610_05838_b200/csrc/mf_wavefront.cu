@@ -25,6 +25,7 @@
 #include <vector>
 
 #include "mf_ctx.h"
+#include "mf_host_util.h"
 #include "sgd_core.cuh"
 
 using namespace mf;
@@ -32,24 +33,6 @@ using namespace mf;
 namespace {
 
 constexpr int kBlock = 256;
-
-uint64_t host_mix(uint64_t x) {
-    uint64_t z = x + 0x9E3779B97F4A7C15ull;
-    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
-    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
-    return z ^ (z >> 31);
-}
-
-// Fisher-Yates permutation of [0, n) driven by a counter hash stream
-void permutation(std::vector<int32_t> &out, int n, uint64_t key) {
-    out.resize(n);
-    std::iota(out.begin(), out.end(), 0);
-    for (int i = n - 1; i > 0; i--) {
-        const uint64_t h = host_mix(key ^ (uint64_t)i * 0xD1B54A32D192ED03ull);
-        const int j = (int)(h % (uint64_t)(i + 1));
-        std::swap(out[i], out[j]);
-    }
-}
 
 __global__ void k_block_keys(const int32_t *u, const int32_t *v, int64_t n, int64_t band_w, int64_t grp_w, int s,
                              int c, uint32_t *keys, uint32_t *idx) {

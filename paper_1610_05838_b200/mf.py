@@ -50,6 +50,8 @@ _sig = {
     "mf_attach_nccl": ([_P, _P, c.c_int, c.c_int], c.c_int),
     "mf_segment": ([c.c_int64, c.c_int32, c.c_int32, c.POINTER(c.c_int64), c.POINTER(c.c_int64)], c.c_int),
     "mf_round_segment": ([c.c_uint64, c.c_int32, c.c_int32, c.c_int32, c.c_int32, c.POINTER(c.c_int32)], c.c_int),
+    "mf_round_peers": ([c.c_uint64, c.c_int32, c.c_int32, c.c_int32, c.c_int32, c.POINTER(c.c_int32),
+                        c.POINTER(c.c_int32)], c.c_int),
     "mf_wavefront_trace": ([_P, _P, c.c_int64, c.POINTER(c.c_int64)], c.c_int),
     "mf_destroy": ([_P], None),
     "mf_last_error": ([_P], c.c_char_p),
@@ -173,6 +175,12 @@ def mf_round_segment(seed, epoch, G, rnd, rank):
     out = c.c_int32()
     _check(None, _lib.mf_round_segment(seed, epoch, G, rnd, rank, c.byref(out)))
     return out.value
+
+
+def mf_round_peers(seed, epoch, G, rnd, rank):
+    s, r = c.c_int32(), c.c_int32()
+    _check(None, _lib.mf_round_peers(seed, epoch, G, rnd, rank, c.byref(s), c.byref(r)))
+    return s.value, r.value
 
 
 def mf_wavefront_trace(ctx, cap):

@@ -1,0 +1,86 @@
+"""Worker for tests/test_partition_host.py: the partitioned schedule's host algebra over gloo (CPU).
+
+Each of G processes owns P row segment g and the samples of that segment, holds one Q column
+segment at a time as libmf's schedule says (mf_round_segment), updates its block with the serial
+oracle, and passes Q segments to the peers libmf names (mf_round_peers) with torch.distributed
+send/recv.  Rank 0 gathers P and Q at the end and writes them to `out` for comparison with a
+single-process oracle sweep over the same block order.
+"""
+import os
+import sys
+
+import numpy as np
+
+
+def run(rank, G, port, data, out, epochs, seed):
+    import torch
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=G)
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import oracle
+    from paper_1610_05838_b200 import mf
+
+    d = np.load(data)
+    u, v, r, P0, Q0 = d["u"], d["v"], d["r"], d["P0"], d["Q0"]
+    m, n, k = P0.shape[0], Q0.shape[0], P0.shape[1]
+    lam, alpha = float(d["lam"]), float(d["alpha"])
+    pb, pe = mf.mf_segment(m, G, rank)
+    mine = (u >= pb) & (u < pe)          # samples of my row segment, stored order kept
+    P = P0[pb:pe].copy()
+    seg = [mf.mf_segment(n, G, c) for c in range(G)]
+    held = mf.mf_round_segment(seed, 0, G, 0, rank)
+    Q = Q0[seg[held][0]:seg[held][1]].copy()
+    for e in range(epochs):
+        eta = oracle.eta(alpha, 0.0, e)
+        for rnd in range(G):
+            c = mf.mf_round_segment(seed, e, G, rnd, rank)
+            assert c == held, "holding the wrong Q segment"
+            qb, qe = seg[c]
+            sel = mine & (v >= qb) & (v < qe)
+            mdl = oracle.Model(pe - pb, qe - qb, k, oracle.F32, P=P, Q=Q)
+            mdl.epoch(u[sel] - pb, v[sel] - qb, r[sel], eta, lam)
+            P, Q = mdl.P, mdl.Q
+            dst, src = mf.mf_round_peers(seed, e, G, rnd, rank)
+            nxt_e, nxt_r = (e, rnd + 1) if rnd + 1 < G else (e + 1, 0)
+            want = mf.mf_round_segment(seed, nxt_e, G, nxt_r, rank)
+            buf = np.empty((seg[want][1] - seg[want][0], k), np.float32)
+            if dst == rank:
+                assert src == rank
+                buf = Q
+            else:
+                reqs = [dist.isend(torch.from_numpy(np.ascontiguousarray(Q)), dst),
+                        dist.irecv(torch.from_numpy(buf), src)]
+                for q in reqs:
+                    q.wait()
+            Q, held = buf, want
+    # gather: P segments and the Q segment each rank holds
+    Ps = [torch.zeros((e_ - b_, k)) for b_, e_ in (mf.mf_segment(m, G, g) for g in range(G))]
+    dist.all_gather(Ps, torch.from_numpy(P)) if len({p.shape for p in Ps}) == 1 else _gather_var(dist, torch, P, Ps)
+    helds = [torch.zeros(1, dtype=torch.int64) for _ in range(G)]
+    dist.all_gather(helds, torch.tensor([held]))
+    Qfull = np.zeros_like(Q0)
+    for g in range(G):
+        h = int(helds[g])
+        t = torch.zeros((seg[h][1] - seg[h][0], k))
+        if g == rank:
+            t = torch.from_numpy(Q)
+        dist.broadcast(t, g)
+        Qfull[seg[h][0]:seg[h][1]] = t.numpy()
+    if rank == 0:
+        np.savez(out, P=np.concatenate([p.numpy() for p in Ps]), Q=Qfull)
+    dist.destroy_process_group()
+
+
+def _gather_var(dist, torch, P, Ps):
+    rank = dist.get_rank()
+    for g in range(len(Ps)):
+        t = torch.from_numpy(P) if g == rank else Ps[g]
+        dist.broadcast(t, g)
+        Ps[g] = t
+
+
+if __name__ == "__main__":
+    rank, G, port, data, out, epochs, seed = sys.argv[1:]
+    run(int(rank), int(G), int(port), data, out, int(epochs), int(seed))
