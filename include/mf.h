@@ -78,7 +78,8 @@ typedef enum {
     MF_OPT_PARTITIONS = 12,   /* MF_SCHED_PARTITIONED without NCCL: G logical partitions run on this GPU (loopback) */
     MF_OPT_SEED_SHUFFLE = 13, /* seed of the A-8 shuffle (default: the mf_create seed) */
     MF_OPT_VARIANT = 14,      /* kernel variant selector for tuning (0 = default) */
-    MF_OPT_TRACE = 15         /* wavefront audit trace: 1 = record (worker, block, t_start, t_end) per block */
+    MF_OPT_TRACE = 15,        /* wavefront audit trace: 1 = record (worker, block, t_start, t_end) per block */
+    MF_OPT_SUBEPOCHS = 16     /* partitioned: passes S per epoch, each over 1/S of the shuffled samples with its own Latin square (default 4) */
 } mf_option;
 
 typedef struct {
@@ -135,14 +136,15 @@ int mf_attach_nccl(mf_ctx *ctx, const void *id128, int rank, int world);
 
 /* Host-only helpers of the partitioned schedule (no device needed):
  * row segment of rank g among G: [seg_begin, seg_end) = [floor(g*m/G), floor((g+1)*m/G));
- * column segment held by rank g in round r of epoch e: sigma_e(g, r) = pi_e((g + r) mod G), pi_e a
- * per-epoch permutation drawn from `seed` (the context's shuffle seed) -- a Latin square, so the
- * blocks of one round share no row or column segment. */
+ * an epoch e is S passes (MF_OPT_SUBEPOCHS) over consecutive slices of the shuffled samples, pass
+ * index p = e*S + s.  In round r of pass p rank g holds column segment sigma_p(g, r) =
+ * pi_p((g + r) mod G), pi_p a permutation drawn from `seed` (the context's shuffle seed): a Latin
+ * square, so the blocks of one round share no row or column segment. */
 int mf_segment(int64_t extent, int32_t parts, int32_t index, int64_t *begin, int64_t *end);
-int mf_round_segment(uint64_t seed, int32_t epoch, int32_t G, int32_t round, int32_t rank, int32_t *col_segment);
-/* Peers of partition `rank` for the Q exchange after round `round` of `epoch` (the last round hands over
- * to round 0 of epoch+1): it sends its segment to *send_to and receives from *recv_from. */
-int mf_round_peers(uint64_t seed, int32_t epoch, int32_t G, int32_t round, int32_t rank, int32_t *send_to,
+int mf_round_segment(uint64_t seed, int32_t pass, int32_t G, int32_t round, int32_t rank, int32_t *col_segment);
+/* Peers of partition `rank` for the Q exchange after round `round` of pass `pass` (the last round hands
+ * over to round 0 of pass+1): it sends its segment to *send_to and receives from *recv_from. */
+int mf_round_peers(uint64_t seed, int32_t pass, int32_t G, int32_t round, int32_t rank, int32_t *send_to,
                    int32_t *recv_from);
 
 /* Wavefront audit (MF_OPT_TRACE=1): copies up to cap records of 4 int64 (worker, block, t_start, t_end

@@ -97,6 +97,13 @@ int mf_ctx::ensure_device() {
     CK(cudaMallocHost((void **)&h_scratch, sizeof(DevScratch)));
     for (auto &ev : events) CK(cudaEventCreate(&ev));
     CK(cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, device));
+    {  // keep stream-ordered allocations cached instead of unmapping them at every synchronisation
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+            uint64_t thr = UINT64_MAX;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+        }
+    }
     dev_ready = true;
     return MF_OK;
 }
@@ -143,6 +150,9 @@ void mf_ctx::release() {
     dev_free(&v);
     dev_free(&r);
     dev_free(&perm);
+    dev_free(&stg_u);
+    dev_free(&stg_v);
+    dev_free(&stg_r);
     dev_free(&tu);
     dev_free(&tv);
     dev_free(&tr);
@@ -275,6 +285,11 @@ extern "C" int mf_set_option(mf_ctx *ctx, int key, double value) {
         case MF_OPT_TRACE:
             ctx->trace = iv ? 1 : 0;
             return MF_OK;
+        case MF_OPT_SUBEPOCHS:
+            if (iv < 1 || iv > 4096) return ctx->fail(MF_EINVAL, "subepochs must be in [1, 4096]");
+            ctx->subepochs = (int)iv;
+            ctx->part_valid = false;
+            return MF_OK;
         default:
             return ctx->fail(MF_EINVAL, "unknown option %d", key);
     }
@@ -299,6 +314,7 @@ extern "C" int mf_get_option(const mf_ctx *ctx, int key, double *value) {
         case MF_OPT_SEED_SHUFFLE: *value = (double)ctx->seed_shuffle; return MF_OK;
         case MF_OPT_VARIANT: *value = ctx->variant; return MF_OK;
         case MF_OPT_TRACE: *value = ctx->trace; return MF_OK;
+        case MF_OPT_SUBEPOCHS: *value = ctx->subepochs; return MF_OK;
         default: return MF_EINVAL;
     }
 }
@@ -315,68 +331,50 @@ extern "C" int mf_load_coo(mf_ctx *ctx, const int32_t *u, const int32_t *v, cons
     RC(ctx->ensure_device());
     CK(cudaSetDevice(ctx->device));
     cudaStream_t st = ctx->stream();
-    if (nnz != ctx->cap_n) {
-        dev_free(&ctx->u);
-        dev_free(&ctx->v);
-        dev_free(&ctx->r);
-        dev_free(&ctx->perm);
+    if (nnz != ctx->cap_n) {  // (re)allocate; buffers are reused by repeated loads of the same size
+        for (void **p : {(void **)&ctx->u, (void **)&ctx->v, (void **)&ctx->r, (void **)&ctx->perm,
+                         (void **)&ctx->stg_u, (void **)&ctx->stg_v, (void **)&ctx->stg_r})
+            if (*p) cudaFree(*p), *p = nullptr;
         ctx->cap_n = 0;
+        ctx->perm_n = -1;
         RC(dev_alloc(ctx, &ctx->u, nnz, "alloc u"));
         RC(dev_alloc(ctx, &ctx->v, nnz, "alloc v"));
         RC(dev_alloc(ctx, &ctx->r, nnz, "alloc r"));
-        if (ctx->shuffle) RC(dev_alloc(ctx, &ctx->perm, nnz, "alloc perm"));
         ctx->cap_n = nnz;
     }
-    if (ctx->shuffle && !ctx->perm) RC(dev_alloc(ctx, &ctx->perm, nnz, "alloc perm"));
+    if (ctx->shuffle) {
+        RC(dev_alloc(ctx, &ctx->perm, nnz, "alloc perm"));
+        RC(dev_alloc(ctx, &ctx->stg_u, nnz, "alloc staging u"));
+        RC(dev_alloc(ctx, &ctx->stg_v, nnz, "alloc staging v"));
+        RC(dev_alloc(ctx, &ctx->stg_r, nnz, "alloc staging r"));
+    }
     RC(ctx->gather_q());
     ctx->drop_layouts();
     ctx->seg_valid = false;
     ctx->N = 0;
-    const bool dev_src = is_device_ptr(u);
-    const cudaMemcpyKind kind = dev_src ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
-    int32_t *su = ctx->u, *sv = ctx->v;
-    float *sr = ctx->r;
-    int32_t *tmp_u = nullptr, *tmp_v = nullptr;
-    float *tmp_r = nullptr;
-    if (ctx->shuffle) {  // stage unshuffled copy, then gather into the final buffers
-        CK(cudaMallocAsync((void **)&tmp_u, sizeof(int32_t) * nnz, st));
-        CK(cudaMallocAsync((void **)&tmp_v, sizeof(int32_t) * nnz, st));
-        CK(cudaMallocAsync((void **)&tmp_r, sizeof(float) * nnz, st));
-        su = tmp_u;
-        sv = tmp_v;
-        sr = tmp_r;
+    const cudaMemcpyKind kind = is_device_ptr(u) ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+    // shuffle: stage the caller's order, then one fused gather + validate + rebase kernel writes the
+    // A-8 order; no shuffle: copy in place and run the same kernel as validate + rebase.
+    int32_t *su = ctx->shuffle ? ctx->stg_u : ctx->u, *sv = ctx->shuffle ? ctx->stg_v : ctx->v;
+    float *sr = ctx->shuffle ? ctx->stg_r : ctx->r;
+    CK(cudaMemcpyAsync(su, u, sizeof(int32_t) * nnz, kind, st));
+    CK(cudaMemcpyAsync(sv, v, sizeof(int32_t) * nnz, kind, st));
+    CK(cudaMemcpyAsync(sr, r, sizeof(float) * nnz, kind, st));
+    if (ctx->shuffle && !(ctx->perm_n == nnz && ctx->perm_seed == ctx->seed_shuffle)) {
+        // the A-8 permutation depends only on (nnz, seed): computed once and cached
+        CK(launch_shuffle_perm(nnz, ctx->seed_shuffle, ctx->perm, st));
+        ctx->perm_n = nnz;
+        ctx->perm_seed = ctx->seed_shuffle;
     }
-    int rc = MF_OK;
-    auto cleanup = [&]() {
-        if (tmp_u) cudaFreeAsync(tmp_u, st);
-        if (tmp_v) cudaFreeAsync(tmp_v, st);
-        if (tmp_r) cudaFreeAsync(tmp_r, st);
-    };
-#define CKL(expr)                                   \
-    do {                                            \
-        rc = ctx->cuda((expr), #expr);              \
-        if (rc != MF_OK) { cleanup(); return rc; }  \
-    } while (0)
-    CKL(cudaMemcpyAsync(su, u, sizeof(int32_t) * nnz, kind, st));
-    CKL(cudaMemcpyAsync(sv, v, sizeof(int32_t) * nnz, kind, st));
-    CKL(cudaMemcpyAsync(sr, r, sizeof(float) * nnz, kind, st));
-    CKL(cudaMemsetAsync(ctx->scratch, 0, sizeof(DevScratch), st));
-    int64_t row_lo = ctx->p_begin, row_hi = ctx->p_end;
-    CKL(launch_validate_rows(su, sv, sr, nnz, row_lo, row_hi, ctx->n, ctx->scratch, st));
-    CKL(cudaMemcpyAsync(ctx->h_scratch, ctx->scratch, sizeof(DevScratch), cudaMemcpyDeviceToHost, st));
-    CKL(cudaStreamSynchronize(st));
-    if (ctx->h_scratch->bad) {
-        cleanup();
+    CK(cudaMemsetAsync(ctx->scratch, 0, sizeof(DevScratch), st));
+    CK(launch_gather_validate(su, sv, sr, ctx->shuffle ? ctx->perm : nullptr, nnz, ctx->p_begin, ctx->p_end, ctx->n,
+                              ctx->u, ctx->v, ctx->r, ctx->scratch, st));
+    CK(cudaMemcpyAsync(ctx->h_scratch, ctx->scratch, sizeof(DevScratch), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (ctx->h_scratch->bad)
         return ctx->fail(MF_EINVAL, "mf_load_coo: %llu samples with u outside [%lld,%lld), v outside [0,%lld) or non-finite r",
-                         (unsigned long long)ctx->h_scratch->bad, (long long)row_lo, (long long)row_hi, (long long)ctx->n);
-    }
-    if (row_lo != 0) CKL(launch_rebase(su, nnz, (int32_t)row_lo, st));  // P holds rows [row_lo, row_hi) only
-    if (ctx->shuffle) {
-        CKL(launch_shuffle(su, sv, sr, nnz, ctx->seed_shuffle, ctx->u, ctx->v, ctx->r, ctx->perm, st));
-        CKL(cudaStreamSynchronize(st));
-    }
-    cleanup();
-#undef CKL
+                         (unsigned long long)ctx->h_scratch->bad, (long long)ctx->p_begin, (long long)ctx->p_end,
+                         (long long)ctx->n);
     ctx->N = nnz;
     ctx->shuffled = ctx->shuffle;
     RC(ctx->ensure_factors());

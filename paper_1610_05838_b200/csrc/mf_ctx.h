@@ -31,6 +31,7 @@ struct mf_ctx {
     int shuffle = 1;
     int count_updates = 0;
     int partitions = 0;
+    int subepochs = 4;  // passes per epoch of the partitioned schedule (MF_OPT_SUBEPOCHS)
     int variant = 0;
     int trace = 0;
     cudaStream_t user_stream = nullptr;
@@ -49,6 +50,10 @@ struct mf_ctx {
     int32_t *u = nullptr, *v = nullptr;
     float *r = nullptr;
     uint32_t *perm = nullptr;  // perm[i] = caller index of stored sample i
+    int64_t perm_n = -1;       // perm is the A-8 permutation of perm_n samples under perm_seed (cached)
+    uint64_t perm_seed = 0;
+    int32_t *stg_u = nullptr, *stg_v = nullptr;  // staging copy of the caller's order (shuffle on)
+    float *stg_r = nullptr;
     int64_t N = 0, cap_n = 0;
     int shuffled = 0;
 
@@ -73,6 +78,7 @@ struct mf_ctx {
     bool part_valid = false;
     int part_G = 0;                  // partitions = world size (NCCL) or logical partitions (loopback)
     int part_local = 0;              // partitions hosted by this context (1 with NCCL, G in loopback)
+    int part_S = 1;                  // passes per epoch in the current layout
     int32_t *bu = nullptr, *bv = nullptr;  // samples bucketed by (local partition, column segment); v segment-local
     float *br = nullptr;
     std::vector<int64_t> h_blk_off;  // (part_local * G + 1) block offsets

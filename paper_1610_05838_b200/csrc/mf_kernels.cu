@@ -112,19 +112,44 @@ __global__ void __launch_bounds__(kBlock) k_hogwild(UpdateArgs a) {
     unsigned long long done = 0;
     int bad = 0;
 
-    for (;;) {
+    // Chunk claims run one chunk ahead and triple tiles one tile ahead, so neither the claim
+    // atomic nor the 3 x 128-byte triple loads sit on the per-rating critical path.
+    auto claim = [&]() -> int64_t {
         unsigned long long c = 0;
         if (lane == 0) c = atomicAdd(&a.scratch->chunk, 1ull);
-        c = __shfl_sync(0xffffffffu, c, 0);
-        const int64_t beg = (int64_t)c * f;
-        if (beg >= N) break;
-        const int64_t end = min(beg + (int64_t)f, N);
-        for (int64_t base = beg; base < end; base += 32) {
-            const int64_t i = base + lane;
-            const bool ok = i < end;
-            const int32_t tu = ok ? __ldg(a.u + i) : 0;
-            const int32_t tv = ok ? __ldg(a.v + i) : 0;
-            const float tr = ok ? __ldg(a.r + i) : 0.f;
+        return (int64_t)__shfl_sync(0xffffffffu, c, 0) * f;
+    };
+    int64_t base = claim();
+    int64_t next_chunk = claim();
+    if (base >= N) return;
+    int64_t end = min(base + (int64_t)f, N);
+    int32_t tu, tv;
+    float tr;
+    {
+        const int64_t i = base + lane;
+        const bool ok = i < end;
+        tu = ok ? __ldg(a.u + i) : 0;
+        tv = ok ? __ldg(a.v + i) : 0;
+        tr = ok ? __ldg(a.r + i) : 0.f;
+    }
+    for (;;) {
+        int64_t nbase = base + 32, nend = end;
+        if (nbase >= end) {  // next tile starts the chunk claimed one chunk ago; claim the one after
+            nbase = next_chunk;
+            nend = min(nbase + (int64_t)f, N);
+            if (nbase < N) next_chunk = claim();
+        }
+        const bool more = nbase < N;
+        int32_t nu = 0, nv = 0;
+        float nr = 0.f;
+        {
+            const int64_t i = nbase + lane;
+            const bool ok = more && i < nend;
+            nu = ok ? __ldg(a.u + i) : 0;
+            nv = ok ? __ldg(a.v + i) : 0;
+            nr = ok ? __ldg(a.r + i) : 0.f;
+        }
+        {
             const int cnt = (int)(end - base < 32 ? end - base : 32);
             if (a.count_updates) done += (lane == 0) ? cnt : 0;
 #pragma unroll 1
@@ -161,6 +186,12 @@ __global__ void __launch_bounds__(kBlock) k_hogwild(UpdateArgs a) {
                 }
             }
         }
+        if (!more) break;
+        base = nbase;
+        end = nend;
+        tu = nu;
+        tv = nv;
+        tr = nr;
     }
     if (bad) a.scratch->diverged = 1;
     if (a.count_updates && lane == 0 && done) atomicAdd(&a.scratch->updates, done);
@@ -183,6 +214,9 @@ static cudaError_t hogwild_launch(const UpdateArgs &a, int workers, cudaStream_t
     if (used) *used = (int)(groups * D);
     UpdateArgs args = a;
     args.active_groups = groups;
+    // every launch claims chunks from 0 (the partitioned path launches once per block)
+    cudaError_t e = cudaMemsetAsync(&a.scratch->chunk, 0, sizeof(unsigned long long), st);
+    if (e != cudaSuccess) return e;
     k_hogwild<SH, D><<<blocks, kBlock, 0, st>>>(args);
     return cudaGetLastError();
 }
@@ -454,8 +488,8 @@ cudaError_t launch_gather(const int32_t *u_in, const int32_t *v_in, const float 
     return cudaGetLastError();
 }
 
-cudaError_t launch_shuffle(const int32_t *u_in, const int32_t *v_in, const float *r_in, int64_t n, uint64_t seed,
-                           int32_t *u_out, int32_t *v_out, float *r_out, uint32_t *perm_out, cudaStream_t st) {
+// A-8 permutation only (data independent): keys, radix sort, perm_out[j] = original index
+cudaError_t launch_shuffle_perm(int64_t n, uint64_t seed, uint32_t *perm_out, cudaStream_t st) {
     if (n > (int64_t)0xFFFFFFFFll) return cudaErrorInvalidValue;
     uint64_t *k0 = nullptr, *k1 = nullptr;
     uint32_t *i0 = nullptr;
@@ -474,7 +508,6 @@ cudaError_t launch_shuffle(const int32_t *u_in, const int32_t *v_in, const float
     MF_TRY(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, k0, k1, i0, perm_out, n, 0, 64, st));
     MF_TRY(cudaMallocAsync(&tmp, tmp_bytes, st));
     MF_TRY(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, k0, k1, i0, perm_out, n, 0, 64, st));
-    MF_TRY(launch_gather(u_in, v_in, r_in, perm_out, n, u_out, v_out, r_out, st));
 done:
     if (tmp) cudaFreeAsync(tmp, st);
     if (k0) cudaFreeAsync(k0, st);
@@ -482,6 +515,33 @@ done:
     if (i0) cudaFreeAsync(i0, st);
 #undef MF_TRY
     return e;
+}
+
+// Fused load step: out[i] = in[idx[i]] (idx == nullptr: identity, may run in place), counting samples
+// with u outside [row_lo, row_hi), v outside [0, n_cols) or non-finite r; u is rebased by row_lo.
+__global__ void k_gather_validate(const int32_t *u_in, const int32_t *v_in, const float *r_in, const uint32_t *idx,
+                                  int64_t n, int64_t row_lo, int64_t row_hi, int64_t n_cols, int32_t *u_out,
+                                  int32_t *v_out, float *r_out, DevScratch *s) {
+    unsigned long long bad = 0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t j = idx ? (int64_t)idx[i] : i;
+        const int32_t a = u_in[j], b = v_in[j];
+        const float x = r_in[j];
+        bad += (a < row_lo || a >= row_hi || b < 0 || b >= n_cols || !isfinite(x)) ? 1 : 0;
+        u_out[i] = a - (int32_t)row_lo;
+        v_out[i] = b;
+        r_out[i] = x;
+    }
+    for (int o = 16; o > 0; o >>= 1) bad += __shfl_xor_sync(0xffffffffu, bad, o);
+    if ((threadIdx.x & 31) == 0 && bad) atomicAdd(&s->bad, bad);
+}
+cudaError_t launch_gather_validate(const int32_t *u_in, const int32_t *v_in, const float *r_in, const uint32_t *idx,
+                                   int64_t n, int64_t row_lo, int64_t row_hi, int64_t n_cols, int32_t *u_out,
+                                   int32_t *v_out, float *r_out, DevScratch *scratch, cudaStream_t st) {
+    const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 148 * 16));
+    k_gather_validate<<<blocks, 256, 0, st>>>(u_in, v_in, r_in, idx, n, row_lo, row_hi, n_cols, u_out, v_out, r_out,
+                                              scratch);
+    return cudaGetLastError();
 }
 
 }  // namespace mf

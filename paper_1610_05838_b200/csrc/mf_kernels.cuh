@@ -59,8 +59,10 @@ cudaError_t launch_to_f32(int storage, const void *X, float *dst, int64_t count,
 cudaError_t launch_validate_rows(const int32_t *u, const int32_t *v, const float *r, int64_t n, int64_t row_lo,
                                  int64_t row_hi, int64_t n_cols, DevScratch *scratch, cudaStream_t st);
 cudaError_t launch_rebase(int32_t *u, int64_t n, int32_t off, cudaStream_t st);
-cudaError_t launch_shuffle(const int32_t *u_in, const int32_t *v_in, const float *r_in, int64_t n, uint64_t seed,
-                           int32_t *u_out, int32_t *v_out, float *r_out, uint32_t *perm_out, cudaStream_t st);
+cudaError_t launch_shuffle_perm(int64_t n, uint64_t seed, uint32_t *perm_out, cudaStream_t st);
+cudaError_t launch_gather_validate(const int32_t *u_in, const int32_t *v_in, const float *r_in, const uint32_t *idx,
+                                   int64_t n, int64_t row_lo, int64_t row_hi, int64_t n_cols, int32_t *u_out,
+                                   int32_t *v_out, float *r_out, DevScratch *scratch, cudaStream_t st);
 cudaError_t launch_gather(const int32_t *u_in, const int32_t *v_in, const float *r_in, const uint32_t *idx, int64_t n,
                           int32_t *u_out, int32_t *v_out, float *r_out, cudaStream_t st);
 

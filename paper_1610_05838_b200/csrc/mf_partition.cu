@@ -47,11 +47,15 @@ __device__ __forceinline__ int seg_of(int64_t x, int64_t extent, int parts) {
     return g;
 }
 
+// block key = ((pass * local + row segment) * G + column segment); the pass of stored sample i is
+// floor(i * S / n), i.e. every epoch is S passes over consecutive slices of the shuffled order
 __global__ void k_part_keys(const int32_t *u, const int32_t *v, int64_t n, int64_t m_rows, int64_t n_cols, int G,
-                            int rows_split, uint32_t *keys, uint32_t *idx) {
+                            int rows_split, int S, uint32_t *keys, uint32_t *idx) {
+    const int local = rows_split ? G : 1;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
         const int rs = rows_split ? seg_of(u[i], m_rows, G) : 0;
-        keys[i] = (uint32_t)(rs * G + seg_of(v[i], n_cols, G));
+        const int s = (int)((i * S) / n);
+        keys[i] = (uint32_t)(((int64_t)s * local + rs) * G + seg_of(v[i], n_cols, G));
         idx[i] = (uint32_t)i;
     }
 }
@@ -209,7 +213,9 @@ int mf_ctx::build_partition() {
     seg_valid = false;
 
     cudaStream_t st = stream();
-    const int64_t nb = (int64_t)local * G;
+    const int S = (int)std::max<int64_t>(1, std::min<int64_t>(subepochs, std::max<int64_t>(1, N)));
+    const int64_t nb = (int64_t)S * local * G;
+    if (nb >= (1ll << 31)) return fail(MF_EINVAL, "partitioned: too many blocks (S * G * G)");
     uint32_t *k0 = nullptr, *k1 = nullptr, *i0 = nullptr, *i1 = nullptr;
     int64_t *doff = nullptr;
     void *tmp = nullptr;
@@ -224,7 +230,7 @@ int mf_ctx::build_partition() {
     CK(cudaMallocAsync((void **)&doff, sizeof(int64_t) * (nb + 1), st));
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((N + 255) / 256, 148 * 16));
     // loopback: rows are global, split into G segments; NCCL: u is already local to this rank's segment
-    k_part_keys<<<grid, 256, 0, st>>>(u, v, N, m, n, G, is_distributed() ? 0 : 1, k0, i0);
+    k_part_keys<<<grid, 256, 0, st>>>(u, v, N, m, n, G, is_distributed() ? 0 : 1, S, k0, i0);
     CK(cudaGetLastError());
     int bits = 1;
     while (bits < 32 && (1ull << bits) < (uint64_t)nb) bits++;
@@ -250,6 +256,7 @@ int mf_ctx::build_partition() {
     if (is_distributed() && !comm_stream) CK(cudaStreamCreateWithFlags(&comm_stream, cudaStreamNonBlocking));
     part_G = G;
     part_local = local;
+    part_S = S;
     held.assign(G, -1);
     part_valid = true;
     return MF_OK;
@@ -336,42 +343,45 @@ int mf_ctx::epoch_partitioned(mf_epoch_stats *stats) {
     if (rc != MF_OK) return rc;
     const int G = part_G;
     cudaStream_t st = stream();
+    const int S = part_S, L = part_local;
     const float eta = eta_at(epoch);
-    std::vector<int32_t> pi, want(G);
-    round_perm(pi, seed_shuffle, epoch, G);
-    for (int g = 0; g < G; g++) want[g] = sigma(pi, G, g, 0);
+    const ShapeId sh = select_shape(k, storage, variant & 0xF);
+    auto blk = [&](int s, int li, int c) { return ((size_t)s * L + li) * G + c; };
+    std::vector<int64_t> n_local(L, 0);  // samples of each hosted partition per epoch (worker clamp, A-10)
+    for (int s = 0; s < S; s++)
+        for (int li = 0; li < L; li++) n_local[li] += h_blk_off[blk(s, li, G - 1) + 1] - h_blk_off[blk(s, li, 0)];
+    int launches = 0, used_max = 0;
     CK(cudaEventRecord(events[0], st));
     CK(cudaMemsetAsync(scratch, 0, sizeof(DevScratch), st));
-    if (!seg_valid) rc = scatter_segments(this, want);
-    else rc = exchange_segments(want);
-    if (rc != MF_OK) return rc;
-    full_valid = false;
-    const ShapeId sh = select_shape(k, storage, variant & 0xF);
-    int launches = 0, used_max = 0;
     CK(cudaEventRecord(events[1], st));
-    for (int r = 0; r < G; r++) {
-        for (int li = 0; li < part_local; li++) {
-            const int g = is_distributed() ? rank : li;
-            const int c = sigma(pi, G, g, r);
-            const int64_t lo = h_blk_off[(size_t)li * G + c], hi = h_blk_off[(size_t)li * G + c + 1];
-            if (hi <= lo) continue;
-            UpdateArgs a = update_args(eta);
-            a.u = bu + lo;
-            a.v = bv + lo;
-            a.r = br + lo;
-            a.n = hi - lo;
-            a.Q = q_cur[li];
-            const int64_t n_local = h_blk_off[(size_t)(li + 1) * G] - h_blk_off[(size_t)li * G];
-            const int w = workers > 0 ? workers : (int)std::max<int64_t>(1, std::min<int64_t>(n_local / 10000, 1 << 30));
-            int used = 0;
-            CK(launch_hogwild(sh, a, w, variant, st, &used));
-            used_max = std::max(used_max, used);
-            launches++;
-        }
-        if (r + 1 < G) {
-            for (int g = 0; g < G; g++) want[g] = sigma(pi, G, g, r + 1);
-            rc = exchange_segments(want);
+    std::vector<int32_t> pi, want(G);
+    // an epoch is S passes; pass s of epoch e runs the G rounds of Latin square pi_{eS+s}
+    for (int s = 0; s < S; s++) {
+        const int32_t pass = epoch * S + s;
+        round_perm(pi, seed_shuffle, pass, G);
+        for (int r = 0; r < G; r++) {
+            for (int g = 0; g < G; g++) want[g] = sigma(pi, G, g, r);
+            rc = seg_valid ? exchange_segments(want) : scatter_segments(this, want);
             if (rc != MF_OK) return rc;
+            full_valid = false;
+            for (int li = 0; li < L; li++) {
+                const int g = is_distributed() ? rank : li;
+                const size_t b = blk(s, li, want[g]);
+                const int64_t lo = h_blk_off[b], hi = h_blk_off[b + 1];
+                if (hi <= lo) continue;
+                UpdateArgs a = update_args(eta);
+                a.u = bu + lo;
+                a.v = bv + lo;
+                a.r = br + lo;
+                a.n = hi - lo;
+                a.Q = q_cur[li];
+                const int w = workers > 0 ? workers
+                                          : (int)std::max<int64_t>(1, std::min<int64_t>(n_local[li] / 10000, 1 << 30));
+                int used = 0;
+                CK(launch_hogwild(sh, a, w, variant, st, &used));
+                used_max = std::max(used_max, used);
+                launches++;
+            }
         }
     }
     CK(cudaEventRecord(events[2], st));

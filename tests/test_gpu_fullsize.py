@@ -1,0 +1,95 @@
+"""Full-size Netflix-shaped parity (BASELINE.json configs[1], N = 99,072,112, k = 128).  -m gpu.
+
+The oracle needs ~2 min (fp32) / ~8 min (fp16) per serial epoch at this size, so its results are
+golden files written on the dev box by committed scripts that call only oracle/ and datagen/:
+  tests/golden/C2_<st>_trace.json        scripts/make_golden.py       (test RMSE per epoch, 20 epochs)
+  tests/golden/C2_<st>_epoch1_rows.npz   scripts/make_golden_rows.py  (sampled rows after epoch 1)
+The GPU runs in the launch configuration bench.py times (default workers / variant).
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+
+import datagen
+import oracle
+
+pytestmark = pytest.mark.gpu
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+TOL = {"f32": 1e-5, "f16": 2e-3}
+
+
+@pytest.fixture(scope="module")
+def c2():
+    cfg = datagen.CONFIGS["C2"]
+    return cfg, datagen.make(cfg)
+
+
+def _ctx(cfg, storage, **kw):
+    from paper_1610_05838_b200 import mf
+    variant = 16 if storage != "f32" else 0   # bench.py's default launch configuration
+    return mf.MF(cfg.m, cfg.n, cfg.k, cfg.alpha, cfg.lam, cfg.seed_init, storage=storage, beta=cfg.beta,
+                 seed_shuffle=cfg.seed_shuffle, variant=variant, **kw)
+
+
+@pytest.mark.parametrize("storage", ["f32", "f16"])
+def test_c2_hogwild_rmse_trace_vs_oracle_golden(c2, storage):
+    path = os.path.join(GOLD, f"C2_{storage}_trace.json")
+    if not os.path.exists(path):
+        pytest.skip(f"{path} not generated yet")
+    gold = json.load(open(path))["rmse"]
+    cfg, ((u, v, r), test) = c2
+    with _ctx(cfg, storage, count_updates=1) as g:
+        g.load(u, v, r)
+        got = []
+        for t in range(len(gold)):
+            st = g.epoch("hogwild")
+            assert st.updates == len(u)
+            got.append(g.rmse(*test))
+    # north star: every schedule's test RMSE within 0.5% of the oracle's after the same epochs
+    assert abs(got[-1] - gold[-1]) <= 0.005 * gold[-1], (got[-1], gold[-1])
+    assert all(b < a for a, b in zip(got, got[1:]))  # decaying schedule: monotone test RMSE here
+
+
+@pytest.mark.parametrize("storage", ["f32", "f16"])
+def test_c2_deterministic_epoch_sampled_rows(c2, storage):
+    path = os.path.join(GOLD, f"C2_{storage}_epoch1_rows.npz")
+    if not os.path.exists(path):
+        pytest.skip(f"{path} not generated yet")
+    gold = np.load(path)
+    cfg, ((u, v, r), _) = c2
+    from paper_1610_05838_b200 import mf
+    with _ctx(cfg, storage) as g:
+        g.load(u, v, r)
+        assert mf.mf_wave_count(g.h) == int(gold["nwaves"])
+        g.epoch("deterministic")
+        P, Q = g.factors()
+    for X, key in ((P, "P"), (Q, "Q")):
+        rows = X[gold[f"{key[0].lower()}_idx"]]
+        ref = gold[f"{key}_rows"]
+        assert np.linalg.norm(rows - ref) / np.linalg.norm(ref) <= TOL[storage]
+        assert np.linalg.norm(X.astype(np.float64)) == pytest.approx(float(gold[f"{key}_fro"]), rel=TOL[storage])
+
+
+def test_c2_rmse_kernel_full_test_set(c2):
+    """mf_rmse over the full 1.4M test set == oracle RMSE (fp64 dot) on the same factors."""
+    cfg, ((u, v, r), test) = c2
+    with _ctx(cfg, "f32") as g:
+        g.load(u, v, r)
+        g.epoch("hogwild")
+        P, Q = g.factors()
+        got = g.rmse(*test)
+    ref = oracle.Model(cfg.m, cfg.n, cfg.k, oracle.F32, P=P, Q=Q).rmse(*test)
+    assert got == pytest.approx(ref, rel=1e-6)
+
+
+def test_c2_exactly_once_and_order(c2):
+    """Full-size load: the A-8 order equals the oracle's permutation; one epoch touches every sample once."""
+    cfg, ((u, v, r), _) = c2
+    with _ctx(cfg, "f16", count_updates=1) as g:
+        g.load(u, v, r)
+        np.testing.assert_array_equal(g.order(), oracle.shuffle_perm(cfg.seed_shuffle, len(u)))
+        assert g.epoch("hogwild").updates == len(u)
+        g.load(u, v, r)  # second load reuses the cached permutation and buffers
+        np.testing.assert_array_equal(g.order()[:1000], oracle.shuffle_perm(cfg.seed_shuffle, len(u))[:1000])

@@ -19,17 +19,21 @@ def mf():
     return mf
 
 
-def _block_sweep_order(mf, perm, u, v, m, n, G, seed, e):
-    """Stored positions in processing order: round -> partition -> block samples in stored order."""
+def _block_sweep_order(mf, perm, u, v, m, n, G, seed, e, S=4):
+    """Caller indices in processing order: pass s (stored positions [s N/S, (s+1) N/S)) -> round ->
+    partition -> block samples in stored order; pass s of epoch e uses Latin square e*S + s."""
     us, vs = u[perm], v[perm]
+    N = len(perm)
+    pas = (np.arange(N) * S) // N
     rs = [mf.mf_segment(m, G, g) for g in range(G)]
     cs = [mf.mf_segment(n, G, c) for c in range(G)]
     out = []
-    for rnd in range(G):
-        for g in range(G):
-            c = mf.mf_round_segment(seed, e, G, rnd, g)
-            sel = (us >= rs[g][0]) & (us < rs[g][1]) & (vs >= cs[c][0]) & (vs < cs[c][1])
-            out.append(perm[np.nonzero(sel)[0]])
+    for s in range(S):
+        for rnd in range(G):
+            for g in range(G):
+                c = mf.mf_round_segment(seed, e * S + s, G, rnd, g)
+                sel = (pas == s) & (us >= rs[g][0]) & (us < rs[g][1]) & (vs >= cs[c][0]) & (vs < cs[c][1])
+                out.append(perm[np.nonzero(sel)[0]])
     return np.concatenate(out)
 
 
