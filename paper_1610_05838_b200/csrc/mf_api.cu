@@ -286,7 +286,7 @@ extern "C" int mf_set_option(mf_ctx *ctx, int key, double value) {
             ctx->trace = iv ? 1 : 0;
             return MF_OK;
         case MF_OPT_SUBEPOCHS:
-            if (iv < 1 || iv > 4096) return ctx->fail(MF_EINVAL, "subepochs must be in [1, 4096]");
+            if (iv < 0 || iv > 4096) return ctx->fail(MF_EINVAL, "subepochs must be in [0 (auto), 4096]");
             ctx->subepochs = (int)iv;
             ctx->part_valid = false;
             return MF_OK;

@@ -31,7 +31,7 @@ struct mf_ctx {
     int shuffle = 1;
     int count_updates = 0;
     int partitions = 0;
-    int subepochs = 4;  // passes per epoch of the partitioned schedule (MF_OPT_SUBEPOCHS)
+    int subepochs = 0;  // passes per epoch of the partitioned schedule (MF_OPT_SUBEPOCHS; 0 = max(4, G))
     int variant = 0;
     int trace = 0;
     cudaStream_t user_stream = nullptr;

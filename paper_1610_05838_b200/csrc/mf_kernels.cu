@@ -158,6 +158,7 @@ __global__ void __launch_bounds__(kBlock) k_hogwild(UpdateArgs a) {
                 float sr[D];
                 bool val[D];
                 RowRaw<SH> pr[D], qr[D];
+                float pf[D][SH::E], qf[D][SH::E], dot[D];
 #pragma unroll
                 for (int d = 0; d < D; d++) {
                     const int s = (j0 + d) * gper + grp;
@@ -173,14 +174,18 @@ __global__ void __launch_bounds__(kBlock) k_hogwild(UpdateArgs a) {
                 }
 #pragma unroll
                 for (int d = 0; d < D; d++) {
-                    float p[SH::E], q[SH::E];
-                    widen_row<SH>(pr[d], p);
-                    widen_row<SH>(qr[d], q);
-                    const float err = sr[d] - group_dot<SH>(p, q);
+                    widen_row<SH>(pr[d], pf[d]);
+                    widen_row<SH>(qr[d], qf[d]);
+                    dot[d] = lane_dot<SH>(pf[d], qf[d]);
+                }
+                group_allreduce<SH, D>(dot);
+#pragma unroll
+                for (int d = 0; d < D; d++) {
+                    const float err = sr[d] - dot[d];
                     if (val[d] && !isfinite(err)) bad = 1;
-                    sgd_step<SH>(p, q, err, a.eta, a.lam);
-                    narrow_row<SH>(p, pr[d]);
-                    narrow_row<SH>(q, qr[d]);
+                    sgd_step<SH>(pf[d], qf[d], err, a.eta, a.lam);
+                    narrow_row<SH>(pf[d], pr[d]);
+                    narrow_row<SH>(qf[d], qr[d]);
                     store_row<SH>(a.P, su[d], k, sub, val[d], pr[d]);
                     store_row<SH>(a.Q, sv[d], k, sub, val[d], qr[d]);
                 }

@@ -213,7 +213,10 @@ int mf_ctx::build_partition() {
     seg_valid = false;
 
     cudaStream_t st = stream();
-    const int S = (int)std::max<int64_t>(1, std::min<int64_t>(subepochs, std::max<int64_t>(1, N)));
+    // passes per epoch: auto = max(4, G) (serial block-sweep simulation on C2-1pct, 10 epochs:
+    // S = 1 costs +10..+20% test RMSE vs the shuffled serial order; S = max(4, G) is within 0.05%)
+    const int S_req = subepochs > 0 ? subepochs : std::max(4, G);
+    const int S = (int)std::max<int64_t>(1, std::min<int64_t>(S_req, std::max<int64_t>(1, N)));
     const int64_t nb = (int64_t)S * local * G;
     if (nb >= (1ll << 31)) return fail(MF_EINVAL, "partitioned: too many blocks (S * G * G)");
     uint32_t *k0 = nullptr, *k1 = nullptr, *i0 = nullptr, *i1 = nullptr;
