@@ -116,13 +116,20 @@ def run_reference(a, cfg):
     if rank != 0:
         return
     st = oracle.STORAGE_NAME[a.storage]
+    G = int(os.environ.get("WORLD_SIZE", "1"))
+    # the same workload as our arm (for G > 1: rank 0's Netflix-shaped shard, which is generated
+    # exactly like the G = 1 problem; the factors are full size, m x G rows)
     (u, v, r), test = datagen.make(cfg)
-    sample = a.ref_sample
-    m = oracle.Model(cfg.m, cfg.n, cfg.k, st, seed=cfg.seed_init)
+    m = oracle.Model(cfg.m * G, cfg.n, cfg.k, st, seed=cfg.seed_init)
     eta = oracle.eta(cfg.alpha, cfg.beta, 0)
+    # bound the run: size each step so warmup + steps take ~2 minutes on this core
+    t0 = time.perf_counter()
+    m.epoch(u[:50_000], v[:50_000], r[:50_000], eta, cfg.lam)
+    speed = 50_000 / (time.perf_counter() - t0)
+    sample = int(min(a.ref_sample, max(10_000, speed * 120.0 / (a.warmup + a.steps))))
     times = []
     for i in range(a.warmup + a.steps):
-        lo = (i * sample) % (len(u) - sample)
+        lo = (i * sample) % max(1, len(u) - sample)
         t0 = time.perf_counter()
         m.epoch(u[lo:lo + sample], v[lo:lo + sample], r[lo:lo + sample], eta, cfg.lam)
         dt = time.perf_counter() - t0
@@ -130,16 +137,34 @@ def run_reference(a, cfg):
             times.append(dt)
     tot = sum(times)
     val = a.steps * sample / tot
+    desc = f"{sample} consecutive shuffled samples of {cfg.name} per step, full-size P/Q, {a.storage} storage"
     out = {"metric": "sgd_updates_per_sec", "value": val, "unit": "updates/s", "n_gpus": a.gpus,
            "steps": a.steps, "warmup": a.warmup, "ms_per_step": 1e3 * tot / a.steps, "higher_is_better": True,
            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "storage": a.storage, "data": "synthetic",
            "impl": "reference",
-           "config": {"workload": f"{cfg.name} (Netflix-shaped, Table 2) m={cfg.m} n={cfg.n} k={cfg.k}",
-                      "schedule": "serial", "sample_per_step": sample},
-           "cpu_baseline": {"value": val, "unit": "updates/s", "cores": 1, "kind": "oracle",
-                            "sample": f"{sample} consecutive shuffled samples of {cfg.name} per step, full-size P/Q"},
+           "config": workload_config(cfg, G, a.storage, a.schedule if G == 1 else "partitioned"),
+           "arm": {"what": "serial C++ oracle (oracle/mf_oracle.cpp), 1 core", "sample_per_step": sample},
+           "cpu_baseline": {"value": val, "unit": "updates/s", "cores": 1, "kind": "oracle", "sample": desc},
            "e2e": {"value": val, "unit": "updates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out), flush=True)
+
+
+def workload_config(cfg, G, storage, schedule):
+    """The `config` object, identical for both arms of the same run."""
+    b = 4 if storage == "f32" else 2
+    if G == 1:
+        return {"workload": f"{cfg.name}: Netflix-shaped (PAPER.md Table 2) m={cfg.m} n={cfg.n} "
+                            f"N={cfg.n_train} k={cfg.k}, planted rank-8 synthetic ratings",
+                "schedule": schedule, "storage": storage, "alpha": cfg.alpha, "beta": cfg.beta, "lambda": cfg.lam,
+                "l2": "inputs larger than L2 (R %.2f GB, P %.0f MB); no flush" % (12 * cfg.n_train / 1e9,
+                                                                                  cfg.m * cfg.k * b / 1e6),
+                "step": "one epoch over all N ratings (mf_epoch) + test RMSE (mf_rmse)"}
+    return {"workload": f"{cfg.name} rows x {G}: m={cfg.m * G} n={cfg.n} N={cfg.n_train * G} k={cfg.k} "
+                        f"(one Netflix-shaped row segment per GPU)",
+            "schedule": "partitioned (S passes x G rounds of G x G Latin-square blocks, NCCL Q rotation)",
+            "storage": storage, "parallelism": f"P row segments x rotating Q segments over {G} GPUs",
+            "alpha": cfg.alpha, "beta": cfg.beta, "lambda": cfg.lam, "l2": "inputs larger than L2; no flush",
+            "step": "one epoch (mf_epoch partitioned) + test RMSE (mf_rmse, collective)"}
 
 
 def cpu_baseline(cfg, storage, u, v, r, budget_s=12.0):
@@ -272,13 +297,8 @@ def main():
         "metric": "sgd_updates_per_sec", "value": value, "unit": "updates/s", "n_gpus": 1, "steps": a.steps,
         "warmup": a.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "f32", "storage": a.storage, "data": "synthetic",
-        "config": {"workload": f"{cfg.name}: Netflix-shaped (PAPER.md Table 2) m={cfg.m} n={cfg.n} "
-                               f"N={N} k={cfg.k}, planted rank-8 synthetic ratings",
-                   "schedule": a.schedule, "storage": a.storage, "workers": workers, "batch_f": 256,
-                   "alpha": cfg.alpha, "beta": cfg.beta, "lambda": cfg.lam,
-                   "l2": "inputs larger than L2 (R %.2f GB, P %.0f MB); no flush" % (12 * N / 1e9,
-                         cfg.m * cfg.k * (4 if a.storage == 'f32' else 2) / 1e6),
-                   "step": "mf_epoch (N updates) + mf_rmse (test set)"},
+        "config": workload_config(cfg, 1, a.storage, a.schedule),
+        "arm": {"workers": workers, "batch_f": 256, "variant": variant},
         "test_rmse": rmses[-1],
         "roofline": roof,
         "cpu_baseline": cpu,
@@ -384,11 +404,7 @@ def run_partitioned(a, cfg, rank, world, local):
             "metric": "sgd_updates_per_sec", "value": value, "unit": "updates/s", "n_gpus": G, "steps": a.steps,
             "warmup": a.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f32", "storage": a.storage, "data": "synthetic",
-            "config": {"workload": f"{cfg.name} rows x {G}: m={m_glob} n={cfg.n} N={int(n_tot)} k={cfg.k} "
-                                   f"(Netflix-shaped row segment per GPU)",
-                       "schedule": "partitioned (G x G blocks, Latin-square rounds, NCCL Q rotation)",
-                       "parallelism": f"P row segments x rotating Q segments over {G} GPUs",
-                       "l2": "inputs larger than L2; no flush", "step": "mf_epoch (partitioned) + mf_rmse"},
+            "config": workload_config(cfg, G, a.storage, "partitioned"),
             "test_rmse": rm,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                          "traffic": None, "peak_kind": peak_kind, "kernel": "k_hogwild (rank 0, all rounds)",

@@ -290,6 +290,11 @@ extern "C" int mf_set_option(mf_ctx *ctx, int key, double value) {
             ctx->subepochs = (int)iv;
             ctx->part_valid = false;
             return MF_OK;
+        case MF_OPT_WAVE_CTA:
+            if (iv < 0 || iv > 1) return ctx->fail(MF_EINVAL, "wave cta must be 0 or 1");
+            ctx->wave_cta = (int)iv;
+            ctx->wf_valid = false;
+            return MF_OK;
         default:
             return ctx->fail(MF_EINVAL, "unknown option %d", key);
     }
@@ -302,8 +307,8 @@ extern "C" int mf_get_option(const mf_ctx *ctx, int key, double *value) {
         case MF_OPT_BETA: *value = ctx->beta; return MF_OK;
         case MF_OPT_WORKERS: *value = ctx->workers; return MF_OK;
         case MF_OPT_BATCH_F: *value = ctx->batch_f; return MF_OK;
-        case MF_OPT_WAVE_ROWS: *value = ctx->wave_rows; return MF_OK;
-        case MF_OPT_WAVE_COLS: *value = ctx->wave_cols; return MF_OK;
+        case MF_OPT_WAVE_ROWS: *value = ctx->wave_rows ? ctx->wave_rows : ctx->wf_s; return MF_OK;  // effective
+        case MF_OPT_WAVE_COLS: *value = ctx->wave_cols ? ctx->wave_cols : ctx->wf_c; return MF_OK;
         case MF_OPT_DEVICE: *value = ctx->device; return MF_OK;
         case MF_OPT_STREAM: *value = (double)(uintptr_t)ctx->user_stream; return MF_OK;
         case MF_OPT_SHUFFLE: *value = ctx->shuffle; return MF_OK;
@@ -314,7 +319,8 @@ extern "C" int mf_get_option(const mf_ctx *ctx, int key, double *value) {
         case MF_OPT_SEED_SHUFFLE: *value = (double)ctx->seed_shuffle; return MF_OK;
         case MF_OPT_VARIANT: *value = ctx->variant; return MF_OK;
         case MF_OPT_TRACE: *value = ctx->trace; return MF_OK;
-        case MF_OPT_SUBEPOCHS: *value = ctx->subepochs; return MF_OK;
+        case MF_OPT_SUBEPOCHS: *value = ctx->subepochs ? ctx->subepochs : ctx->part_S; return MF_OK;
+        case MF_OPT_WAVE_CTA: *value = ctx->wave_cta; return MF_OK;
         default: return MF_EINVAL;
     }
 }

@@ -65,6 +65,8 @@ struct WfArgs {
     DevScratch *scratch;
     int s, c, k, latin, count_updates;
     float eta, lam;
+    int64_t grp_w;        // column group width (the last group takes the remainder)
+    int64_t n_cols;
 };
 
 __device__ __forceinline__ int64_t globaltimer() {
@@ -166,6 +168,175 @@ __global__ void __launch_bounds__(kBlock) k_wavefront(WfArgs a) {
     if (a.count_updates && lane == 0 && done) atomicAdd(&a.scratch->updates, done);
 }
 
+// ------------------------------------------------------------ CTA workers --
+// MF_OPT_WAVE_CTA = 1: worker = one CTA of 1024 threads (one per SM).  While it holds column group c
+// the group's Q rows are staged in shared memory, so every rating of the block reads and writes q_v
+// on chip and only p_u (and the triple) crosses L2 -- half the L2 traffic of the warp-worker form.
+// Inside the block the CTA's warps claim 32-sample tiles and update lock-free (batch-Hogwild! inside
+// a block: P rows of the band and Q rows of the group are owned by this CTA alone).  The group is
+// copied back to global memory before the column lock is released.
+constexpr int kCtaThreads = 1024;
+
+template <int VB>
+__device__ __forceinline__ void smem_ld(const unsigned char *p, uint32_t (&w)[Vec<VB>::NW]) {
+    if constexpr (VB == 16) {
+        const uint4 x = *reinterpret_cast<const uint4 *>(p);
+        w[0] = x.x; w[1] = x.y; w[2] = x.z; w[3] = x.w;
+    } else if constexpr (VB == 8) {
+        const uint2 x = *reinterpret_cast<const uint2 *>(p);
+        w[0] = x.x; w[1] = x.y;
+    } else if constexpr (VB == 4) {
+        w[0] = *reinterpret_cast<const uint32_t *>(p);
+    } else {
+        w[0] = *reinterpret_cast<const unsigned short *>(p);
+    }
+}
+template <int VB>
+__device__ __forceinline__ void smem_st(unsigned char *p, const uint32_t (&w)[Vec<VB>::NW]) {
+    if constexpr (VB == 16) {
+        *reinterpret_cast<uint4 *>(p) = make_uint4(w[0], w[1], w[2], w[3]);
+    } else if constexpr (VB == 8) {
+        *reinterpret_cast<uint2 *>(p) = make_uint2(w[0], w[1]);
+    } else if constexpr (VB == 4) {
+        *reinterpret_cast<uint32_t *>(p) = w[0];
+    } else {
+        *reinterpret_cast<unsigned short *>(p) = (unsigned short)(w[0] & 0xFFFFu);
+    }
+}
+
+// block-wide copy of nbytes (a multiple of 2) between global and shared memory
+__device__ __forceinline__ void cta_copy_in(unsigned char *dst, const unsigned char *src, int64_t nbytes) {
+    if (((nbytes | (int64_t)(uintptr_t)src) & 15) == 0) {
+        for (int64_t i = threadIdx.x; i < nbytes / 16; i += blockDim.x)
+            reinterpret_cast<uint4 *>(dst)[i] = __ldcg(reinterpret_cast<const uint4 *>(src) + i);
+    } else {
+        for (int64_t i = threadIdx.x; i < nbytes / 2; i += blockDim.x)
+            reinterpret_cast<unsigned short *>(dst)[i] = __ldcg(reinterpret_cast<const unsigned short *>(src) + i);
+    }
+}
+__device__ __forceinline__ void cta_copy_out(unsigned char *dst, const unsigned char *src, int64_t nbytes) {
+    if (((nbytes | (int64_t)(uintptr_t)dst) & 15) == 0) {
+        for (int64_t i = threadIdx.x; i < nbytes / 16; i += blockDim.x)
+            __stcg(reinterpret_cast<uint4 *>(dst) + i, reinterpret_cast<const uint4 *>(src)[i]);
+    } else {
+        for (int64_t i = threadIdx.x; i < nbytes / 2; i += blockDim.x)
+            __stcg(reinterpret_cast<unsigned short *>(dst) + i, reinterpret_cast<const unsigned short *>(src)[i]);
+    }
+}
+
+template <class SH>
+__global__ void __launch_bounds__(kCtaThreads, 1) k_wavefront_cta(WfArgs a) {
+    extern __shared__ __align__(16) unsigned char qs[];
+    __shared__ int s_col, s_next;
+    constexpr int L = SH::L, G = SH::G;
+    const int lane = threadIdx.x & 31, grp = lane / L, sub = lane % L;
+    const int w = blockIdx.x;
+    if (w >= a.s) return;  // CTA-uniform
+    const int k = SH::FULL ? SH::KMAX : a.k;
+    const int64_t row_bytes = (int64_t)k * SH::BYTES;
+    const int c = a.c;
+    int bad = 0;
+    unsigned long long done = 0;
+    for (int j = 0; j < c; j++) {
+        if (threadIdx.x == 0) {
+            const int col = a.latin ? a.seq[(a.seq[c + w] + j) % c] : a.seq[(int64_t)w * c + j];
+            while (atomicCAS(a.locks + col, 0, 1) != 0) __nanosleep(64);
+            __threadfence();  // acquire
+            s_col = col;
+            s_next = 0;
+        }
+        __syncthreads();
+        const int col = s_col;
+        const int64_t q0 = (int64_t)col * a.grp_w;
+        const int64_t nrows = col == c - 1 ? a.n_cols - q0 : a.grp_w;
+        const unsigned char *qg = reinterpret_cast<const unsigned char *>(a.Q) + q0 * row_bytes;
+        cta_copy_in(qs, qg, nrows * row_bytes);
+        __syncthreads();
+        const int64_t t0 = a.trace ? globaltimer() : 0;
+        const int64_t blk = (int64_t)w * c + col;
+        const int64_t lo = a.off[blk], hi = a.off[blk + 1];
+        for (;;) {
+            int t = 0;
+            if (lane == 0) t = atomicAdd(&s_next, 32);
+            t = __shfl_sync(0xffffffffu, t, 0);
+            const int64_t base = lo + t;
+            if (base >= hi) break;  // warp-uniform
+            const int64_t i = base + lane;
+            const bool ok = i < hi;
+            const int32_t tu = ok ? __ldg(a.u + i) : 0;
+            const int32_t tv = ok ? (int32_t)(__ldg(a.v + i) - q0) : 0;
+            const float tr = ok ? __ldg(a.r + i) : 0.f;
+            const int cnt = (int)(hi - base < 32 ? hi - base : 32);
+            if (lane == 0) done += cnt;
+#pragma unroll 1
+            for (int jj = 0; jj < 32 / G; jj++) {
+                const int s = jj * G + grp;
+                const int32_t su = __shfl_sync(0xffffffffu, tu, s);
+                const int32_t sv = __shfl_sync(0xffffffffu, tv, s);
+                const float sr = __shfl_sync(0xffffffffu, tr, s);
+                const bool val = s < cnt;
+                RowRaw<SH> pr, qr;
+                load_row<SH>(a.P, su, k, sub, val, pr);
+                unsigned char *qrow = qs + (int64_t)sv * row_bytes;
+#pragma unroll
+                for (int jv = 0; jv < SH::V; jv++) {
+                    const int64_t e = vec_elem<SH>(jv, sub);
+                    if (val && (SH::FULL || e < k)) smem_ld<SH::VB>(qrow + e * SH::BYTES, qr.w[jv]);
+                    else
+#pragma unroll
+                        for (int x = 0; x < SH::NW; x++) qr.w[jv][x] = 0u;
+                }
+                float p[SH::E], q[SH::E];
+                widen_row<SH>(pr, p);
+                widen_row<SH>(qr, q);
+                const float err = sr - group_dot<SH>(p, q);
+                if (val && !isfinite(err)) bad = 1;
+                sgd_step<SH>(p, q, err, a.eta, a.lam);
+                narrow_row<SH>(p, pr);
+                narrow_row<SH>(q, qr);
+                store_row<SH>(a.P, su, k, sub, val, pr);
+#pragma unroll
+                for (int jv = 0; jv < SH::V; jv++) {
+                    const int64_t e = vec_elem<SH>(jv, sub);
+                    if (val && (SH::FULL || e < k)) smem_st<SH::VB>(qrow + e * SH::BYTES, qr.w[jv]);
+                }
+            }
+        }
+        __syncthreads();
+        cta_copy_out(reinterpret_cast<unsigned char *>(a.Q) + q0 * row_bytes, qs, nrows * row_bytes);
+        if (a.trace && threadIdx.x == 0) {
+            int64_t *tr = a.trace + 4 * blk;
+            tr[0] = w;
+            tr[1] = blk;
+            tr[2] = t0;
+            tr[3] = globaltimer();
+        }
+        __threadfence();  // release: P and Q stores of this block before the unlock
+        __syncthreads();
+        if (threadIdx.x == 0) atomicExch(a.locks + col, 0);
+    }
+    if (bad) a.scratch->diverged = 1;
+    if (a.count_updates && lane == 0 && done) atomicAdd(&a.scratch->updates, done);
+}
+
+template <class F>
+cudaError_t dispatch_cta_shape(const ShapeId &s, F &&f) {
+#define MF_CCASE(S_, L_, V_, VB_, FULL_)                                                             \
+    if (s.storage == S_ && s.L == L_ && s.V == V_ && s.VB == VB_ && s.full == FULL_)                \
+        return f(Shape<S_, L_, V_, VB_, (bool)FULL_>{});
+    MF_CCASE(kF32, 8, 1, 16, 1) MF_CCASE(kF32, 16, 1, 16, 1) MF_CCASE(kF32, 32, 1, 16, 1)
+    MF_CCASE(kF32, 32, 2, 16, 1) MF_CCASE(kF16, 4, 1, 16, 1) MF_CCASE(kF16, 8, 1, 16, 1)
+    MF_CCASE(kF16, 16, 1, 16, 1) MF_CCASE(kF16, 32, 1, 16, 1) MF_CCASE(kBF16, 4, 1, 16, 1)
+    MF_CCASE(kBF16, 8, 1, 16, 1) MF_CCASE(kBF16, 16, 1, 16, 1) MF_CCASE(kBF16, 32, 1, 16, 1)
+    MF_CCASE(kF32, 32, 1, 4, 0) MF_CCASE(kF32, 32, 4, 4, 0) MF_CCASE(kF32, 32, 16, 4, 0) MF_CCASE(kF32, 32, 32, 4, 0)
+    MF_CCASE(kF16, 32, 1, 4, 0) MF_CCASE(kF16, 32, 4, 4, 0) MF_CCASE(kF16, 32, 16, 4, 0)
+    MF_CCASE(kF16, 32, 1, 2, 0) MF_CCASE(kF16, 32, 4, 2, 0) MF_CCASE(kF16, 32, 16, 2, 0) MF_CCASE(kF16, 32, 32, 2, 0)
+    MF_CCASE(kBF16, 32, 1, 4, 0) MF_CCASE(kBF16, 32, 4, 4, 0) MF_CCASE(kBF16, 32, 16, 4, 0)
+    MF_CCASE(kBF16, 32, 1, 2, 0) MF_CCASE(kBF16, 32, 4, 2, 0) MF_CCASE(kBF16, 32, 16, 2, 0) MF_CCASE(kBF16, 32, 32, 2, 0)
+#undef MF_CCASE
+    return cudaErrorInvalidValue;
+}
+
 ShapeId warp_shape(int k, int storage) {
     if (storage == kF32) {
         if (k == 128) return {storage, 32, 1, 16, 1};
@@ -221,6 +392,18 @@ int mf_ctx::build_wavefront() {
     release_wavefront();
     const int64_t rows = p_rows();
     int s = wave_rows, c = wave_cols;
+    if (wave_cta) {
+        // one CTA worker per SM; c >= 2s column groups, and the largest group must fit in shared
+        // memory (200 KB of the 227 KB per CTA)
+        if (s <= 0) s = (int)std::max<int64_t>(1, std::min<int64_t>(num_sms, rows));
+        if (c <= 0) {
+            const int64_t row_bytes = (int64_t)k * storage_bytes();
+            const int64_t fit = std::max<int64_t>(1, (200 * 1024) / row_bytes);
+            int64_t cc = std::min<int64_t>(2 * (int64_t)s, n);
+            while (cc < n && n - (cc - 1) * (n / cc) > fit) cc++;
+            c = (int)cc;
+        }
+    }
     if (s <= 0) {
         const double by_blocks = std::sqrt((double)N / 200.0);
         s = (int)std::max<double>(1.0, std::min<double>({(double)num_sms * 8, by_blocks, (double)rows}));
@@ -320,13 +503,31 @@ int mf_ctx::run_wavefront(const ShapeId &, const UpdateArgs &ua, int *launches, 
     a.count_updates = count_updates;
     a.eta = ua.eta;
     a.lam = ua.lam;
-    const ShapeId sh = warp_shape(k, storage);
-    const int blocks = (s * 32 + kBlock - 1) / kBlock;
-    CK(dispatch_warp_shape(sh, [&](auto tag) -> cudaError_t {
-        using SH = decltype(tag);
-        k_wavefront<SH, 2><<<blocks, kBlock, 0, st>>>(a);
-        return cudaGetLastError();
-    }));
+    a.grp_w = std::max<int64_t>(1, n / c);
+    a.n_cols = n;
+    if (wave_cta) {
+        const int64_t row_bytes = (int64_t)k * storage_bytes();
+        const int64_t max_rows = std::max<int64_t>(a.grp_w, n - (int64_t)(c - 1) * a.grp_w);
+        const size_t smem = (size_t)(max_rows * row_bytes);
+        if (smem > 227 * 1024) return fail(MF_EINVAL, "wavefront CTA: column group needs %zu B of shared memory", smem);
+        const ShapeId sh = select_shape(k, storage, 0);
+        CK(dispatch_cta_shape(sh, [&](auto tag) -> cudaError_t {
+            using SH = decltype(tag);
+            cudaError_t e = cudaFuncSetAttribute(k_wavefront_cta<SH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 (int)std::max<size_t>(smem, 16));
+            if (e != cudaSuccess) return e;
+            k_wavefront_cta<SH><<<s, kCtaThreads, std::max<size_t>(smem, 16), st>>>(a);
+            return cudaGetLastError();
+        }));
+    } else {
+        const ShapeId sh = warp_shape(k, storage);
+        const int blocks = (s * 32 + kBlock - 1) / kBlock;
+        CK(dispatch_warp_shape(sh, [&](auto tag) -> cudaError_t {
+            using SH = decltype(tag);
+            k_wavefront<SH, 2><<<blocks, kBlock, 0, st>>>(a);
+            return cudaGetLastError();
+        }));
+    }
     *launches = 1;
     *workers_used = s;
     return MF_OK;

@@ -25,6 +25,7 @@ def main():
     ap.add_argument("--batch", default="256")
     ap.add_argument("--k", type=int, default=0)
     ap.add_argument("--sched", default="hogwild")
+    ap.add_argument("--opt", action="append", default=[], help="extra MF option, e.g. wave_cta=1")
     a = ap.parse_args()
     cfg = datagen.CONFIGS[a.cfg]
     if a.k:
@@ -36,7 +37,9 @@ def main():
     for storage in a.storage.split(","):
         b = 4 if storage == "f32" else 2
         B = 12 + 4 * cfg.k * b
-        g = mf.MF(cfg.m, cfg.n, cfg.k, cfg.alpha, cfg.lam, cfg.seed_init, storage=storage, beta=cfg.beta, shuffle=0)
+        extra = {kv.split("=")[0]: float(kv.split("=")[1]) for kv in a.opt}
+        g = mf.MF(cfg.m, cfg.n, cfg.k, cfg.alpha, cfg.lam, cfg.seed_init, storage=storage, beta=cfg.beta, shuffle=0,
+                  **extra)
         g.load(u, v, r)
         for var in [int(x) for x in a.variants.split(",")]:
             for w in [int(x) for x in a.workers.split(",")]:

@@ -113,3 +113,48 @@ def test_wavefront_single_worker_is_serial_block_order(mfmod):
         P, Q = g.factors()
     assert np.linalg.norm(P - ref.P) / np.linalg.norm(ref.P) <= 1e-5
     assert np.linalg.norm(Q - ref.Q) / np.linalg.norm(ref.Q) <= 1e-5
+
+
+# ------------------------------------------------------- CTA workers (smem Q) --
+def test_wavefront_cta_exactly_once_conflict_free_and_rmse(mfmod):
+    """MF_OPT_WAVE_CTA=1: one CTA per SM, the column group's Q rows in shared memory."""
+    cfg = datagen.CONFIGS["C3-1pct"]
+    (u, v, r), test = datagen.make(cfg)
+    E = 10
+    order = oracle.shuffle_perm(cfg.seed_shuffle, len(u))
+    _, trace = oracle.train(cfg.m, cfg.n, cfg.k, oracle.F32, cfg.seed_init, u, v, r, cfg.alpha, cfg.beta,
+                            cfg.lam, E, order=order, test=test)
+    with mfmod.MF(cfg.m, cfg.n, cfg.k, cfg.alpha, cfg.lam, cfg.seed_init, beta=cfg.beta, wave_cta=1, trace=1,
+                  count_updates=1, seed_shuffle=cfg.seed_shuffle) as g:
+        g.load(u, v, r)
+        for _ in range(E):
+            st = g.epoch("wavefront")
+            assert st.updates == len(u)
+        s, c = int(g.get(mfmod.MF_OPT_WAVE_ROWS)), int(g.get(mfmod.MF_OPT_WAVE_COLS))
+        assert s == st.workers and c >= 2 * s
+        assert _audit(mfmod.mf_wavefront_trace(g.h, s * c), s, c) == 0
+        got = g.rmse(*test)
+    assert abs(got - trace[-1]) <= 0.005 * trace[-1], (got, trace[-1])
+
+
+@pytest.mark.parametrize("storage,k", [(0, 7), (0, 128), (0, 256), (1, 7), (1, 256), (2, 7), (2, 256)])
+def test_wavefront_cta_single_block_is_serial(mfmod, storage, k):
+    """s = c = 1, N = 32 (one tile) and a one-group-per-warp shape (L = 32): the tile is handled by one
+    warp in order, so the CTA kernel is exactly serial SGD (checks the shared-memory staging of Q)."""
+    rng = np.random.default_rng(k)
+    m_, n_, N = 9, 7, 32
+    u = rng.integers(0, m_, N).astype(np.int32)
+    v = rng.integers(0, n_, N).astype(np.int32)
+    r = rng.normal(size=N).astype(np.float32)
+    st = {0: oracle.F32, 1: oracle.F16, 2: oracle.BF16}[storage]
+    ref = oracle.Model(m_, n_, k, st, seed=3)
+    ref.epoch(u, v, r, 0.05, 0.01)
+    Pr, Qr = ref.factors_f32()
+    with mfmod.MF(m_, n_, k, 0.05, 0.01, 3, storage=storage, shuffle=0, wave_cta=1, wave_rows=1,
+                  wave_cols=1) as g:
+        g.load(u, v, r)
+        g.epoch("wavefront")
+        P, Q = g.factors()
+    tol = {0: 1e-5, 1: 2e-3, 2: 1.6e-2}[storage]
+    assert np.linalg.norm(P - Pr) / np.linalg.norm(Pr) <= tol
+    assert np.linalg.norm(Q - Qr) / np.linalg.norm(Qr) <= tol
