@@ -193,11 +193,13 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--storage", default="f16", choices=["f16", "f32", "bf16"])
     ap.add_argument("--config", default="C2")
-    ap.add_argument("--schedule", default="hogwild", choices=["hogwild", "wavefront", "deterministic"])
+    ap.add_argument("--schedule", default="hogwild",
+                    choices=["hogwild", "wavefront", "wavefront_cta", "deterministic"])
     ap.add_argument("--workers", type=int, default=0)
     ap.add_argument("--variant", type=int, default=-1)
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-variants", action="store_true", help="skip the other storage / schedule runs")
     ap.add_argument("--ref-sample", type=int, default=1_000_000)
     a = ap.parse_args()
     a.warmup = max(a.warmup, 3)
@@ -221,41 +223,51 @@ def main():
     (u, v, r), (tu, tv, tr) = datagen.make(cfg)
     N = len(u)
     variant = a.variant if a.variant >= 0 else (16 if a.storage != "f32" else 0)
-    g = mf.MF(cfg.m, cfg.n, cfg.k, cfg.alpha, cfg.lam, cfg.seed_init, storage=a.storage, beta=cfg.beta,
-              seed_shuffle=cfg.seed_shuffle, device=local, stream=stream.cuda_stream, variant=variant,
-              workers=a.workers)
     # inputs resident in HBM (torch tensors as device memory), loaded through the C ABI
     du, dv, dr = (torch.from_numpy(x).cuda() for x in (u, v, r))
     dtu, dtv, dtr = (torch.from_numpy(x).cuda() for x in (tu, tv, tr))
-    g.load(du, dv, dr)
-
-    def step():
-        st = g.epoch(a.schedule)
-        rm = g.rmse(dtu, dtv, dtr)
-        return st, rm
-
-    for _ in range(a.warmup):
-        step()
-    torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    kern, launches, rmses, workers = [], 0, [], 0
-    with Clocks(local) as clk:
+
+    def measure(storage, schedule, steps, warmup, clk=None, **opts):
+        """Device-timed steps (epoch + test RMSE) with inputs resident in HBM."""
+        if schedule == "wavefront_cta":
+            schedule, opts = "wavefront", dict(opts, wave_cta=1)
+        var = a.variant if a.variant >= 0 else (16 if storage != "f32" else 0)
+        g = mf.MF(cfg.m, cfg.n, cfg.k, cfg.alpha, cfg.lam, cfg.seed_init, storage=storage, beta=cfg.beta,
+                  seed_shuffle=cfg.seed_shuffle, device=local, stream=stream.cuda_stream, variant=var,
+                  workers=a.workers, **opts)
+        g.load(du, dv, dr)
+        for _ in range(warmup):
+            g.epoch(schedule)
+            g.rmse(dtu, dtv, dtr)
+        kern, launches, rm, workers = [], 0, None, 0
         torch.cuda.synchronize()
+        if clk:
+            clk.__enter__()
         e0.record(stream)
-        for _ in range(a.steps):
-            st, rm = step()
+        for _ in range(steps):
+            st = g.epoch(schedule)
+            rm = g.rmse(dtu, dtv, dtr)
             kern.append(st.kernel_seconds)
             launches += st.launches + 3  # + validate, rmse, final-sum kernels of mf_rmse
-            rmses.append(rm)
             workers = st.workers
         e1.record(stream)
         torch.cuda.synchronize()
-    ms = e0.elapsed_time(e1) / a.steps
-    value = N / (ms * 1e-3)
+        if clk:
+            clk.__exit__(None, None, None)
+        g.close()
+        ms_ = e0.elapsed_time(e1) / steps
+        return {"ms": ms_, "value": N / (ms_ * 1e-3), "kernel_s": statistics.mean(kern), "launches": launches,
+                "rmse": rm, "workers": workers, "epochs_done": warmup + steps}
+
+    clk = Clocks(local)
+    head = measure(a.storage, a.schedule, a.steps, a.warmup, clk=clk)
+    ms, value, launches, workers = head["ms"], head["value"], head["launches"], head["workers"]
+    rmses = [head["rmse"]]
 
     # roofline of the dominant kernel (the update kernel): algorithmic bytes / its event-timed duration
     peak, peak_kind = peaks()
-    k_s = statistics.mean(kern)
+    k_s = head["kernel_s"]
     B = b_alg(cfg.k, a.storage)
     achieved = B * N / k_s / 1e9
     traffic = load_traffic(a.storage, cfg.name)
@@ -265,18 +277,31 @@ def main():
             "bytes_per_update_alg": B, "updates_per_launch": N,
             "note": "frac > 1 is possible: Q (n*k*b = %.1f MB) stays L2-resident, so HBM carries ~12+2kb B/update"
                     % (cfg.n * cfg.k * (4 if a.storage == "f32" else 2) / 1e6)}
-    g.close()
+
+    # the other storage and the wavefront schedule (CTA workers, Q in shared memory), same workload
+    others = {}
+    if not a.no_variants:
+        other_st = "f32" if a.storage != "f32" else "f16"
+        for key, st_, sch, opts in ((f"hogwild/{other_st}", other_st, "hogwild", {}),
+                                    (f"wavefront_cta/{a.storage}", a.storage, "wavefront", {"wave_cta": 1}),
+                                    (f"wavefront_cta/{other_st}", other_st, "wavefront", {"wave_cta": 1})):
+            res = measure(st_, sch, max(3, a.steps // 5), 3, **opts)
+            res["alg_GBps"] = b_alg(cfg.k, st_) * N / res["kernel_s"] / 1e9
+            res["frac_alg"] = res["alg_GBps"] / peak
+            others[key] = {k_: res[k_] for k_ in ("value", "ms", "kernel_s", "rmse", "workers", "alg_GBps",
+                                                  "frac_alg", "epochs_done")}
 
     # end to end through the public API from pinned host buffers
     hu, hv, hr = (torch.from_numpy(x).pin_memory() for x in (u, v, r))
     htu, htv, htr = (torch.from_numpy(x).pin_memory() for x in (tu, tv, tr))
+    sched = "wavefront" if a.schedule == "wavefront_cta" else a.schedule
     ge = mf.MF(cfg.m, cfg.n, cfg.k, cfg.alpha, cfg.lam, cfg.seed_init, storage=a.storage, beta=cfg.beta,
                seed_shuffle=cfg.seed_shuffle, device=local, stream=stream.cuda_stream, variant=variant,
-               workers=a.workers)
+               workers=a.workers, wave_cta=int(a.schedule == "wavefront_cta"))
 
     def e2e_step():
         ge.load(hu, hv, hr)      # H2D + device validation + A-8 shuffle
-        ge.epoch(a.schedule)
+        ge.epoch(sched)
         return ge.rmse(htu, htv, htr)  # H2D of the test set, RMSE kernels, D2H of the result
 
     e2e_step()
@@ -307,6 +332,8 @@ def main():
                 "includes": "H2D of R + test set from pinned host, validation, A-8 shuffle, epoch, RMSE"},
         "gpu_launches": launches,
         "clocks": clk.summary(),
+        "test_rmse_epochs": head["epochs_done"],
+        "other_runs": others,
     }
     print(json.dumps(out), flush=True)
 

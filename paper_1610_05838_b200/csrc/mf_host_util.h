@@ -28,7 +28,20 @@ inline void permutation(std::vector<int32_t> &out, int n, uint64_t key) {
     }
 }
 
-// segment g of [0, extent) split into `parts` near-equal pieces
-inline int64_t seg_begin(int64_t extent, int parts, int g) { return extent * g / parts; }
+#ifdef __CUDACC__
+#define MF_HD __host__ __device__
+#else
+#define MF_HD
+#endif
+
+// segment g of [0, extent) split into `parts` near-equal pieces: [floor(g*extent/parts), ...)
+MF_HD inline int64_t seg_begin(int64_t extent, int parts, int g) { return extent * g / parts; }
+
+// index of the segment holding x (inverse of seg_begin); widths differ by at most one
+MF_HD inline int seg_index(int64_t x, int64_t extent, int parts) {
+    int g = (int)((x * parts) / extent);
+    if (g + 1 <= parts - 1 && ((int64_t)(g + 1) * extent) / parts <= x) g++;
+    return g;
+}
 
 }  // namespace mf

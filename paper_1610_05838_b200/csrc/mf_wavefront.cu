@@ -1,8 +1,9 @@
 // mf_wavefront.cu -- wavefront-update schedule (§3.2.3, Fig. 8).
 //
-// R is bucketed into an s x c grid of blocks: s equal-width row bands (one per
-// worker) and c equal-width column groups, remainder to the last band/group
-// (SPEC.md:319).  The bucketing is a stable radix sort by block id, so each
+// R is bucketed into an s x c grid of blocks: s row bands (one per worker) and
+// c column groups, balanced segments whose widths differ by at most one (SPEC.md:319
+// puts the remainder in the last band; with c not dividing n that band can be many
+// times wider and serialises the schedule, A-9).  The bucketing is a stable radix sort by block id, so each
 // block keeps the shuffled order.  Worker w (one warp) walks
 // its column sequence pi_w[0..c): for wave j it acquires the lock of column
 // pi_w[j] in the 1-D column lock array, processes block
@@ -34,12 +35,11 @@ namespace {
 
 constexpr int kBlock = 256;
 
-__global__ void k_block_keys(const int32_t *u, const int32_t *v, int64_t n, int64_t band_w, int64_t grp_w, int s,
+// row band / column group by balanced segmentation (widths differ by at most one; A-9)
+__global__ void k_block_keys(const int32_t *u, const int32_t *v, int64_t n, int64_t rows, int64_t cols, int s,
                              int c, uint32_t *keys, uint32_t *idx) {
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-        int64_t b = u[i] / band_w, g = v[i] / grp_w;
-        b = b < s - 1 ? b : s - 1;
-        g = g < c - 1 ? g : c - 1;
+        const int64_t b = seg_index(u[i], rows, s), g = seg_index(v[i], cols, c);
         keys[i] = (uint32_t)(b * c + g);
         idx[i] = (uint32_t)i;
     }
@@ -65,8 +65,7 @@ struct WfArgs {
     DevScratch *scratch;
     int s, c, k, latin, count_updates;
     float eta, lam;
-    int64_t grp_w;        // column group width (the last group takes the remainder)
-    int64_t n_cols;
+    int64_t n_cols;       // column groups are balanced segments [floor(g n / c), floor((g+1) n / c))
 };
 
 __device__ __forceinline__ int64_t globaltimer() {
@@ -224,7 +223,7 @@ __device__ __forceinline__ void cta_copy_out(unsigned char *dst, const unsigned 
     }
 }
 
-template <class SH>
+template <class SH, int D>
 __global__ void __launch_bounds__(kCtaThreads, 1) k_wavefront_cta(WfArgs a) {
     extern __shared__ __align__(16) unsigned char qs[];
     __shared__ int s_col, s_next;
@@ -247,8 +246,8 @@ __global__ void __launch_bounds__(kCtaThreads, 1) k_wavefront_cta(WfArgs a) {
         }
         __syncthreads();
         const int col = s_col;
-        const int64_t q0 = (int64_t)col * a.grp_w;
-        const int64_t nrows = col == c - 1 ? a.n_cols - q0 : a.grp_w;
+        const int64_t q0 = seg_begin(a.n_cols, c, col);
+        const int64_t nrows = seg_begin(a.n_cols, c, col + 1) - q0;
         const unsigned char *qg = reinterpret_cast<const unsigned char *>(a.Q) + q0 * row_bytes;
         cta_copy_in(qs, qg, nrows * row_bytes);
         __syncthreads();
@@ -269,36 +268,51 @@ __global__ void __launch_bounds__(kCtaThreads, 1) k_wavefront_cta(WfArgs a) {
             const int cnt = (int)(hi - base < 32 ? hi - base : 32);
             if (lane == 0) done += cnt;
 #pragma unroll 1
-            for (int jj = 0; jj < 32 / G; jj++) {
-                const int s = jj * G + grp;
-                const int32_t su = __shfl_sync(0xffffffffu, tu, s);
-                const int32_t sv = __shfl_sync(0xffffffffu, tv, s);
-                const float sr = __shfl_sync(0xffffffffu, tr, s);
-                const bool val = s < cnt;
-                RowRaw<SH> pr, qr;
-                load_row<SH>(a.P, su, k, sub, val, pr);
-                unsigned char *qrow = qs + (int64_t)sv * row_bytes;
+            for (int j0 = 0; j0 < 32 / G; j0 += D) {  // D ratings of the tile in flight per group
+                int32_t su[D], sv[D];
+                float sr[D], dot[D];
+                bool val[D];
+                RowRaw<SH> pr[D], qr[D];
+                float pf[D][SH::E], qf[D][SH::E];
 #pragma unroll
-                for (int jv = 0; jv < SH::V; jv++) {
-                    const int64_t e = vec_elem<SH>(jv, sub);
-                    if (val && (SH::FULL || e < k)) smem_ld<SH::VB>(qrow + e * SH::BYTES, qr.w[jv]);
-                    else
-#pragma unroll
-                        for (int x = 0; x < SH::NW; x++) qr.w[jv][x] = 0u;
+                for (int d = 0; d < D; d++) {
+                    const int s = (j0 + d) * G + grp;
+                    su[d] = __shfl_sync(0xffffffffu, tu, s);
+                    sv[d] = __shfl_sync(0xffffffffu, tv, s);
+                    sr[d] = __shfl_sync(0xffffffffu, tr, s);
+                    val[d] = s < cnt;
+                    load_row<SH>(a.P, su[d], k, sub, val[d], pr[d]);
                 }
-                float p[SH::E], q[SH::E];
-                widen_row<SH>(pr, p);
-                widen_row<SH>(qr, q);
-                const float err = sr - group_dot<SH>(p, q);
-                if (val && !isfinite(err)) bad = 1;
-                sgd_step<SH>(p, q, err, a.eta, a.lam);
-                narrow_row<SH>(p, pr);
-                narrow_row<SH>(q, qr);
-                store_row<SH>(a.P, su, k, sub, val, pr);
 #pragma unroll
-                for (int jv = 0; jv < SH::V; jv++) {
-                    const int64_t e = vec_elem<SH>(jv, sub);
-                    if (val && (SH::FULL || e < k)) smem_st<SH::VB>(qrow + e * SH::BYTES, qr.w[jv]);
+                for (int d = 0; d < D; d++) {
+                    const unsigned char *qrow = qs + (int64_t)sv[d] * row_bytes;
+#pragma unroll
+                    for (int jv = 0; jv < SH::V; jv++) {
+                        const int64_t e = vec_elem<SH>(jv, sub);
+                        if (val[d] && (SH::FULL || e < k)) smem_ld<SH::VB>(qrow + e * SH::BYTES, qr[d].w[jv]);
+                        else
+#pragma unroll
+                            for (int x = 0; x < SH::NW; x++) qr[d].w[jv][x] = 0u;
+                    }
+                    widen_row<SH>(pr[d], pf[d]);
+                    widen_row<SH>(qr[d], qf[d]);
+                    dot[d] = lane_dot<SH>(pf[d], qf[d]);
+                }
+                group_allreduce<SH, D>(dot);
+#pragma unroll
+                for (int d = 0; d < D; d++) {
+                    const float err = sr[d] - dot[d];
+                    if (val[d] && !isfinite(err)) bad = 1;
+                    sgd_step<SH>(pf[d], qf[d], err, a.eta, a.lam);
+                    narrow_row<SH>(pf[d], pr[d]);
+                    narrow_row<SH>(qf[d], qr[d]);
+                    store_row<SH>(a.P, su[d], k, sub, val[d], pr[d]);
+                    unsigned char *qrow = qs + (int64_t)sv[d] * row_bytes;
+#pragma unroll
+                    for (int jv = 0; jv < SH::V; jv++) {
+                        const int64_t e = vec_elem<SH>(jv, sub);
+                        if (val[d] && (SH::FULL || e < k)) smem_st<SH::VB>(qrow + e * SH::BYTES, qr[d].w[jv]);
+                    }
                 }
             }
         }
@@ -393,14 +407,15 @@ int mf_ctx::build_wavefront() {
     const int64_t rows = p_rows();
     int s = wave_rows, c = wave_cols;
     if (wave_cta) {
-        // one CTA worker per SM; c >= 2s column groups, and the largest group must fit in shared
-        // memory (200 KB of the 227 KB per CTA)
+        // one CTA worker per SM; c = s column groups (the largest blocks: per-block lock, copy-in and
+        // tail cost is amortised best -- Netflix shape, f16: c = s 11.8 G/s, 2s 10.0, 4s 7.7, 8s 6.2),
+        // more if the largest group does not fit in shared memory (200 KB of the 227 KB per CTA)
         if (s <= 0) s = (int)std::max<int64_t>(1, std::min<int64_t>(num_sms, rows));
         if (c <= 0) {
             const int64_t row_bytes = (int64_t)k * storage_bytes();
             const int64_t fit = std::max<int64_t>(1, (200 * 1024) / row_bytes);
-            int64_t cc = std::min<int64_t>(2 * (int64_t)s, n);
-            while (cc < n && n - (cc - 1) * (n / cc) > fit) cc++;
+            int64_t cc = std::min<int64_t>((int64_t)s, n);
+            while (cc < n && (n + cc - 1) / cc > fit) cc++;
             c = (int)cc;
         }
     }
@@ -427,8 +442,7 @@ int mf_ctx::build_wavefront() {
     CK(cudaMallocAsync((void **)&i0, sizeof(uint32_t) * N, st));
     CK(cudaMallocAsync((void **)&i1, sizeof(uint32_t) * N, st));
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((N + 255) / 256, 148 * 16));
-    k_block_keys<<<grid, 256, 0, st>>>(u, v, N, std::max<int64_t>(1, rows / s), std::max<int64_t>(1, n / c), s, c, k0,
-                                       i0);
+    k_block_keys<<<grid, 256, 0, st>>>(u, v, N, rows, n, s, c, k0, i0);
     CK(cudaGetLastError());
     int bits = 1;
     while (bits < 32 && (1ull << bits) < (uint64_t)nb) bits++;
@@ -503,20 +517,20 @@ int mf_ctx::run_wavefront(const ShapeId &, const UpdateArgs &ua, int *launches, 
     a.count_updates = count_updates;
     a.eta = ua.eta;
     a.lam = ua.lam;
-    a.grp_w = std::max<int64_t>(1, n / c);
     a.n_cols = n;
     if (wave_cta) {
         const int64_t row_bytes = (int64_t)k * storage_bytes();
-        const int64_t max_rows = std::max<int64_t>(a.grp_w, n - (int64_t)(c - 1) * a.grp_w);
+        const int64_t max_rows = (n + c - 1) / c;  // balanced column groups
         const size_t smem = (size_t)(max_rows * row_bytes);
         if (smem > 227 * 1024) return fail(MF_EINVAL, "wavefront CTA: column group needs %zu B of shared memory", smem);
         const ShapeId sh = select_shape(k, storage, 0);
         CK(dispatch_cta_shape(sh, [&](auto tag) -> cudaError_t {
             using SH = decltype(tag);
-            cudaError_t e = cudaFuncSetAttribute(k_wavefront_cta<SH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+            constexpr int DD = (SH::FULL && (32 / SH::G) % 2 == 0) ? 2 : 1;  // 2 ratings in flight per group
+            cudaError_t e = cudaFuncSetAttribute(k_wavefront_cta<SH, DD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                  (int)std::max<size_t>(smem, 16));
             if (e != cudaSuccess) return e;
-            k_wavefront_cta<SH><<<s, kCtaThreads, std::max<size_t>(smem, 16), st>>>(a);
+            k_wavefront_cta<SH, DD><<<s, kCtaThreads, std::max<size_t>(smem, 16), st>>>(a);
             return cudaGetLastError();
         }));
     } else {

@@ -53,6 +53,23 @@ def test_c2_hogwild_rmse_trace_vs_oracle_golden(c2, storage):
 
 
 @pytest.mark.parametrize("storage", ["f32", "f16"])
+def test_c2_wavefront_cta_rmse_trace_vs_oracle_golden(c2, storage):
+    """The wavefront schedule with CTA workers (bench.py's throughput configuration) at full size."""
+    path = os.path.join(GOLD, f"C2_{storage}_trace.json")
+    if not os.path.exists(path):
+        pytest.skip(f"{path} not generated yet")
+    gold = json.load(open(path))["rmse"]
+    cfg, ((u, v, r), test) = c2
+    with _ctx(cfg, storage, count_updates=1, wave_cta=1) as g:
+        g.load(u, v, r)
+        for t in range(len(gold)):
+            st = g.epoch("wavefront")
+            assert st.updates == len(u)
+        got = g.rmse(*test)
+    assert abs(got - gold[-1]) <= 0.005 * gold[-1], (got, gold[-1])
+
+
+@pytest.mark.parametrize("storage", ["f32", "f16"])
 def test_c2_deterministic_epoch_sampled_rows(c2, storage):
     path = os.path.join(GOLD, f"C2_{storage}_epoch1_rows.npz")
     if not os.path.exists(path):

@@ -131,16 +131,17 @@ def test_wavefront_cta_exactly_once_conflict_free_and_rmse(mfmod):
             st = g.epoch("wavefront")
             assert st.updates == len(u)
         s, c = int(g.get(mfmod.MF_OPT_WAVE_ROWS)), int(g.get(mfmod.MF_OPT_WAVE_COLS))
-        assert s == st.workers and c >= 2 * s
+        assert s == st.workers and c >= s
         assert _audit(mfmod.mf_wavefront_trace(g.h, s * c), s, c) == 0
         got = g.rmse(*test)
     assert abs(got - trace[-1]) <= 0.005 * trace[-1], (got, trace[-1])
 
 
-@pytest.mark.parametrize("storage,k", [(0, 7), (0, 128), (0, 256), (1, 7), (1, 256), (2, 7), (2, 256)])
+@pytest.mark.parametrize("storage,k", [(0, 7), (0, 33), (0, 100), (1, 7), (1, 100), (2, 7), (2, 66)])
 def test_wavefront_cta_single_block_is_serial(mfmod, storage, k):
-    """s = c = 1, N = 32 (one tile) and a one-group-per-warp shape (L = 32): the tile is handled by one
-    warp in order, so the CTA kernel is exactly serial SGD (checks the shared-memory staging of Q)."""
+    """s = c = 1, N = 32 (one tile) and a masked L = 32 shape (one group per warp, one rating in flight):
+    the tile is handled by one warp in order, so the CTA kernel is exactly serial SGD (checks the
+    shared-memory staging of Q, including rows whose byte size is not a multiple of 16)."""
     rng = np.random.default_rng(k)
     m_, n_, N = 9, 7, 32
     u = rng.integers(0, m_, N).astype(np.int32)
