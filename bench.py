@@ -200,6 +200,8 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-variants", action="store_true", help="skip the other storage / schedule runs")
+    ap.add_argument("--partitioned", action="store_true",
+                    help="run the multi-GPU (NCCL, partitioned) path even at one rank")
     ap.add_argument("--ref-sample", type=int, default=1_000_000)
     a = ap.parse_args()
     a.warmup = max(a.warmup, 3)
@@ -215,7 +217,7 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    if world > 1:
+    if world > 1 or a.partitioned:
         return run_partitioned(a, cfg, rank, world, local)
     torch.cuda.set_device(local)
     stream = torch.cuda.current_stream()
@@ -349,6 +351,11 @@ def run_partitioned(a, cfg, rank, world, local):
     from paper_1610_05838_b200 import mf
 
     torch.cuda.set_device(local)
+    if world == 1:  # --partitioned on one GPU: a 1-rank NCCL job exercising the multi-GPU code path
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29533")
+        os.environ.setdefault("RANK", "0")
+        os.environ.setdefault("WORLD_SIZE", "1")
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     stream = torch.cuda.current_stream()
     G = world

@@ -536,8 +536,15 @@ int mf_ctx::run_wavefront(const ShapeId &, const UpdateArgs &ua, int *launches, 
     } else {
         const ShapeId sh = warp_shape(k, storage);
         const int blocks = (s * 32 + kBlock - 1) / kBlock;
+        const int depth = ((variant >> 4) & 0xF) == 4 ? 4 : 2;  // samples of a block in flight per warp
         CK(dispatch_warp_shape(sh, [&](auto tag) -> cudaError_t {
             using SH = decltype(tag);
+            if constexpr (SH::FULL) {
+                if (depth == 4) {
+                    k_wavefront<SH, 4><<<blocks, kBlock, 0, st>>>(a);
+                    return cudaGetLastError();
+                }
+            }
             k_wavefront<SH, 2><<<blocks, kBlock, 0, st>>>(a);
             return cudaGetLastError();
         }));

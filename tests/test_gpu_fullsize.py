@@ -49,7 +49,8 @@ def test_c2_hogwild_rmse_trace_vs_oracle_golden(c2, storage):
             got.append(g.rmse(*test))
     # north star: every schedule's test RMSE within 0.5% of the oracle's after the same epochs
     assert abs(got[-1] - gold[-1]) <= 0.005 * gold[-1], (got[-1], gold[-1])
-    assert all(b < a for a, b in zip(got, got[1:]))  # decaying schedule: monotone test RMSE here
+    # every epoch of the trace, not only the last, stays within the gate
+    assert all(abs(a - b) <= 0.005 * b for a, b in zip(got, gold)), list(zip(got, gold))
 
 
 @pytest.mark.parametrize("storage", ["f32", "f16"])
