@@ -80,8 +80,9 @@ typedef enum {
     MF_OPT_VARIANT = 14,      /* kernel variant selector for tuning (0 = default) */
     MF_OPT_TRACE = 15,        /* wavefront audit trace: 1 = record (worker, block, t_start, t_end) per block */
     MF_OPT_SUBEPOCHS = 16,    /* partitioned: passes S per epoch, each over 1/S of the shuffled samples with its own Latin square (0 = auto, max(4, G)) */
-    MF_OPT_WAVE_CTA = 17      /* wavefront worker: 0 = one warp, block processed serially; 1 = one CTA per SM with the
+    MF_OPT_WAVE_CTA = 17,     /* wavefront worker: 0 = one warp, block processed serially; 1 = one CTA per SM with the
                                  column group's Q rows staged in shared memory, lock-free inside the block */
+    MF_OPT_STREAM_CHUNK = 18  /* mf_epoch_host: samples per streamed chunk (default 2^23) */
 } mf_option;
 
 typedef struct {
@@ -111,6 +112,17 @@ int mf_load_coo(mf_ctx *ctx, const int32_t *u, const int32_t *v, const float *r,
 /* Run one epoch (N updates) under `schedule` at eta_t, then t += 1.  stats may be NULL.
  * Returns MF_EDIVERGED if any err was non-finite (factors are left as they are). */
 int mf_epoch(mf_ctx *ctx, int schedule, mf_epoch_stats *stats);
+
+/* Streamed epoch: batch-Hogwild! (schedule must be MF_SCHED_HOGWILD) over caller ratings that are NOT
+ * kept resident -- host memory (pinned for full speed) or device memory, processed in the given order
+ * in chunks of MF_OPT_STREAM_CHUNK samples.  The copy of chunk i+1 overlaps the update kernel on chunk i
+ * (three device staging buffers, a copy stream and the context stream; the paper's transfer/compute
+ * overlap, §4.2), so the training set may exceed HBM.  Every chunk is validated on the
+ * device before use: on the first invalid sample the remaining chunks are skipped (earlier chunks stay
+ * applied) and MF_EINVAL is returned.  The caller shuffles; t advances by 1.  Factors
+ * must exist or are created (A-7) on first use; no prior mf_load_coo is needed. */
+int mf_epoch_host(mf_ctx *ctx, int schedule, const int32_t *u, const int32_t *v, const float *r, int64_t nnz,
+                  mf_epoch_stats *stats);
 
 /* Test RMSE sqrt(sum (r - p_u.q_v)^2 / nnz) over the given triples: fp32 dot, fp64 sum,
  * deterministic reduction order.  nnz >= 1.  In the partitioned NCCL mode the call is collective and

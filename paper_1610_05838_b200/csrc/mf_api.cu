@@ -164,6 +164,7 @@ void mf_ctx::release() {
     P = Q = nullptr;
     release_wavefront();
     release_partition();
+    release_stream();
     if (scratch) cudaFree(scratch);
     scratch = nullptr;
     if (h_scratch) cudaFreeHost(h_scratch);
@@ -295,6 +296,10 @@ extern "C" int mf_set_option(mf_ctx *ctx, int key, double value) {
             ctx->wave_cta = (int)iv;
             ctx->wf_valid = false;
             return MF_OK;
+        case MF_OPT_STREAM_CHUNK:
+            if (iv < 32 || iv > (1ll << 34)) return ctx->fail(MF_EINVAL, "stream chunk must be in [32, 2^34]");
+            ctx->stream_chunk = iv;
+            return MF_OK;
         default:
             return ctx->fail(MF_EINVAL, "unknown option %d", key);
     }
@@ -321,6 +326,7 @@ extern "C" int mf_get_option(const mf_ctx *ctx, int key, double *value) {
         case MF_OPT_TRACE: *value = ctx->trace; return MF_OK;
         case MF_OPT_SUBEPOCHS: *value = ctx->subepochs ? ctx->subepochs : ctx->part_S; return MF_OK;
         case MF_OPT_WAVE_CTA: *value = ctx->wave_cta; return MF_OK;
+        case MF_OPT_STREAM_CHUNK: *value = (double)ctx->stream_chunk; return MF_OK;
         default: return MF_EINVAL;
     }
 }

@@ -93,6 +93,16 @@ struct mf_ctx {
     cudaStream_t comm_stream = nullptr;
     void *gather_tmp = nullptr;
 
+    // streamed epochs from caller memory (mf_stream.cu)
+    static constexpr int kStreamBufs = 3;
+    int64_t stream_chunk = 1 << 23;  // samples per chunk (MF_OPT_STREAM_CHUNK)
+    cudaStream_t copy_stream = nullptr;
+    int32_t *sb_u[kStreamBufs] = {}, *sb_v[kStreamBufs] = {};
+    float *sb_r[kStreamBufs] = {};
+    int64_t sb_cap = 0;
+    cudaEvent_t sb_copied[kStreamBufs] = {}, sb_used[kStreamBufs] = {};
+    void release_stream();
+
     // scratch for rmse / factors
     int32_t *tu = nullptr, *tv = nullptr;
     float *tr = nullptr;

@@ -107,6 +107,7 @@ __global__ void __launch_bounds__(kBlock) k_hogwild(UpdateArgs a) {
     // exact worker count: groups beyond a.active_groups idle; a warp with no active group exits
     const int64_t gleft = (int64_t)a.active_groups - warp_id * G;
     if (gleft <= 0) return;  // warp-uniform
+    if (a.abort_if && *a.abort_if) return;  // streamed chunk failed validation
     const int gper = gleft < G ? (int)gleft : G;  // active groups in this warp
     const int ntile = (32 + gper - 1) / gper;     // samples per group per 32-sample tile
     unsigned long long done = 0;

@@ -36,6 +36,7 @@ struct UpdateArgs {
     const int64_t *wave_off;  // deterministic: wave offsets (nwaves + 1)
     int64_t nwaves;
     int64_t active_groups;  // batch-Hogwild!: groups beyond this idle (exact worker count)
+    const unsigned long long *abort_if;  // optional: the kernel does nothing if *abort_if != 0
 };
 
 // Kernel-shape choice for (k, storage); filled by select_shape().

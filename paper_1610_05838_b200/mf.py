@@ -25,7 +25,8 @@ MF_SCHED_HOGWILD, MF_SCHED_WAVEFRONT, MF_SCHED_DETERMINISTIC, MF_SCHED_PARTITION
 SCHEDULES = {"hogwild": 0, "wavefront": 1, "deterministic": 2, "partitioned": 3}
 (MF_OPT_STORAGE, MF_OPT_BETA, MF_OPT_WORKERS, MF_OPT_BATCH_F, MF_OPT_WAVE_ROWS, MF_OPT_WAVE_COLS, MF_OPT_DEVICE,
  MF_OPT_STREAM, MF_OPT_SHUFFLE, MF_OPT_COUNT_UPDATES, MF_OPT_WAVE_PERM, MF_OPT_EPOCH, MF_OPT_PARTITIONS,
- MF_OPT_SEED_SHUFFLE, MF_OPT_VARIANT, MF_OPT_TRACE, MF_OPT_SUBEPOCHS, MF_OPT_WAVE_CTA) = range(18)
+ MF_OPT_SEED_SHUFFLE, MF_OPT_VARIANT, MF_OPT_TRACE, MF_OPT_SUBEPOCHS, MF_OPT_WAVE_CTA,
+ MF_OPT_STREAM_CHUNK) = range(19)
 STORAGE = {"f32": 0, "fp32": 0, "f16": 1, "fp16": 1, "bf16": 2}
 
 
@@ -41,6 +42,7 @@ _sig = {
     "mf_get_option": ([_P, c.c_int, c.POINTER(c.c_double)], c.c_int),
     "mf_load_coo": ([_P, _P, _P, _P, c.c_int64], c.c_int),
     "mf_epoch": ([_P, c.c_int, c.POINTER(mf_epoch_stats)], c.c_int),
+    "mf_epoch_host": ([_P, c.c_int, _P, _P, _P, c.c_int64, c.POINTER(mf_epoch_stats)], c.c_int),
     "mf_rmse": ([_P, _P, _P, _P, c.c_int64, c.POINTER(c.c_double)], c.c_int),
     "mf_get_factors": ([_P, _P, _P], c.c_int),
     "mf_set_factors": ([_P, _P, _P], c.c_int),
@@ -120,6 +122,16 @@ def mf_epoch(ctx, schedule=MF_SCHED_HOGWILD, raise_on_error=True):
     if raise_on_error:
         _check(ctx, rc)
     return st if raise_on_error else (rc, st)
+
+
+def mf_epoch_host(ctx, u, v, r, schedule=MF_SCHED_HOGWILD):
+    pu, au = _ptr(u, np.int32)
+    pv, av = _ptr(v, np.int32)
+    pr, ar = _ptr(r, np.float32)
+    n = len(au) if not hasattr(au, "numel") else au.numel()
+    st = mf_epoch_stats()
+    _check(ctx, _lib.mf_epoch_host(ctx, SCHEDULES.get(schedule, schedule), pu, pv, pr, n, c.byref(st)))
+    return st
 
 
 def mf_rmse(ctx, u, v, r):
@@ -219,6 +231,10 @@ class MF:
 
     def epoch(self, schedule="hogwild"):
         return mf_epoch(self.h, schedule)
+
+    def epoch_host(self, u, v, r):
+        """Streamed batch-Hogwild! epoch over caller ratings (not kept resident)."""
+        return mf_epoch_host(self.h, u, v, r)
 
     def rmse(self, u, v, r):
         return mf_rmse(self.h, u, v, r)

@@ -249,3 +249,44 @@ def test_device_pointers_accepted(mfmod, c1):
             g.epoch("deterministic")
             outs.append(g.factors())
     np.testing.assert_array_equal(outs[0][0], outs[1][0])
+
+
+# ----------------------------------------------------------- streamed epochs --
+def test_streamed_epoch_serial_matches_oracle(mfmod, c1):
+    """mf_epoch_host with one worker and small chunks (many chunk boundaries, ragged tail) is serial SGD
+    in the caller's order: equal to the oracle to fp32 rounding."""
+    cfg, ((u, v, r), test) = c1
+    ref = oracle.Model(cfg.m, cfg.n, cfg.k, oracle.F32, seed=cfg.seed_init)
+    for t in range(2):
+        ref.epoch(u, v, r, oracle.eta(cfg.alpha, cfg.beta, t), cfg.lam)
+    import torch
+    hu, hv, hr = (torch.from_numpy(x).pin_memory() for x in (u, v, r))
+    with mfmod.MF(cfg.m, cfg.n, cfg.k, cfg.alpha, cfg.lam, cfg.seed_init, beta=cfg.beta, workers=1,
+                  stream_chunk=4_000, count_updates=1) as g:
+        for _ in range(2):
+            st = g.epoch_host(hu, hv, hr)
+            assert st.updates == len(u)
+        P, Q = g.factors()
+        assert g.rmse(*test) == pytest.approx(ref.rmse(*test), rel=1e-5)
+    assert frob(P, ref.P) <= 2e-5 and frob(Q, ref.Q) <= 2e-5
+
+
+def test_streamed_epoch_rejects_bad_chunk_and_hogwild_parity(mfmod):
+    cfg = datagen.CONFIGS["C2-1pct"]
+    (u, v, r), test = datagen.make(cfg)
+    order = oracle.shuffle_perm(cfg.seed_shuffle, len(u))
+    us, vs, rs = u[order], v[order], r[order]
+    E = 10
+    _, trace = oracle.train(cfg.m, cfg.n, cfg.k, oracle.F32, cfg.seed_init, us, vs, rs, cfg.alpha, cfg.beta,
+                            cfg.lam, E, test=test)
+    with mfmod.MF(cfg.m, cfg.n, cfg.k, cfg.alpha, cfg.lam, cfg.seed_init, beta=cfg.beta, count_updates=1,
+                  stream_chunk=100_000) as g:
+        for _ in range(E):
+            assert g.epoch_host(us, vs, rs).updates == len(u)
+        got = g.rmse(*test)
+        bad = us.copy()
+        bad[-5] = cfg.m  # out of range, in the last chunk
+        with pytest.raises(mfmod.MFError) as e:
+            g.epoch_host(bad, vs, rs)
+        assert e.value.status == mfmod.MF_EINVAL
+    assert abs(got - trace[-1]) <= 0.005 * trace[-1], (got, trace[-1])
