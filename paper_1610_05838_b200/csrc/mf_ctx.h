@@ -91,6 +91,8 @@ struct mf_ctx {
     mf_nccl *nccl = nullptr;
     int rank = 0, world = 1;
     cudaStream_t comm_stream = nullptr;
+    cudaEvent_t ev_half[2] = {}, ev_recv[2] = {};  // pipelined half-segment exchange
+    bool recv_pending = false;  // q_cur halves are still arriving on comm_stream (wait on ev_recv)
     void *gather_tmp = nullptr;
 
     // streamed epochs from caller memory (mf_stream.cu)
@@ -139,6 +141,7 @@ struct mf_ctx {
     int epoch_partitioned(mf_epoch_stats *stats);
     int build_partition();
     int exchange_segments(const std::vector<int32_t> &want);
+    int exchange_half(const std::vector<int32_t> &want, int h);
     int rmse_partitioned(int64_t nnz, double *out);
     int gather_q();
     void release_partition();

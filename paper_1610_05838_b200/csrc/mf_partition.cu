@@ -47,15 +47,20 @@ __device__ __forceinline__ int seg_of(int64_t x, int64_t extent, int parts) {
     return g;
 }
 
-// block key = ((pass * local + row segment) * G + column segment); the pass of stored sample i is
-// floor(i * S / n), i.e. every epoch is S passes over consecutive slices of the shuffled order
+// block key = (((pass * local + row segment) * G + column segment) * 2 + half); the pass of stored
+// sample i is floor(i * S / n), i.e. every epoch is S passes over consecutive slices of the shuffled
+// order; each block is split into the samples of the lower and upper half of its column segment
 __global__ void k_part_keys(const int32_t *u, const int32_t *v, int64_t n, int64_t m_rows, int64_t n_cols, int G,
                             int rows_split, int S, uint32_t *keys, uint32_t *idx) {
     const int local = rows_split ? G : 1;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
         const int rs = rows_split ? seg_of(u[i], m_rows, G) : 0;
         const int s = (int)((i * S) / n);
-        keys[i] = (uint32_t)(((int64_t)s * local + rs) * G + seg_of(v[i], n_cols, G));
+        const int cs = seg_of(v[i], n_cols, G);
+        // half: the column segment's lower / upper half of rows (pipelined exchange)
+        const int64_t qb = ((int64_t)cs * n_cols) / G, qe = ((int64_t)(cs + 1) * n_cols) / G;
+        const int half = v[i] >= qb + (qe - qb) / 2 ? 1 : 0;
+        keys[i] = (uint32_t)(((((int64_t)s * local + rs) * G + cs) << 1) | half);
         idx[i] = (uint32_t)i;
     }
 }
@@ -66,7 +71,7 @@ __global__ void k_part_gather(const int32_t *u, const int32_t *v, const float *r
                               float *br) {
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
         const uint32_t j = idx[i];
-        const int cs = (int)(keys[i] % (uint32_t)G);
+        const int cs = (int)((keys[i] >> 1) % (uint32_t)G);
         bu[i] = u[j];
         bv[i] = v[j] - (int32_t)(((int64_t)cs * n_cols) / G);
         br[i] = r[j];
@@ -187,6 +192,11 @@ void mf_ctx::release_partition() {
     h_blk_off.clear();
     seg_valid = false;
     part_valid = false;
+    recv_pending = false;
+    for (auto *ev : {&ev_half[0], &ev_half[1], &ev_recv[0], &ev_recv[1]})
+        if (*ev) cudaEventDestroy(*ev), *ev = nullptr;
+    if (comm_stream) cudaStreamDestroy(comm_stream);
+    comm_stream = nullptr;
     if (nccl) {
         if (nccl->comm) ncclCommDestroy(nccl->comm);
         delete nccl;
@@ -200,6 +210,8 @@ int mf_ctx::build_partition() {
     if (G > n || G > p_rows() * (is_distributed() ? world : 1))
         return fail(MF_EINVAL, "partitioned: G = %d exceeds the matrix dimensions", G);
     const int local = is_distributed() ? 1 : G;
+    if (comm_stream) cudaStreamSynchronize(comm_stream);  // no hand-over may still target old buffers
+    recv_pending = false;
     // free a previous layout's buffers (keep the NCCL comm)
     for (void *p : {(void *)bu, (void *)bv, (void *)br})
         if (p) cudaFree(p);
@@ -217,8 +229,8 @@ int mf_ctx::build_partition() {
     // S = 1 costs +10..+20% test RMSE vs the shuffled serial order; S = max(4, G) is within 0.05%)
     const int S_req = subepochs > 0 ? subepochs : std::max(4, G);
     const int S = (int)std::max<int64_t>(1, std::min<int64_t>(S_req, std::max<int64_t>(1, N)));
-    const int64_t nb = (int64_t)S * local * G;
-    if (nb >= (1ll << 31)) return fail(MF_EINVAL, "partitioned: too many blocks (S * G * G)");
+    const int64_t nb = (int64_t)S * local * G * 2;
+    if (nb >= (1ll << 31)) return fail(MF_EINVAL, "partitioned: too many blocks (S * G * G * 2)");
     uint32_t *k0 = nullptr, *k1 = nullptr, *i0 = nullptr, *i1 = nullptr;
     int64_t *doff = nullptr;
     void *tmp = nullptr;
@@ -256,7 +268,9 @@ int mf_ctx::build_partition() {
         CK(cudaMalloc(&q_cur[g], bytes));
         CK(cudaMalloc(&q_next[g], bytes));
     }
-    if (is_distributed() && !comm_stream) CK(cudaStreamCreateWithFlags(&comm_stream, cudaStreamNonBlocking));
+    if (!comm_stream) CK(cudaStreamCreateWithFlags(&comm_stream, cudaStreamNonBlocking));
+    for (auto *ev : {&ev_half[0], &ev_half[1], &ev_recv[0], &ev_recv[1]})
+        if (!*ev) CK(cudaEventCreateWithFlags(ev, cudaEventDisableTiming));
     part_G = G;
     part_local = local;
     part_S = S;
@@ -320,6 +334,11 @@ int mf_ctx::gather_q() {
     const size_t rb = (size_t)k * storage_bytes();
     const size_t bytes = (size_t)seg_rows_max * rb;
     cudaStream_t st = stream();
+    if (recv_pending) {  // the last round's hand-over is still on the comm stream
+        CK(cudaStreamWaitEvent(st, ev_recv[0], 0));
+        CK(cudaStreamWaitEvent(st, ev_recv[1], 0));
+        recv_pending = false;
+    }
     if (is_distributed()) {
         if (!gather_tmp) CK(cudaMalloc(&gather_tmp, bytes * G));
         NK(ncclAllGather(q_cur[0], gather_tmp, bytes, ncclUint8, nccl->comm, st));
@@ -349,46 +368,122 @@ int mf_ctx::epoch_partitioned(mf_epoch_stats *stats) {
     const int S = part_S, L = part_local;
     const float eta = eta_at(epoch);
     const ShapeId sh = select_shape(k, storage, variant & 0xF);
-    auto blk = [&](int s, int li, int c) { return ((size_t)s * L + li) * G + c; };
+    auto blk = [&](int s, int li, int c, int h) { return ((((size_t)s * L + li) * G + c) << 1) | (size_t)h; };
     std::vector<int64_t> n_local(L, 0);  // samples of each hosted partition per epoch (worker clamp, A-10)
     for (int s = 0; s < S; s++)
-        for (int li = 0; li < L; li++) n_local[li] += h_blk_off[blk(s, li, G - 1) + 1] - h_blk_off[blk(s, li, 0)];
+        for (int li = 0; li < L; li++) n_local[li] += h_blk_off[blk(s, li, G - 1, 1) + 1] - h_blk_off[blk(s, li, 0, 0)];
     int launches = 0, used_max = 0;
     CK(cudaEventRecord(events[0], st));
     CK(cudaMemsetAsync(scratch, 0, sizeof(DevScratch), st));
     CK(cudaEventRecord(events[1], st));
-    std::vector<int32_t> pi, want(G);
-    // an epoch is S passes; pass s of epoch e runs the G rounds of Latin square pi_{eS+s}
+    std::vector<int32_t> pi, want(G), next(G);
+    // segments for round 0 of this epoch's first pass (normally already in place: the last round of
+    // the previous epoch handed them over)
+    round_perm(pi, seed_shuffle, epoch * S, G);
+    for (int g = 0; g < G; g++) want[g] = sigma(pi, G, g, 0);
+    if (!seg_valid) {
+        rc = scatter_segments(this, want);
+        recv_pending = false;
+    } else if (held != want) {
+        if (recv_pending) {
+            CK(cudaStreamWaitEvent(st, ev_recv[0], 0));
+            CK(cudaStreamWaitEvent(st, ev_recv[1], 0));
+            recv_pending = false;
+        }
+        rc = exchange_segments(want);
+    }
+    if (rc != MF_OK) return rc;
+    full_valid = false;
+    // An epoch is S passes; pass p = eS + s runs the G rounds of Latin square pi_p.  Each round runs
+    // the lower-half sub-block, then the upper-half sub-block of every hosted block; the lower half of
+    // the Q segment is sent to the next holder (comm stream) while the upper half is still computing,
+    // and the next round starts on its lower half as soon as that half has arrived.
     for (int s = 0; s < S; s++) {
-        const int32_t pass = epoch * S + s;
-        round_perm(pi, seed_shuffle, pass, G);
+        round_perm(pi, seed_shuffle, epoch * S + s, G);
         for (int r = 0; r < G; r++) {
             for (int g = 0; g < G; g++) want[g] = sigma(pi, G, g, r);
-            rc = seg_valid ? exchange_segments(want) : scatter_segments(this, want);
-            if (rc != MF_OK) return rc;
-            full_valid = false;
-            for (int li = 0; li < L; li++) {
-                const int g = is_distributed() ? rank : li;
-                const size_t b = blk(s, li, want[g]);
-                const int64_t lo = h_blk_off[b], hi = h_blk_off[b + 1];
-                if (hi <= lo) continue;
-                UpdateArgs a = update_args(eta);
-                a.u = bu + lo;
-                a.v = bv + lo;
-                a.r = br + lo;
-                a.n = hi - lo;
-                a.Q = q_cur[li];
-                const int w = workers > 0 ? workers
-                                          : (int)std::max<int64_t>(1, std::min<int64_t>(n_local[li] / 10000, 1 << 30));
-                int used = 0;
-                CK(launch_hogwild(sh, a, w, variant, st, &used));
-                used_max = std::max(used_max, used);
-                launches++;
+            if (r + 1 < G) {
+                for (int g = 0; g < G; g++) next[g] = sigma(pi, G, g, r + 1);
+            } else {  // hand over to round 0 of the next pass (of this or the next epoch)
+                std::vector<int32_t> pn;
+                round_perm(pn, seed_shuffle, epoch * S + s + 1, G);
+                for (int g = 0; g < G; g++) next[g] = sigma(pn, G, g, 0);
             }
+            for (int h = 0; h < 2; h++) {
+                if (recv_pending) CK(cudaStreamWaitEvent(st, ev_recv[h], 0));
+                for (int li = 0; li < L; li++) {
+                    const int g = is_distributed() ? rank : li;
+                    const size_t b = blk(s, li, want[g], h);
+                    const int64_t lo = h_blk_off[b], hi = h_blk_off[b + 1];
+                    if (hi <= lo) continue;
+                    UpdateArgs a = update_args(eta);
+                    a.u = bu + lo;
+                    a.v = bv + lo;
+                    a.r = br + lo;
+                    a.n = hi - lo;
+                    a.Q = q_cur[li];
+                    const int w = workers > 0 ? workers
+                                              : (int)std::max<int64_t>(1, std::min<int64_t>(n_local[li] / 10000, 1 << 30));
+                    int used = 0;
+                    CK(launch_hogwild(sh, a, w, variant, st, &used));
+                    used_max = std::max(used_max, used);
+                    launches++;
+                }
+                rc = exchange_half(next, h);
+                if (rc != MF_OK) return rc;
+            }
+            for (int li = 0; li < L; li++) std::swap(q_cur[li], q_next[li]);
+            held = next;
+            recv_pending = true;
         }
     }
     CK(cudaEventRecord(events[2], st));
     return finish_epoch(MF_SCHED_PARTITIONED, eta, launches, used_max, stats);
+}
+
+// Half h (0: rows [0, len/2), 1: rows [len/2, len) of a segment) of every held Q segment moves toward
+// `want` on the comm stream, after the compute stream has finished this round's half-h sub-blocks;
+// the receive lands in q_next.  Staying segments (dst == self) are copied locally so that q_next is
+// complete when the buffers swap.
+int mf_ctx::exchange_half(const std::vector<int32_t> &want, int h) {
+    const int G = part_G;
+    const size_t rb = (size_t)k * storage_bytes();
+    cudaStream_t st = stream(), cs = comm_stream;
+    auto half_rows = [&](int c, int64_t *off, int64_t *rows) {
+        const int64_t len = seg_begin(n, G, c + 1) - seg_begin(n, G, c), hm = len / 2;
+        *off = h ? hm : 0;
+        *rows = h ? len - hm : hm;
+    };
+    CK(cudaEventRecord(ev_half[h], st));
+    CK(cudaStreamWaitEvent(cs, ev_half[h], 0));
+    std::vector<int> dst(G), src(G);
+    for (int g = 0; g < G; g++)
+        for (int x = 0; x < G; x++) {
+            if (want[x] == held[g]) dst[g] = x;
+            if (held[x] == want[g]) src[g] = x;
+        }
+    for (int li = 0; li < part_local; li++) {
+        const int g = is_distributed() ? rank : li;
+        int64_t so, sr, ro, rr;
+        half_rows(held[g], &so, &sr);
+        half_rows(want[g], &ro, &rr);
+        const char *sbuf = (const char *)q_cur[li] + so * rb;
+        if (is_distributed()) {
+            char *rbuf = (char *)q_next[0] + ro * rb;
+            if (dst[g] == g) {
+                if (sr) CK(cudaMemcpyAsync(rbuf, sbuf, sr * rb, cudaMemcpyDeviceToDevice, cs));
+            } else {
+                NK(ncclGroupStart());
+                if (sr) NK(ncclSend(sbuf, sr * rb, ncclUint8, dst[g], nccl->comm, cs));
+                if (rr) NK(ncclRecv(rbuf, rr * rb, ncclUint8, src[g], nccl->comm, cs));
+                NK(ncclGroupEnd());
+            }
+        } else if (sr) {  // loopback: partition g's half lands in the receive buffer of partition dst[g]
+            CK(cudaMemcpyAsync((char *)q_next[dst[g]] + so * rb, sbuf, sr * rb, cudaMemcpyDeviceToDevice, cs));
+        }
+    }
+    CK(cudaEventRecord(ev_recv[h], cs));
+    return MF_OK;
 }
 
 int mf_ctx::rmse_partitioned(int64_t nnz, double *out) {

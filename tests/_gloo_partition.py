@@ -38,22 +38,31 @@ def run(rank, G, port, data, out, epochs, seed):
             c = mf.mf_round_segment(seed, e, G, rnd, rank)
             assert c == held, "holding the wrong Q segment"
             qb, qe = seg[c]
-            sel = mine & (v >= qb) & (v < qe)
-            mdl = oracle.Model(pe - pb, qe - qb, k, oracle.F32, P=P, Q=Q)
-            mdl.epoch(u[sel] - pb, v[sel] - qb, r[sel], eta, lam)
-            P, Q = mdl.P, mdl.Q
             dst, src = mf.mf_round_peers(seed, e, G, rnd, rank)
             nxt_e, nxt_r = (e, rnd + 1) if rnd + 1 < G else (e + 1, 0)
             want = mf.mf_round_segment(seed, nxt_e, G, nxt_r, rank)
             buf = np.empty((seg[want][1] - seg[want][0], k), np.float32)
-            if dst == rank:
-                assert src == rank
-                buf = Q
-            else:
-                reqs = [dist.isend(torch.from_numpy(np.ascontiguousarray(Q)), dst),
-                        dist.irecv(torch.from_numpy(buf), src)]
-                for q in reqs:
-                    q.wait()
+            # libmf's round: the block's lower-half columns, hand over that half of Q, then the upper half
+            for h in (0, 1):
+                mid = (qe - qb) // 2
+                lo, hi = (qb, qb + mid) if h == 0 else (qb + mid, qe)
+                sel = mine & (v >= lo) & (v < hi)
+                mdl = oracle.Model(pe - pb, qe - qb, k, oracle.F32, P=P, Q=Q)
+                mdl.epoch(u[sel] - pb, v[sel] - qb, r[sel], eta, lam)
+                P, Q = mdl.P, mdl.Q
+                wl = len(buf) // 2
+                rows_out = slice(0, mid) if h == 0 else slice(mid, qe - qb)
+                rows_in = slice(0, wl) if h == 0 else slice(wl, len(buf))
+                if dst == rank:
+                    assert src == rank
+                    buf[rows_in] = Q[rows_out]
+                else:
+                    recv = np.empty_like(buf[rows_in])
+                    reqs = [dist.isend(torch.from_numpy(np.ascontiguousarray(Q[rows_out])), dst),
+                            dist.irecv(torch.from_numpy(recv), src)]
+                    for q in reqs:
+                        q.wait()
+                    buf[rows_in] = recv
             Q, held = buf, want
     # gather: P segments and the Q segment each rank holds
     Ps = [torch.zeros((e_ - b_, k)) for b_, e_ in (mf.mf_segment(m, G, g) for g in range(G))]

@@ -32,8 +32,10 @@ def _block_sweep_order(mf, perm, u, v, m, n, G, seed, e, S=4):
         for rnd in range(G):
             for g in range(G):
                 c = mf.mf_round_segment(seed, e * S + s, G, rnd, g)
-                sel = (pas == s) & (us >= rs[g][0]) & (us < rs[g][1]) & (vs >= cs[c][0]) & (vs < cs[c][1])
-                out.append(perm[np.nonzero(sel)[0]])
+                mid = cs[c][0] + (cs[c][1] - cs[c][0]) // 2  # lower half first, then upper half
+                for lo, hi in ((cs[c][0], mid), (mid, cs[c][1])):
+                    sel = (pas == s) & (us >= rs[g][0]) & (us < rs[g][1]) & (vs >= lo) & (vs < hi)
+                    out.append(perm[np.nonzero(sel)[0]])
     return np.concatenate(out)
 
 

@@ -111,8 +111,10 @@ def test_gloo_exchange_equals_serial_block_sweep(tmp_path, G):
         for rnd in range(G):
             for g in range(G):
                 c = mf.mf_round_segment(seed, e, G, rnd, g)
-                sel = (u >= rs[g][0]) & (u < rs[g][1]) & (v >= cs[c][0]) & (v < cs[c][1])
-                order.append(np.nonzero(sel)[0])
+                mid = cs[c][0] + (cs[c][1] - cs[c][0]) // 2  # lower-half columns first, as libmf
+                for lo, hi in ((cs[c][0], mid), (mid, cs[c][1])):
+                    sel = (u >= rs[g][0]) & (u < rs[g][1]) & (v >= lo) & (v < hi)
+                    order.append(np.nonzero(sel)[0])
         ref.epoch(u, v, r, oracle.eta(0.05, 0.0, e), 0.02, np.concatenate(order))
     np.testing.assert_array_equal(got["P"], ref.P)
     np.testing.assert_array_equal(got["Q"], ref.Q)
