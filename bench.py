@@ -279,6 +279,13 @@ def main():
             "bytes_per_update_alg": B, "updates_per_launch": N,
             "note": "frac > 1 is possible: Q (n*k*b = %.1f MB) stays L2-resident, so HBM carries ~12+2kb B/update"
                     % (cfg.n * cfg.k * (4 if a.storage == "f32" else 2) / 1e6)}
+    # the same kernel against the bytes DRAM must move when Q is L2-resident (R + P read + P write), and
+    # against the DRAM bytes ncu measured for one launch (profiles/ncu_summary.json)
+    b_hbm = 12 + 2 * cfg.k * (4 if a.storage == "f32" else 2)
+    roof["frac_hbm_compulsory"] = b_hbm * N / k_s / 1e9 / peak
+    if traffic:
+        roof["frac_dram_measured_bytes"] = traffic / k_s / 1e9 / peak
+        roof["dram_bytes_per_update_measured"] = traffic / N
 
     # the other storage and the wavefront schedule (CTA workers, Q in shared memory), same workload
     others = {}
