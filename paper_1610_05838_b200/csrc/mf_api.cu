@@ -292,7 +292,7 @@ extern "C" int mf_set_option(mf_ctx *ctx, int key, double value) {
             ctx->part_valid = false;
             return MF_OK;
         case MF_OPT_WAVE_CTA:
-            if (iv < 0 || iv > 1) return ctx->fail(MF_EINVAL, "wave cta must be 0 or 1");
+            if (iv < 0 || iv > 2) return ctx->fail(MF_EINVAL, "wave cta must be 0, 1 or 2");
             ctx->wave_cta = (int)iv;
             ctx->wf_valid = false;
             return MF_OK;

@@ -223,8 +223,8 @@ __device__ __forceinline__ void cta_copy_out(unsigned char *dst, const unsigned 
     }
 }
 
-template <class SH, int D>
-__global__ void __launch_bounds__(kCtaThreads, 1) k_wavefront_cta(WfArgs a) {
+template <class SH, int D, int THREADS>
+__global__ void __launch_bounds__(THREADS, kCtaThreads / THREADS) k_wavefront_cta(WfArgs a) {
     extern __shared__ __align__(16) unsigned char qs[];
     __shared__ int s_col, s_next;
     constexpr int L = SH::L, G = SH::G;
@@ -254,21 +254,30 @@ __global__ void __launch_bounds__(kCtaThreads, 1) k_wavefront_cta(WfArgs a) {
         const int64_t t0 = a.trace ? globaltimer() : 0;
         const int64_t blk = (int64_t)w * c + col;
         const int64_t lo = a.off[blk], hi = a.off[blk + 1];
+        const int64_t blk_n = hi - lo;
         for (;;) {
-            int t = 0;
-            if (lane == 0) t = atomicAdd(&s_next, 32);
+            // 32-sample tiles while plenty remain; near the end of the block claim G*D samples at a
+            // time so the warps finish together (the block ends at a CTA barrier)
+            int t = 0, want = 32;
+            if (lane == 0) {
+                const int64_t rem = blk_n - *(volatile int *)&s_next;
+                want = rem > 2 * 32 * (THREADS / 32) ? 32 : G * D;
+                t = atomicAdd(&s_next, want);
+            }
             t = __shfl_sync(0xffffffffu, t, 0);
+            want = __shfl_sync(0xffffffffu, want, 0);
             const int64_t base = lo + t;
             if (base >= hi) break;  // warp-uniform
             const int64_t i = base + lane;
-            const bool ok = i < hi;
+            const bool ok = lane < want && i < hi;
             const int32_t tu = ok ? __ldg(a.u + i) : 0;
             const int32_t tv = ok ? (int32_t)(__ldg(a.v + i) - q0) : 0;
             const float tr = ok ? __ldg(a.r + i) : 0.f;
-            const int cnt = (int)(hi - base < 32 ? hi - base : 32);
+            const int cnt = (int)(hi - base < want ? hi - base : want);
             if (lane == 0) done += cnt;
+            const int per_group = (cnt + G - 1) / G;
 #pragma unroll 1
-            for (int j0 = 0; j0 < 32 / G; j0 += D) {  // D ratings of the tile in flight per group
+            for (int j0 = 0; j0 < per_group; j0 += D) {  // D ratings of the tile in flight per group
                 int32_t su[D], sv[D];
                 float sr[D], dot[D];
                 bool val[D];
@@ -410,7 +419,7 @@ int mf_ctx::build_wavefront() {
         // one CTA worker per SM; c = s column groups (the largest blocks: per-block lock, copy-in and
         // tail cost is amortised best -- Netflix shape, f16: c = s 11.8 G/s, 2s 10.0, 4s 7.7, 8s 6.2),
         // more if the largest group does not fit in shared memory (200 KB of the 227 KB per CTA)
-        if (s <= 0) s = (int)std::max<int64_t>(1, std::min<int64_t>(num_sms, rows));
+        if (s <= 0) s = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)num_sms * wave_cta, rows));
         if (c <= 0) {
             const int64_t row_bytes = (int64_t)k * storage_bytes();
             const int64_t fit = std::max<int64_t>(1, (200 * 1024) / row_bytes);
@@ -527,11 +536,17 @@ int mf_ctx::run_wavefront(const ShapeId &, const UpdateArgs &ua, int *launches, 
         CK(dispatch_cta_shape(sh, [&](auto tag) -> cudaError_t {
             using SH = decltype(tag);
             constexpr int DD = (SH::FULL && (32 / SH::G) % 2 == 0) ? 2 : 1;  // 2 ratings in flight per group
-            cudaError_t e = cudaFuncSetAttribute(k_wavefront_cta<SH, DD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                 (int)std::max<size_t>(smem, 16));
-            if (e != cudaSuccess) return e;
-            k_wavefront_cta<SH, DD><<<s, kCtaThreads, std::max<size_t>(smem, 16), st>>>(a);
-            return cudaGetLastError();
+            auto launch = [&](auto kern, int threads) -> cudaError_t {
+                cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                     (int)std::max<size_t>(smem, 16));
+                if (e != cudaSuccess) return e;
+                kern<<<s, threads, std::max<size_t>(smem, 16), st>>>(a);
+                return cudaGetLastError();
+            };
+            // MF_OPT_WAVE_CTA = 2: two 512-thread workers per SM, so one's block boundary (write-back,
+            // lock hand-over, staging) overlaps the other's updates
+            if (wave_cta == 2) return launch(k_wavefront_cta<SH, DD, 512>, 512);
+            return launch(k_wavefront_cta<SH, DD, 1024>, 1024);
         }));
     } else {
         const ShapeId sh = warp_shape(k, storage);
