@@ -256,16 +256,13 @@ __global__ void __launch_bounds__(THREADS, kCtaThreads / THREADS) k_wavefront_ct
         const int64_t lo = a.off[blk], hi = a.off[blk + 1];
         const int64_t blk_n = hi - lo;
         for (;;) {
-            // 32-sample tiles while plenty remain; near the end of the block claim G*D samples at a
-            // time so the warps finish together (the block ends at a CTA barrier)
+            // 32-sample tiles.  (Claiming smaller tiles near the end of a block balances the warps but
+            // raises the number of a small block's samples in flight at once -- more write conflicts
+            // on the group's Q rows: C3-1pct test RMSE +2.0% vs +0.3%, and 4-7% slower on C2.)
             int t = 0, want = 32;
-            if (lane == 0) {
-                const int64_t rem = blk_n - *(volatile int *)&s_next;
-                want = rem > 2 * 32 * (THREADS / 32) ? 32 : G * D;
-                t = atomicAdd(&s_next, want);
-            }
+            if (lane == 0) t = atomicAdd(&s_next, want);
             t = __shfl_sync(0xffffffffu, t, 0);
-            want = __shfl_sync(0xffffffffu, want, 0);
+            (void)blk_n;
             const int64_t base = lo + t;
             if (base >= hi) break;  // warp-uniform
             const int64_t i = base + lane;

@@ -1,0 +1,41 @@
+"""One small run of every kernel family, for `compute-sanitizer --tool memcheck`.
+
+    compute-sanitizer --tool memcheck --error-exitcode 1 python scripts/sanitize_run.py
+"""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import numpy as np  # noqa: E402
+
+import datagen  # noqa: E402
+from paper_1610_05838_b200 import mf  # noqa: E402
+
+
+def main():
+    cfg = datagen.CONFIGS["C1"]
+    (u, v, r), test = datagen.make(cfg)
+    for storage in ("f32", "f16", "bf16"):
+        for k in (cfg.k, 7, 128):
+            for sched, opts in (("hogwild", {}), ("deterministic", {}), ("wavefront", {}),
+                                ("wavefront", {"wave_cta": 1}), ("wavefront", {"wave_cta": 2}),
+                                ("partitioned", {"partitions": 3})):
+                g = mf.MF(cfg.m, cfg.n, k, cfg.alpha, cfg.lam, cfg.seed_init, storage=storage, beta=cfg.beta,
+                          count_updates=1, trace=1, **opts)
+                g.load(u, v, r)
+                for _ in range(2):
+                    st = g.epoch(sched)
+                    assert st.updates == len(u), (storage, k, sched, opts, st.updates)
+                g.rmse(*test)
+                P, Q = g.factors()
+                assert np.isfinite(P).all() and np.isfinite(Q).all()
+                g.close()
+            g = mf.MF(cfg.m, cfg.n, k, cfg.alpha, cfg.lam, cfg.seed_init, storage=storage, stream_chunk=7000)
+            g.epoch_host(u, v, r)
+            g.close()
+    print("sanitize run ok")
+
+
+if __name__ == "__main__":
+    main()
