@@ -72,8 +72,8 @@ int main() {
     for (int64_t sz : sizes) {
         for (int bps : {4, 6, 8}) {
             const int blocks = sms * bps;
-            const double g16 = run<16, 2>(sz, blocks, threads, 4000);  // 256-byte rows (k=128 fp16)
-            const double g32 = run<32, 2>(sz, blocks, threads, 2000);  // 512-byte rows (k=128 fp32)
+            const double g16 = run<16, 8>(sz, blocks, threads, 1000);  // 256-byte rows (k=128 fp16), 8 in flight
+            const double g32 = run<32, 8>(sz, blocks, threads, 500);   // 512-byte rows (k=128 fp32)
             printf("%s {\"table_MB\": %lld, \"warps_per_sm\": %d, \"rmw_GBps_256B_rows\": %.1f, "
                    "\"rmw_GBps_512B_rows\": %.1f}",
                    first ? "" : ",\n", (long long)(sz >> 20), bps * threads / 32, g16, g32);
