@@ -38,6 +38,10 @@ def _load():
         lib.mfgen_planted_factors.argtypes = [ctypes.c_uint64, ctypes.c_int64, ctypes.c_int64, ctypes.c_int,
                                               ctypes.c_void_p, ctypes.c_void_p]
         lib.mfgen_planted_factors.restype = ctypes.c_int
+        lib.mfgen_zipf_coo.argtypes = [ctypes.c_uint64, ctypes.c_int64, ctypes.c_int64, ctypes.c_int, ctypes.c_double,
+                                       ctypes.c_int64, ctypes.c_double, ctypes.c_double,
+                                       ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
+        lib.mfgen_zipf_coo.restype = ctypes.c_int
         _lib = lib
     return _lib
 
@@ -59,6 +63,17 @@ def planted_coo(seed, m, n, rank, sigma, total, with_replacement=True):
     return u, v, r
 
 
+def zipf_coo(seed, m, n, rank, sigma, total, s_u, s_v):
+    """Skewed degrees (NEXT-4): u ~ Zipf(s_u), v ~ Zipf(s_v) over scrambled ids, same planted ratings."""
+    u = np.empty(total, np.int32)
+    v = np.empty(total, np.int32)
+    r = np.empty(total, np.float32)
+    if _load().mfgen_zipf_coo(seed, m, n, rank, sigma, total, s_u, s_v, u.ctypes.data, v.ctypes.data,
+                              r.ctypes.data) != 0:
+        raise ValueError("mfgen_zipf_coo rejected its arguments")
+    return u, v, r
+
+
 def planted_factors(seed, m, n, rank):
     P = np.empty((m, rank), np.float64)
     Q = np.empty((n, rank), np.float64)
@@ -75,6 +90,9 @@ def split(cfg: "Config", u, v, r):
 
 def make(cfg: "Config"):
     """Generate the config's full train+test COO; returns ((u,v,r) train, (u,v,r) test)."""
-    u, v, r = planted_coo(cfg.seed_data, cfg.m, cfg.n, cfg.rank, cfg.sigma,
-                          cfg.n_train + cfg.n_test, cfg.with_replacement)
+    if cfg.zipf is not None:
+        u, v, r = zipf_coo(cfg.seed_data, cfg.m, cfg.n, cfg.rank, cfg.sigma, cfg.n_train + cfg.n_test, *cfg.zipf)
+    else:
+        u, v, r = planted_coo(cfg.seed_data, cfg.m, cfg.n, cfg.rank, cfg.sigma,
+                              cfg.n_train + cfg.n_test, cfg.with_replacement)
     return split(cfg, u, v, r)

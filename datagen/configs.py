@@ -27,6 +27,7 @@ class Config:
     seed_init: int = 7
     with_replacement: bool = True
     epochs: int = 20
+    zipf: tuple | None = None  # (s_u, s_v): Zipf-skewed row / column popularity (NEXT-4)
 
     def scaled(self, **kw) -> "Config":
         return replace(self, **kw)
@@ -50,6 +51,12 @@ CONFIGS = {
     # Netflix-scaled 10% (SURVEY §8(c) [SIM] instance): same degrees as C2
     "C2-10pct": Config("C2-10pct", 48_019, 1_777, 9_907_211, 140_840, 128, 0.08, 0.3, 0.05, 0.1,
                        seed_data=2, epochs=20),
+    # NEXT-4: Netflix shape with power-law degrees (top item ~0.4% of the ratings, as real data is
+    # heavy-tailed) and its 1% slice for oracle-sized parity
+    "C2-zipf": Config("C2-zipf", 480_190, 17_771, 99_072_112, 1_408_395, 128, 0.08, 0.3, 0.05, 0.1,
+                      seed_data=5, epochs=20, zipf=(0.3, 0.5)),
+    "C2-zipf-1pct": Config("C2-zipf-1pct", 4_802, 178, 990_721, 14_084, 128, 0.08, 0.3, 0.05, 0.1,
+                           seed_data=5, epochs=20, zipf=(0.3, 0.5)),
     # configs[2]: Yahoo!Music-shaped, lambda per reading A-18
     "C3": Config("C3", 1_000_990, 624_961, 252_800_275, 4_003_960, 128, 0.08, 0.2, 0.05, 0.1,
                  seed_data=3, epochs=10),

@@ -105,3 +105,63 @@ int mfgen_planted_coo(uint64_t seed, int64_t m, int64_t n, int rank, double sigm
     free(Qs);
     return 0;
 }
+
+/* Zipf(s) popularity over `count` ids: cdf[i] = sum_{j<=i} (j+1)^-s / total; the id order is then
+ * scrambled by a seeded Fisher-Yates permutation (hot ids are not clustered at low indices). */
+static int zipf_table(uint64_t seed, uint64_t tag, int64_t count, double s, double **cdf_out, int32_t **perm_out) {
+    double *cdf = (double *)malloc(sizeof(double) * (size_t)count);
+    int32_t *perm = (int32_t *)malloc(sizeof(int32_t) * (size_t)count);
+    if (!cdf || !perm) { free(cdf); free(perm); return -1; }
+    double acc = 0.0;
+    for (int64_t i = 0; i < count; i++) { acc += pow((double)(i + 1), -s); cdf[i] = acc; }
+    for (int64_t i = 0; i < count; i++) { cdf[i] /= acc; perm[i] = (int32_t)i; }
+    cdf[count - 1] = 1.0;
+    for (int64_t i = count - 1; i > 0; i--) {
+        const int64_t j = (int64_t)(gen_H(seed, tag, (uint64_t)i) % (uint64_t)(i + 1));
+        const int32_t t = perm[i]; perm[i] = perm[j]; perm[j] = t;
+    }
+    *cdf_out = cdf;
+    *perm_out = perm;
+    return 0;
+}
+
+static inline int32_t zipf_draw(const double *cdf, const int32_t *perm, int64_t count, uint64_t h) {
+    const double x = (double)(h >> 11) * 0x1.0p-53;
+    int64_t lo = 0, hi = count - 1;
+    while (lo < hi) {  /* first index with cdf >= x */
+        const int64_t mid = (lo + hi) / 2;
+        if (cdf[mid] < x) lo = mid + 1; else hi = mid;
+    }
+    return perm[lo];
+}
+
+/*
+ * Skewed workload: row ids ~ Zipf(s_u), column ids ~ Zipf(s_v) (with
+ * replacement, ids scrambled), ratings from the same planted rank-`rank` model as mfgen_planted_coo.
+ */
+int mfgen_zipf_coo(uint64_t seed, int64_t m, int64_t n, int rank, double sigma, int64_t total, double s_u,
+                   double s_v, int32_t *u, int32_t *v, float *r) {
+    if (m <= 0 || n <= 0 || rank <= 0 || total < 0 || !u || !v || !r || s_u < 0 || s_v < 0) return -1;
+    if (m > 2147483647ll || n > 2147483647ll) return -1;
+    double *cu = NULL, *cv = NULL;
+    int32_t *pu = NULL, *pv = NULL;
+    double *Ps = (double *)malloc(sizeof(double) * (size_t)m * rank);
+    double *Qs = (double *)malloc(sizeof(double) * (size_t)n * rank);
+    if (!Ps || !Qs || zipf_table(seed, 6, m, s_u, &cu, &pu) || zipf_table(seed, 7, n, s_v, &cv, &pv)) {
+        free(Ps); free(Qs); free(cu); free(cv); free(pu); free(pv);
+        return -1;
+    }
+    planted(seed, 0, m, rank, Ps);
+    planted(seed, 1, n, rank, Qs);
+#pragma omp parallel for schedule(static)
+    for (int64_t i = 0; i < total; i++) {
+        u[i] = zipf_draw(cu, pu, m, gen_H(seed, 2, (uint64_t)i));
+        v[i] = zipf_draw(cv, pv, n, gen_H(seed, 3, (uint64_t)i));
+        const double *p = Ps + (int64_t)u[i] * rank, *q = Qs + (int64_t)v[i] * rank;
+        double s = 0.0;
+        for (int j = 0; j < rank; j++) s += p[j] * q[j];
+        r[i] = (float)(s + sigma * gen_gauss(seed, 4, (uint64_t)i));
+    }
+    free(Ps); free(Qs); free(cu); free(cv); free(pu); free(pv);
+    return 0;
+}

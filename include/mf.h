@@ -71,7 +71,9 @@ typedef enum {
     MF_OPT_WAVE_COLS = 5,     /* wavefront column blocks c >= s (0 = auto) */
     MF_OPT_DEVICE = 6,        /* CUDA device ordinal (before the first load) */
     MF_OPT_STREAM = 7,        /* cudaStream_t as an integer; 0 = the context's own stream */
-    MF_OPT_SHUFFLE = 8,       /* 1 = permute samples once at load by the A-8 hash sort (default); 0 = keep the given order */
+    MF_OPT_SHUFFLE = 8,       /* 1 = permute samples once at load by the A-8 hash sort (default); 0 = keep the given order;
+                                 2 = also re-permute before every later epoch t: order_t = order_{t-1}[pi_t], pi_t the
+                                 A-8 permutation under seed_shuffle ^ (t << 48) (mf_get_order follows) */
     MF_OPT_COUNT_UPDATES = 9, /* 1 = count updates per epoch on the device (exactly-once check) */
     MF_OPT_WAVE_PERM = 10,    /* wavefront column sequences: 0 randomized Latin rectangle (default), 1 independent random permutations */
     MF_OPT_EPOCH = 11,        /* set the epoch index t used by the LR schedule */

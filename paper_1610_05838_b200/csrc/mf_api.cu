@@ -258,7 +258,7 @@ extern "C" int mf_set_option(mf_ctx *ctx, int key, double value) {
             ctx->user_stream = (cudaStream_t)(uintptr_t)iv;
             return MF_OK;
         case MF_OPT_SHUFFLE:
-            if (iv < 0 || iv > 1) return ctx->fail(MF_EINVAL, "shuffle must be 0 or 1");
+            if (iv < 0 || iv > 2) return ctx->fail(MF_EINVAL, "shuffle must be 0, 1 or 2");
             ctx->shuffle = (int)iv;
             return MF_OK;
         case MF_OPT_COUNT_UPDATES:
@@ -388,8 +388,36 @@ extern "C" int mf_load_coo(mf_ctx *ctx, const int32_t *u, const int32_t *v, cons
                          (unsigned long long)ctx->h_scratch->bad, (long long)ctx->p_begin, (long long)ctx->p_end,
                          (long long)ctx->n);
     ctx->N = nnz;
+    ctx->reshuffle_due = false;  // the first epoch after a load uses the load's order
     ctx->shuffled = ctx->shuffle;
     RC(ctx->ensure_factors());
+    return MF_OK;
+}
+
+// Per-epoch reshuffle (MF_OPT_SHUFFLE = 2): before epoch t (t >= 1 after a load) the stored order is
+// permuted again by the A-8 hash sort keyed with seed_shuffle ^ (t << 48):
+//     order_t = order_{t-1}[pi_t],  pi_t = A-8 permutation of N under that seed,
+// so the caller-index map stays available through mf_get_order.  Schedule layouts are rebuilt.
+int mf_ctx::reshuffle() {
+    mf_ctx *ctx = this;
+    cudaStream_t st = stream();
+    uint32_t *p2 = nullptr, *p3 = nullptr;
+    CK(cudaMallocAsync((void **)&p2, sizeof(uint32_t) * N, st));
+    CK(cudaMallocAsync((void **)&p3, sizeof(uint32_t) * N, st));
+    CK(launch_shuffle_perm(N, seed_shuffle ^ ((uint64_t)(uint32_t)epoch << 48), p2, st));
+    CK(launch_gather(u, v, r, p2, N, stg_u, stg_v, stg_r, st));
+    CK(launch_compose(perm, p2, p3, N, st));
+    CK(cudaMemcpyAsync(perm, p3, sizeof(uint32_t) * N, cudaMemcpyDeviceToDevice, st));
+    CK(cudaFreeAsync(p2, st));
+    CK(cudaFreeAsync(p3, st));
+    std::swap(u, stg_u);
+    std::swap(v, stg_v);
+    std::swap(r, stg_r);
+    perm_n = -1;  // perm no longer equals the load-time permutation
+    RC(gather_q());
+    drop_layouts();
+    seg_valid = false;
+    CK(cudaStreamSynchronize(st));
     return MF_OK;
 }
 
@@ -508,6 +536,10 @@ extern "C" int mf_epoch(mf_ctx *ctx, int schedule, mf_epoch_stats *stats) {
         return ctx->fail(MF_EINVAL, "unknown schedule %d", schedule);
     if (ctx->N <= 0 || !ctx->P) return ctx->fail(MF_ESTATE, "mf_epoch before mf_load_coo");
     CK(cudaSetDevice(ctx->device));
+    if (ctx->shuffle == 2 && ctx->shuffled) {  // per-epoch reshuffle (SPEC.md:264 reading; NEXT-4)
+        if (ctx->reshuffle_due) RC(ctx->reshuffle());
+        ctx->reshuffle_due = true;
+    }
     if (schedule == MF_SCHED_DETERMINISTIC) RC(ctx->build_waves());
     if (schedule == MF_SCHED_WAVEFRONT) RC(ctx->build_wavefront());
     if (schedule == MF_SCHED_PARTITIONED) return ctx->epoch_partitioned(stats);

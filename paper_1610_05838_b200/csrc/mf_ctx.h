@@ -52,6 +52,7 @@ struct mf_ctx {
     float *r = nullptr;
     uint32_t *perm = nullptr;  // perm[i] = caller index of stored sample i
     int64_t perm_n = -1;       // perm is the A-8 permutation of perm_n samples under perm_seed (cached)
+    bool reshuffle_due = false;  // MF_OPT_SHUFFLE = 2: permute again before the next epoch
     uint64_t perm_seed = 0;
     int32_t *stg_u = nullptr, *stg_v = nullptr;  // staging copy of the caller's order (shuffle on)
     float *stg_r = nullptr;
@@ -127,6 +128,7 @@ struct mf_ctx {
     mf::UpdateArgs update_args(float eta) const;
     int finish_epoch(int schedule, float eta, int launches, int workers_used, mf_epoch_stats *stats);
     int build_waves();
+    int reshuffle();
     int copy_out(const void *X, int64_t count, float *dst);
     int copy_in(void *X, int64_t count, const float *src);
     void drop_layouts();

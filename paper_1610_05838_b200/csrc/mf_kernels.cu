@@ -502,6 +502,17 @@ cudaError_t launch_gather(const int32_t *u_in, const int32_t *v_in, const float 
     return cudaGetLastError();
 }
 
+// out[i] = a[b[i]]: composition of two permutations (per-epoch reshuffle keeps the caller order map)
+__global__ void k_compose(const uint32_t *a, const uint32_t *b, uint32_t *out, int64_t n) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        out[i] = a[b[i]];
+}
+cudaError_t launch_compose(const uint32_t *a, const uint32_t *b, uint32_t *out, int64_t n, cudaStream_t st) {
+    const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 148 * 16));
+    k_compose<<<blocks, 256, 0, st>>>(a, b, out, n);
+    return cudaGetLastError();
+}
+
 // A-8 permutation only (data independent): keys, radix sort, perm_out[j] = original index
 cudaError_t launch_shuffle_perm(int64_t n, uint64_t seed, uint32_t *perm_out, cudaStream_t st) {
     if (n > (int64_t)0xFFFFFFFFll) return cudaErrorInvalidValue;

@@ -64,6 +64,7 @@ cudaError_t launch_shuffle_perm(int64_t n, uint64_t seed, uint32_t *perm_out, cu
 cudaError_t launch_gather_validate(const int32_t *u_in, const int32_t *v_in, const float *r_in, const uint32_t *idx,
                                    int64_t n, int64_t row_lo, int64_t row_hi, int64_t n_cols, int32_t *u_out,
                                    int32_t *v_out, float *r_out, DevScratch *scratch, cudaStream_t st);
+cudaError_t launch_compose(const uint32_t *a, const uint32_t *b, uint32_t *out, int64_t n, cudaStream_t st);
 cudaError_t launch_gather(const int32_t *u_in, const int32_t *v_in, const float *r_in, const uint32_t *idx, int64_t n,
                           int32_t *u_out, int32_t *v_out, float *r_out, cudaStream_t st);
 

@@ -34,6 +34,23 @@ def test_planted_statistics():
     assert abs(deg.mean() - 100) < 1e-9 and deg.std() < 15
 
 
+def test_zipf_degrees_follow_the_power_law():
+    """NEXT-4 generator: column ids ~ Zipf(s) (scrambled): the k-th most frequent id has frequency
+    ~ k^-s / H_n(s); ratings keep the planted model."""
+    n, s, N = 2000, 0.8, 400_000
+    u, v, r = datagen.zipf_coo(9, 5000, n, 8, 0.1, N, 0.0, s)
+    freq = np.sort(np.bincount(v, minlength=n))[::-1] / N
+    H = np.sum(np.arange(1, n + 1) ** -s)
+    for kk in (1, 10, 100):
+        assert abs(freq[kk - 1] - kk ** -s / H) < 0.1 * kk ** -s / H + 3e-4
+    assert np.argmax(np.bincount(v)) != 0  # hot ids are scrambled, not clustered at 0
+    du = np.bincount(u, minlength=5000) / N  # s_u = 0: uniform rows
+    assert du.max() < 3 / 5000
+    P, Q = datagen.planted_factors(9, 5000, n, 8)
+    resid = r.astype(np.float64) - np.einsum("ij,ij->i", P[u], Q[v])
+    assert abs(resid.std() - 0.1) < 0.005
+
+
 def test_configs_table2_shapes():
     """PAPER.md:373-377 Table 2."""
     c = datagen.CONFIGS

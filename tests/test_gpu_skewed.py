@@ -1,0 +1,81 @@
+"""NEXT-4: power-law degrees and per-epoch reshuffle.  -m gpu.
+
+C2-zipf-1pct has the Netflix 1% slice's size with Zipf(0.3) rows and Zipf(0.5) columns: the hottest
+column holds ~4% of the ratings (39k samples, 7x the uniform slice's maximum degree), so Hogwild
+conflicts concentrate on it and the deterministic schedule needs ~39k waves.
+"""
+import numpy as np
+import pytest
+
+import datagen
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def mf():
+    from paper_1610_05838_b200 import mf
+    return mf
+
+
+@pytest.fixture(scope="module")
+def zipf():
+    cfg = datagen.CONFIGS["C2-zipf-1pct"]
+    return cfg, datagen.make(cfg)
+
+
+def _ctx(mf, cfg, **kw):
+    return mf.MF(cfg.m, cfg.n, cfg.k, cfg.alpha, cfg.lam, cfg.seed_init, beta=cfg.beta,
+                 seed_shuffle=cfg.seed_shuffle, **kw)
+
+
+def test_skewed_deterministic_parity(mf, zipf):
+    cfg, ((u, v, r), _) = zipf
+    order = oracle.shuffle_perm(cfg.seed_shuffle, len(u))
+    ref = oracle.Model(cfg.m, cfg.n, cfg.k, oracle.F32, seed=cfg.seed_init)
+    ref.epoch(u, v, r, oracle.eta(cfg.alpha, cfg.beta, 0), cfg.lam, order)
+    with _ctx(mf, cfg) as g:
+        g.load(u, v, r)
+        assert mf.mf_wave_count(g.h) == oracle.waves(cfg.m, cfg.n, u, v, order)[1]
+        g.epoch("deterministic")
+        P, Q = g.factors()
+    assert np.linalg.norm(P - ref.P) / np.linalg.norm(ref.P) <= 1e-5
+    assert np.linalg.norm(Q - ref.Q) / np.linalg.norm(ref.Q) <= 1e-5
+
+
+@pytest.mark.parametrize("schedule,opts", [("hogwild", {}), ("wavefront", {"wave_cta": 1}), ("wavefront", {}),
+                                           ("partitioned", {"partitions": 4})])
+def test_skewed_schedules_rmse_within_half_percent(mf, zipf, schedule, opts):
+    cfg, ((u, v, r), test) = zipf
+    E = 10
+    order = oracle.shuffle_perm(cfg.seed_shuffle, len(u))
+    _, trace = oracle.train(cfg.m, cfg.n, cfg.k, oracle.F32, cfg.seed_init, u, v, r, cfg.alpha, cfg.beta, cfg.lam,
+                            E, order=order, test=test)
+    with _ctx(mf, cfg, count_updates=1, **opts) as g:
+        g.load(u, v, r)
+        for _ in range(E):
+            assert g.epoch(schedule).updates == len(u)
+        got = g.rmse(*test)
+    assert abs(got - trace[-1]) <= 0.005 * trace[-1], (got, trace[-1])
+
+
+def test_per_epoch_reshuffle_is_serial_sgd_on_the_composed_orders(mf):
+    """MF_OPT_SHUFFLE=2 with one worker: epoch t runs serially over order_t = order_{t-1}[pi_t],
+    pi_t the A-8 permutation under seed ^ (t << 48); mf_get_order reports order_t."""
+    cfg = datagen.CONFIGS["C1"]
+    (u, v, r), test = datagen.make(cfg)
+    N = len(u)
+    ref = oracle.Model(cfg.m, cfg.n, cfg.k, oracle.F32, seed=cfg.seed_init)
+    order = oracle.shuffle_perm(cfg.seed_shuffle, N)
+    with _ctx(mf, cfg, shuffle=2, workers=1) as g:
+        g.load(u, v, r)
+        for t in range(3):
+            if t > 0:
+                order = order[oracle.shuffle_perm(cfg.seed_shuffle ^ (t << 48), N)]
+            g.epoch("hogwild")
+            np.testing.assert_array_equal(g.order(), order)
+            ref.epoch(u, v, r, oracle.eta(cfg.alpha, cfg.beta, t), cfg.lam, order)
+        P, Q = g.factors()
+    assert np.linalg.norm(P - ref.P) / np.linalg.norm(ref.P) <= 2e-5
+    assert np.linalg.norm(Q - ref.Q) / np.linalg.norm(ref.Q) <= 2e-5
