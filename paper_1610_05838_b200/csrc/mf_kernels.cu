@@ -213,7 +213,18 @@ static cudaError_t hogwild_launch(const UpdateArgs &a, int workers, cudaStream_t
     // workers = concurrent ratings = active groups x D
     int64_t groups = (int64_t)sms * per_sm * kWarpsPerBlock * SH::G;
     if (workers > 0) groups = std::min<int64_t>(groups, (workers + D - 1) / D);
-    const int64_t chunks = (a.n + a.batch_f - 1) / a.batch_f;
+    // Small launches (the partitioned path's sub-blocks): shrink the chunk so every warp gets at
+    // least ~4 chunks -- with fewer chunks than warps one warp would walk 256 samples serially while
+    // the rest idle.  Any f > 128/12 keeps the R-stream locality the paper chose f for.
+    int batch_f = a.batch_f;
+    {
+        const int64_t want_warps = (groups + SH::G - 1) / SH::G;
+        if ((a.n + batch_f - 1) / batch_f < 4 * want_warps) {
+            const int64_t f = a.n / (4 * want_warps);
+            batch_f = (int)std::max<int64_t>(32, std::min<int64_t>(batch_f, (f / 32) * 32));
+        }
+    }
+    const int64_t chunks = (a.n + batch_f - 1) / batch_f;
     groups = std::max<int64_t>(1, std::min<int64_t>(groups, chunks * SH::G));
     // Balance the SMs: when the grid spans more than one CTA per SM, round the CTA count down to a
     // multiple of the SM count so every SM runs the same number of warps (an SM holding one CTA
@@ -228,6 +239,7 @@ static cudaError_t hogwild_launch(const UpdateArgs &a, int workers, cudaStream_t
     if (used) *used = (int)(groups * D);
     UpdateArgs args = a;
     args.active_groups = groups;
+    args.batch_f = batch_f;
     // every launch claims chunks from 0 (the partitioned path launches once per block)
     cudaError_t e = cudaMemsetAsync(&a.scratch->chunk, 0, sizeof(unsigned long long), st);
     if (e != cudaSuccess) return e;
