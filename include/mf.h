@@ -81,7 +81,7 @@ typedef enum {
     MF_OPT_SEED_SHUFFLE = 13, /* seed of the A-8 shuffle (default: the mf_create seed) */
     MF_OPT_VARIANT = 14,      /* kernel variant selector for tuning (0 = default) */
     MF_OPT_TRACE = 15,        /* wavefront audit trace: 1 = record (worker, block, t_start, t_end) per block */
-    MF_OPT_SUBEPOCHS = 16,    /* partitioned: passes S per epoch, each over 1/S of the shuffled samples with its own Latin square (0 = auto, max(4, G)) */
+    MF_OPT_SUBEPOCHS = 16,    /* partitioned: passes S per epoch, each over 1/S of the shuffled samples with its own Latin square (0 = auto = 4) */
     MF_OPT_WAVE_CTA = 17,     /* wavefront worker: 0 = one warp, block processed serially; 1 = one 1024-thread CTA
                                  per SM with the column group's Q rows staged in shared memory, lock-free inside the block;
                                  2 = as 1 with two 512-thread CTA workers per SM */

@@ -31,7 +31,7 @@ struct mf_ctx {
     int shuffle = 1;
     int count_updates = 0;
     int partitions = 0;
-    int subepochs = 0;  // passes per epoch of the partitioned schedule (MF_OPT_SUBEPOCHS; 0 = max(4, G))
+    int subepochs = 0;  // passes per epoch of the partitioned schedule (MF_OPT_SUBEPOCHS; 0 = 4)
     int wave_cta = 0;   // wavefront worker = CTA with shared-memory Q group (MF_OPT_WAVE_CTA)
     int variant = 0;
     int trace = 0;

@@ -115,15 +115,31 @@ __global__ void __launch_bounds__(kBlock) k_hogwild(UpdateArgs a) {
 
     // Chunk claims run one chunk ahead and triple tiles one tile ahead, so neither the claim
     // atomic nor the 3 x 128-byte triple loads sit on the per-rating critical path.
-    auto claim = [&]() -> int64_t {
+    // The claim counter counts samples.  A warp claims f samples at a time until the last ~one chunk
+    // per warp remains, then single 32-sample tiles, so the launch drains in about one tile's time
+    // (the partitioned path runs many launches per epoch).
+    // The first two chunks of every warp are static (warp w: chunks w and W + w), so the launch does
+    // not open with W x 2 same-address atomics; the shared counter hands out the rest, starting
+    // after those 2W chunks.
+    const int64_t nwarps = (a.active_groups + G - 1) / G;
+    const int64_t tail_zone = nwarps * (int64_t)f;
+    const int64_t dyn0 = 2 * nwarps * (int64_t)f;
+    auto claim = [&](int64_t *len) -> int64_t {
         unsigned long long c = 0;
-        if (lane == 0) c = atomicAdd(&a.scratch->chunk, 1ull);
-        return (int64_t)__shfl_sync(0xffffffffu, c, 0) * f;
+        int want = f;
+        if (lane == 0) {
+            const unsigned long long seen = *(volatile unsigned long long *)&a.scratch->chunk;
+            if (dyn0 + (int64_t)seen + tail_zone >= N) want = 32;
+            c = atomicAdd(&a.scratch->chunk, (unsigned long long)want);
+        }
+        *len = __shfl_sync(0xffffffffu, want, 0);
+        return dyn0 + (int64_t)__shfl_sync(0xffffffffu, c, 0);
     };
-    int64_t base = claim();
-    int64_t next_chunk = claim();
+    int64_t len0 = f, next_len = f;
+    int64_t base = warp_id * (int64_t)f;
+    int64_t next_chunk = (nwarps + warp_id) * (int64_t)f;
     if (base >= N) return;
-    int64_t end = min(base + (int64_t)f, N);
+    int64_t end = min(base + len0, N);
     int32_t tu, tv;
     float tr;
     {
@@ -137,8 +153,8 @@ __global__ void __launch_bounds__(kBlock) k_hogwild(UpdateArgs a) {
         int64_t nbase = base + 32, nend = end;
         if (nbase >= end) {  // next tile starts the chunk claimed one chunk ago; claim the one after
             nbase = next_chunk;
-            nend = min(nbase + (int64_t)f, N);
-            if (nbase < N) next_chunk = claim();
+            nend = min(nbase + next_len, N);
+            if (nbase < N) next_chunk = claim(&next_len);
         }
         const bool more = nbase < N;
         int32_t nu = 0, nv = 0;
@@ -154,7 +170,8 @@ __global__ void __launch_bounds__(kBlock) k_hogwild(UpdateArgs a) {
             const int cnt = (int)(end - base < 32 ? end - base : 32);
             if (a.count_updates) done += (lane == 0) ? cnt : 0;
 #pragma unroll 1
-            for (int j0 = 0; j0 < ntile; j0 += D) {
+            const int steps = (cnt + gper - 1) / gper < ntile ? (cnt + gper - 1) / gper : ntile;
+            for (int j0 = 0; j0 < steps; j0 += D) {
                 int32_t su[D], sv[D];
                 float sr[D];
                 bool val[D];
@@ -205,11 +222,19 @@ __global__ void __launch_bounds__(kBlock) k_hogwild(UpdateArgs a) {
 
 template <class SH, int D>
 static cudaError_t hogwild_launch(const UpdateArgs &a, int workers, cudaStream_t st, int *used) {
-    int dev = 0, sms = 0, per_sm = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_hogwild<SH, D>, kBlock, 0);
-    if (per_sm < 1) per_sm = 1;
+    // occupancy and SM count are queried once per instantiation: the partitioned path launches this
+    // kernel hundreds of times per epoch and the host must stay ahead of ~80 us launches
+    static const int sms = [] {
+        int dev = 0, v = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+        return v;
+    }();
+    static const int per_sm = [] {
+        int v = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, k_hogwild<SH, D>, kBlock, 0);
+        return v < 1 ? 1 : v;
+    }();
     // workers = concurrent ratings = active groups x D
     int64_t groups = (int64_t)sms * per_sm * kWarpsPerBlock * SH::G;
     if (workers > 0) groups = std::min<int64_t>(groups, (workers + D - 1) / D);

@@ -20,7 +20,7 @@ def main():
     ap.add_argument("--cfg", default="C2")
     ap.add_argument("--epochs", type=int, default=3)
     ap.add_argument("--storage", default="f32,f16")
-    ap.add_argument("--variants", default="0")
+    ap.add_argument("--variants", default="-1", help="-1 = bench.py's default for the storage")
     ap.add_argument("--workers", default="0")
     ap.add_argument("--batch", default="256")
     ap.add_argument("--k", type=int, default=0)
@@ -44,7 +44,7 @@ def main():
         for var in [int(x) for x in a.variants.split(",")]:
             for w in [int(x) for x in a.workers.split(",")]:
                 for f in [int(x) for x in a.batch.split(",")]:
-                    g.set(mf.MF_OPT_VARIANT, var)
+                    g.set(mf.MF_OPT_VARIANT, var if var >= 0 else (16 if storage != "f32" else 0))
                     g.set(mf.MF_OPT_WORKERS, w)
                     g.set(mf.MF_OPT_BATCH_F, f)
                     ks = []
