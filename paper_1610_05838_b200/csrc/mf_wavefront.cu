@@ -254,23 +254,22 @@ __global__ void __launch_bounds__(THREADS, kCtaThreads / THREADS) k_wavefront_ct
         const int64_t t0 = a.trace ? globaltimer() : 0;
         const int64_t blk = (int64_t)w * c + col;
         const int64_t lo = a.off[blk], hi = a.off[blk + 1];
-        const int64_t blk_n = hi - lo;
+        // 32-sample tiles.  (Claiming smaller tiles near the end of a block balances the warps but
+        // raises the number of a small block's samples in flight at once -- more write conflicts on
+        // the group's Q rows: C3-1pct test RMSE +2.0% vs +0.3%, and 4-7% slower on C2.  Prefetching the
+        // next tile's triples costs registers under the 64-per-thread cap of a 1024-thread CTA: f16
+        // spills and drops from 12.0 to 10.8 G updates/s on C2.)
         for (;;) {
-            // 32-sample tiles.  (Claiming smaller tiles near the end of a block balances the warps but
-            // raises the number of a small block's samples in flight at once -- more write conflicts
-            // on the group's Q rows: C3-1pct test RMSE +2.0% vs +0.3%, and 4-7% slower on C2.)
-            int t = 0, want = 32;
-            if (lane == 0) t = atomicAdd(&s_next, want);
-            t = __shfl_sync(0xffffffffu, t, 0);
-            (void)blk_n;
-            const int64_t base = lo + t;
+            int t = 0;
+            if (lane == 0) t = atomicAdd(&s_next, 32);
+            const int64_t base = lo + __shfl_sync(0xffffffffu, t, 0);
             if (base >= hi) break;  // warp-uniform
             const int64_t i = base + lane;
-            const bool ok = lane < want && i < hi;
+            const bool ok = i < hi;
             const int32_t tu = ok ? __ldg(a.u + i) : 0;
             const int32_t tv = ok ? (int32_t)(__ldg(a.v + i) - q0) : 0;
             const float tr = ok ? __ldg(a.r + i) : 0.f;
-            const int cnt = (int)(hi - base < want ? hi - base : want);
+            const int cnt = (int)(hi - base < 32 ? hi - base : 32);
             if (lane == 0) done += cnt;
             const int per_group = (cnt + G - 1) / G;
 #pragma unroll 1
