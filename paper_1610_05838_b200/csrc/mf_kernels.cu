@@ -272,9 +272,10 @@ static cudaError_t hogwild_launch(const UpdateArgs &a, int workers, cudaStream_t
     return cudaGetLastError();
 }
 
-cudaError_t launch_hogwild(const ShapeId &sh, const UpdateArgs &a, int workers, int variant, cudaStream_t st,
+cudaError_t launch_hogwild(const ShapeId &sh, const UpdateArgs &a_in, int workers, int variant, cudaStream_t st,
                            int *workers_used) {
     const int D = (variant >> 4) & 0xF;  // bits 4..7 select samples in flight per group (0 = default)
+    const UpdateArgs &a = a_in;
     return dispatch_shape(sh, [&](auto tag) -> cudaError_t {
         using SH = decltype(tag);
         constexpr int L = SH::L;

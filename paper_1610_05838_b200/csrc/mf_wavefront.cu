@@ -278,7 +278,6 @@ __global__ void __launch_bounds__(THREADS, kCtaThreads / THREADS) k_wavefront_ct
                 float sr[D], dot[D];
                 bool val[D];
                 RowRaw<SH> pr[D], qr[D];
-                float pf[D][SH::E], qf[D][SH::E];
 #pragma unroll
                 for (int d = 0; d < D; d++) {
                     const int s = (j0 + d) * G + grp;
@@ -299,18 +298,24 @@ __global__ void __launch_bounds__(THREADS, kCtaThreads / THREADS) k_wavefront_ct
 #pragma unroll
                             for (int x = 0; x < SH::NW; x++) qr[d].w[jv][x] = 0u;
                     }
-                    widen_row<SH>(pr[d], pf[d]);
-                    widen_row<SH>(qr[d], qf[d]);
-                    dot[d] = lane_dot<SH>(pf[d], qf[d]);
+                    float p[SH::E], q[SH::E];
+                    widen_row<SH>(pr[d], p);
+                    widen_row<SH>(qr[d], q);
+                    dot[d] = lane_dot<SH>(p, q);
                 }
                 group_allreduce<SH, D>(dot);
 #pragma unroll
                 for (int d = 0; d < D; d++) {
                     const float err = sr[d] - dot[d];
                     if (val[d] && !isfinite(err)) bad = 1;
-                    sgd_step<SH>(pf[d], qf[d], err, a.eta, a.lam);
-                    narrow_row<SH>(pf[d], pr[d]);
-                    narrow_row<SH>(qf[d], qr[d]);
+                    // widen again from the raw rows instead of keeping D x 2E floats alive across the
+                    // butterfly (register cap of a 1024-thread CTA; free for fp32)
+                    float p[SH::E], q[SH::E];
+                    widen_row<SH>(pr[d], p);
+                    widen_row<SH>(qr[d], q);
+                    sgd_step<SH>(p, q, err, a.eta, a.lam);
+                    narrow_row<SH>(p, pr[d]);
+                    narrow_row<SH>(q, qr[d]);
                     store_row<SH>(a.P, su[d], k, sub, val[d], pr[d]);
                     unsigned char *qrow = qs + (int64_t)sv[d] * row_bytes;
 #pragma unroll
