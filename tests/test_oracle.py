@@ -82,6 +82,48 @@ def test_p1_worked_example_exact(storage):
     assert m.rmse(tu, tv, tr) == pytest.approx(math.sqrt(1 / 8), abs=0, rel=1e-15)
 
 
+def _round_bf16(x: Fraction) -> Fraction:
+    """Exact round-to-nearest-even of a rational to bfloat16 (8 significand bits), no float involved."""
+    if x == 0:
+        return Fraction(0)
+    sign = -1 if x < 0 else 1
+    a = abs(x)
+    e = a.numerator.bit_length() - a.denominator.bit_length()
+    if Fraction(2) ** e > a:
+        e -= 1
+    ulp = Fraction(2) ** (e - 7)
+    q, rem = divmod(a, ulp)
+    if rem * 2 > ulp or (rem * 2 == ulp and q % 2 == 1):
+        q += 1
+    return sign * q * ulp
+
+
+def test_p1_worked_example_bf16_storage():
+    """bf16 storage pin: the same three updates in exact rationals, each stored value rounded to bf16
+    by an exact nearest-even rule (the dyadic intermediates are exact in the oracle's fp32 math)."""
+    g = _p1()
+    P0 = [[_round_bf16(_fr(x)) for x in row] for row in g["P0"]]
+    Q0 = [[_round_bf16(_fr(x)) for x in row] for row in g["Q0"]]
+    P, Q = [row[:] for row in P0], [row[:] for row in Q0]
+    eta, lam = _fr(g["eta"]), _fr(g["lambda"])
+    for u, v, r in g["samples"]:
+        p, q = P[u][:], Q[v][:]
+        e = _fr(r) - sum(a * b for a, b in zip(p, q))
+        P[u] = [_round_bf16(p[d] + eta * (e * q[d] - lam * p[d])) for d in range(2)]
+        Q[v] = [_round_bf16(q[d] + eta * (e * p[d] - lam * q[d])) for d in range(2)]
+    bf = lambda rows: (np.array([[float(x) for x in row] for row in rows], np.float32).view(np.uint32) >> 16  # noqa
+                       ).astype(np.uint16)
+    m = oracle.Model(4, 4, 2, BF16, P=bf(P0), Q=bf(Q0))
+    u = np.array([s[0] for s in g["samples"]], np.int32)
+    v = np.array([s[1] for s in g["samples"]], np.int32)
+    r = np.array([float(_fr(s[2])) for s in g["samples"]], np.float32)
+    assert m.epoch(u, v, r, 0.25, 0.5) == 0
+    Pw, Qw = oracle.widen(m.P, BF16), oracle.widen(m.Q, BF16)
+    np.testing.assert_array_equal(Pw, np.array([[float(x) for x in row] for row in P], np.float32))
+    np.testing.assert_array_equal(Qw, np.array([[float(x) for x in row] for row in Q], np.float32))
+    assert Qw[1, 1] != float(_fr("1479/2048"))  # bf16 rounding is visible in this example
+
+
 def test_p1_discriminates_snapshot_reading():
     """Reading A-1: under the sequential reading step 1 would give Q0=[11/16, 67/64]."""
     g = _p1()
