@@ -22,12 +22,14 @@ def main():
     name, storage = sys.argv[1], sys.argv[2]
     cfg = datagen.CONFIGS[name]
     epochs = int(sys.argv[3]) if len(sys.argv) > 3 else cfg.epochs
+    seed_sh = int(sys.argv[4]) if len(sys.argv) > 4 else cfg.seed_shuffle  # other seeds: the order's spread
     st = oracle.STORAGE_NAME[storage]
     (u, v, r), test = datagen.make(cfg)
-    order = oracle.shuffle_perm(cfg.seed_shuffle, len(u))
+    order = oracle.shuffle_perm(seed_sh, len(u))
     m = oracle.Model(cfg.m, cfg.n, cfg.k, st, seed=cfg.seed_init)
-    out = os.path.join(ROOT, "tests", "golden", f"{name}_{storage}_trace.json")
-    rec = {"what": f"oracle test RMSE per epoch, serial SGD on the A-8 shuffled order (seed {cfg.seed_shuffle}), "
+    tag = "" if seed_sh == cfg.seed_shuffle else f"_seed{seed_sh}"
+    out = os.path.join(ROOT, "tests", "golden", f"{name}_{storage}{tag}_trace.json")
+    rec = {"what": f"oracle test RMSE per epoch, serial SGD on the A-8 shuffled order (seed {seed_sh}), "
                    f"init A-7 (seed {cfg.seed_init}), {storage} storage",
            "written_by": "scripts/make_golden.py (calls only oracle/ and datagen/)",
            "config": cfg.__dict__, "rmse": [], "seconds": []}
