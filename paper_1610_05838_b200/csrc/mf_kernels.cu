@@ -32,9 +32,9 @@ static constexpr int kWarpsPerBlock = kBlock / 32;
     X(kF32, 8, 1, 16, 1) X(kF32, 16, 1, 16, 1) X(kF32, 32, 1, 16, 1) X(kF32, 32, 2, 16, 1)               \
     X(kF32, 16, 2, 16, 1) X(kF32, 8, 4, 16, 1)                                                           \
     X(kF16, 4, 1, 16, 1) X(kF16, 8, 1, 16, 1) X(kF16, 16, 1, 16, 1) X(kF16, 32, 1, 16, 1)                \
-    X(kF16, 8, 2, 16, 1) X(kF16, 32, 1, 8, 1)                                                            \
+    X(kF16, 8, 2, 16, 1) X(kF16, 32, 1, 8, 1) X(kF16, 4, 4, 16, 1)                                       \
     X(kBF16, 4, 1, 16, 1) X(kBF16, 8, 1, 16, 1) X(kBF16, 16, 1, 16, 1) X(kBF16, 32, 1, 16, 1)            \
-    X(kBF16, 8, 2, 16, 1) X(kBF16, 32, 1, 8, 1)
+    X(kBF16, 8, 2, 16, 1) X(kBF16, 32, 1, 8, 1) X(kBF16, 4, 4, 16, 1)
 #define MF_GENERIC_SHAPES(X)                                                                             \
     X(kF32, 32, 1, 4, 0) X(kF32, 32, 4, 4, 0) X(kF32, 32, 16, 4, 0) X(kF32, 32, 32, 4, 0)                \
     X(kF16, 32, 1, 4, 0) X(kF16, 32, 4, 4, 0) X(kF16, 32, 16, 4, 0)                                      \
@@ -68,6 +68,7 @@ ShapeId select_shape(int k, int storage, int variant) {
         if (k == 128) {
             if (variant == 1) return {storage, 8, 2, 16, 1};
             if (variant == 2) return {storage, 32, 1, 8, 1};
+            if (variant == 3) return {storage, 4, 4, 16, 1};
             return {storage, 16, 1, 16, 1};
         }
         if (k == 32) return {storage, 4, 1, 16, 1};

@@ -176,30 +176,33 @@ __global__ void __launch_bounds__(kBlock) k_wavefront(WfArgs a) {
 // copied back to global memory before the column lock is released.
 constexpr int kCtaThreads = 1024;
 
+// Q rows in shared memory are addressed with 32-bit shared-window offsets (ld/st.shared): no
+// generic-to-shared conversion per access.  volatile keeps this thread's st before its next ld of
+// the same row; other warps' races on a row are the lock-free semantics (batch-Hogwild! in a block).
 template <int VB>
-__device__ __forceinline__ void smem_ld(const unsigned char *p, uint32_t (&w)[Vec<VB>::NW]) {
+__device__ __forceinline__ void smem_ld(uint32_t a, uint32_t (&w)[Vec<VB>::NW]) {
     if constexpr (VB == 16) {
-        const uint4 x = *reinterpret_cast<const uint4 *>(p);
-        w[0] = x.x; w[1] = x.y; w[2] = x.z; w[3] = x.w;
+        asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3]) : "r"(a));
     } else if constexpr (VB == 8) {
-        const uint2 x = *reinterpret_cast<const uint2 *>(p);
-        w[0] = x.x; w[1] = x.y;
+        asm volatile("ld.shared.v2.u32 {%0,%1}, [%2];" : "=r"(w[0]), "=r"(w[1]) : "r"(a));
     } else if constexpr (VB == 4) {
-        w[0] = *reinterpret_cast<const uint32_t *>(p);
+        asm volatile("ld.shared.u32 %0, [%1];" : "=r"(w[0]) : "r"(a));
     } else {
-        w[0] = *reinterpret_cast<const unsigned short *>(p);
+        unsigned short h;
+        asm volatile("ld.shared.u16 %0, [%1];" : "=h"(h) : "r"(a));
+        w[0] = h;
     }
 }
 template <int VB>
-__device__ __forceinline__ void smem_st(unsigned char *p, const uint32_t (&w)[Vec<VB>::NW]) {
+__device__ __forceinline__ void smem_st(uint32_t a, const uint32_t (&w)[Vec<VB>::NW]) {
     if constexpr (VB == 16) {
-        *reinterpret_cast<uint4 *>(p) = make_uint4(w[0], w[1], w[2], w[3]);
+        asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(a), "r"(w[0]), "r"(w[1]), "r"(w[2]), "r"(w[3]));
     } else if constexpr (VB == 8) {
-        *reinterpret_cast<uint2 *>(p) = make_uint2(w[0], w[1]);
+        asm volatile("st.shared.v2.u32 [%0], {%1,%2};" ::"r"(a), "r"(w[0]), "r"(w[1]));
     } else if constexpr (VB == 4) {
-        *reinterpret_cast<uint32_t *>(p) = w[0];
+        asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(w[0]));
     } else {
-        *reinterpret_cast<unsigned short *>(p) = (unsigned short)(w[0] & 0xFFFFu);
+        asm volatile("st.shared.u16 [%0], %1;" ::"r"(a), "h"((unsigned short)(w[0] & 0xFFFFu)));
     }
 }
 
@@ -223,18 +226,84 @@ __device__ __forceinline__ void cta_copy_out(unsigned char *dst, const unsigned 
     }
 }
 
+// One 32-sample tile of a block (lane i of the warp holds sample base+i: tu, tv relative to the
+// group's first column, tr).  G groups of L lanes, D ratings in flight per group.  FULLTILE: cnt == 32,
+// no sample predicates (every tile but a block's last).  chk accumulates err * 0, which is NaN iff
+// some err was not finite (one FFMA per rating instead of a compare-and-select).
+template <class SH, int D, bool FULLTILE>
+__device__ __forceinline__ void cta_tile(const WfArgs &a, uint32_t qbase, int k, int grp, int sub, int cnt,
+                                         int32_t tu, int32_t tv, float tr, float &chk) {
+    constexpr int G = SH::G;
+    constexpr uint32_t kRowBytes = SH::FULL ? (uint32_t)(SH::KMAX * SH::BYTES) : 0u;
+    const uint32_t row_bytes = SH::FULL ? kRowBytes : (uint32_t)k * SH::BYTES;
+    const int per_group = FULLTILE ? 32 / G : (cnt + G - 1) / G;
+#pragma unroll 1
+    for (int j0 = 0; j0 < per_group; j0 += D) {
+        int32_t su[D];
+        uint32_t qa[D];
+        float sr[D], dot[D];
+        bool val[D];
+        RowRaw<SH> pr[D], qr[D];
+#pragma unroll
+        for (int d = 0; d < D; d++) {
+            const int s = (j0 + d) * G + grp;
+            su[d] = __shfl_sync(0xffffffffu, tu, s);
+            qa[d] = qbase + (uint32_t)__shfl_sync(0xffffffffu, tv, s) * row_bytes;
+            sr[d] = __shfl_sync(0xffffffffu, tr, s);
+            val[d] = FULLTILE || s < cnt;
+            load_row<SH>(a.P, su[d], k, sub, val[d], pr[d]);
+        }
+#pragma unroll
+        for (int d = 0; d < D; d++) {
+#pragma unroll
+            for (int jv = 0; jv < SH::V; jv++) {
+                const int e = (int)vec_elem<SH>(jv, sub);
+                if (val[d] && (SH::FULL || e < k)) smem_ld<SH::VB>(qa[d] + (uint32_t)(e * SH::BYTES), qr[d].w[jv]);
+                else
+#pragma unroll
+                    for (int x = 0; x < SH::NW; x++) qr[d].w[jv][x] = 0u;
+            }
+            float p[SH::E], q[SH::E];
+            widen_row<SH>(pr[d], p);
+            widen_row<SH>(qr[d], q);
+            dot[d] = lane_dot<SH>(p, q);
+        }
+        group_allreduce<SH, D>(dot);
+#pragma unroll
+        for (int d = 0; d < D; d++) {
+            const float err = sr[d] - dot[d];  // 0 for an invalid slot (zero rows, r = 0)
+            chk = fmaf(err, 0.f, chk);
+            // widen again from the raw rows instead of keeping D x 2E floats alive across the
+            // butterfly (register cap of a 1024-thread CTA; free for fp32)
+            float p[SH::E], q[SH::E];
+            widen_row<SH>(pr[d], p);
+            widen_row<SH>(qr[d], q);
+            sgd_step<SH>(p, q, err, a.eta, a.lam);
+            narrow_row<SH>(p, pr[d]);
+            narrow_row<SH>(q, qr[d]);
+            store_row<SH>(a.P, su[d], k, sub, val[d], pr[d]);
+#pragma unroll
+            for (int jv = 0; jv < SH::V; jv++) {
+                const int e = (int)vec_elem<SH>(jv, sub);
+                if (val[d] && (SH::FULL || e < k)) smem_st<SH::VB>(qa[d] + (uint32_t)(e * SH::BYTES), qr[d].w[jv]);
+            }
+        }
+    }
+}
+
 template <class SH, int D, int THREADS>
 __global__ void __launch_bounds__(THREADS, THREADS >= 1024 ? 1 : kCtaThreads / THREADS) k_wavefront_cta(WfArgs a) {
     extern __shared__ __align__(16) unsigned char qs[];
     __shared__ int s_col, s_next;
-    constexpr int L = SH::L, G = SH::G;
+    constexpr int L = SH::L;
     const int lane = threadIdx.x & 31, grp = lane / L, sub = lane % L;
     const int w = blockIdx.x;
     if (w >= a.s) return;  // CTA-uniform
     const int k = SH::FULL ? SH::KMAX : a.k;
     const int64_t row_bytes = (int64_t)k * SH::BYTES;
     const int c = a.c;
-    int bad = 0;
+    const uint32_t qbase = (uint32_t)__cvta_generic_to_shared(qs);
+    float chk = 0.f;
     unsigned long long done = 0;
     for (int j = 0; j < c; j++) {
         if (threadIdx.x == 0) {
@@ -271,60 +340,8 @@ __global__ void __launch_bounds__(THREADS, THREADS >= 1024 ? 1 : kCtaThreads / T
             const float tr = ok ? __ldg(a.r + i) : 0.f;
             const int cnt = (int)(hi - base < 32 ? hi - base : 32);
             if (lane == 0) done += cnt;
-            const int per_group = (cnt + G - 1) / G;
-#pragma unroll 1
-            for (int j0 = 0; j0 < per_group; j0 += D) {  // D ratings of the tile in flight per group
-                int32_t su[D], sv[D];
-                float sr[D], dot[D];
-                bool val[D];
-                RowRaw<SH> pr[D], qr[D];
-#pragma unroll
-                for (int d = 0; d < D; d++) {
-                    const int s = (j0 + d) * G + grp;
-                    su[d] = __shfl_sync(0xffffffffu, tu, s);
-                    sv[d] = __shfl_sync(0xffffffffu, tv, s);
-                    sr[d] = __shfl_sync(0xffffffffu, tr, s);
-                    val[d] = s < cnt;
-                    load_row<SH>(a.P, su[d], k, sub, val[d], pr[d]);
-                }
-#pragma unroll
-                for (int d = 0; d < D; d++) {
-                    const unsigned char *qrow = qs + (int64_t)sv[d] * row_bytes;
-#pragma unroll
-                    for (int jv = 0; jv < SH::V; jv++) {
-                        const int64_t e = vec_elem<SH>(jv, sub);
-                        if (val[d] && (SH::FULL || e < k)) smem_ld<SH::VB>(qrow + e * SH::BYTES, qr[d].w[jv]);
-                        else
-#pragma unroll
-                            for (int x = 0; x < SH::NW; x++) qr[d].w[jv][x] = 0u;
-                    }
-                    float p[SH::E], q[SH::E];
-                    widen_row<SH>(pr[d], p);
-                    widen_row<SH>(qr[d], q);
-                    dot[d] = lane_dot<SH>(p, q);
-                }
-                group_allreduce<SH, D>(dot);
-#pragma unroll
-                for (int d = 0; d < D; d++) {
-                    const float err = sr[d] - dot[d];
-                    if (val[d] && !isfinite(err)) bad = 1;
-                    // widen again from the raw rows instead of keeping D x 2E floats alive across the
-                    // butterfly (register cap of a 1024-thread CTA; free for fp32)
-                    float p[SH::E], q[SH::E];
-                    widen_row<SH>(pr[d], p);
-                    widen_row<SH>(qr[d], q);
-                    sgd_step<SH>(p, q, err, a.eta, a.lam);
-                    narrow_row<SH>(p, pr[d]);
-                    narrow_row<SH>(q, qr[d]);
-                    store_row<SH>(a.P, su[d], k, sub, val[d], pr[d]);
-                    unsigned char *qrow = qs + (int64_t)sv[d] * row_bytes;
-#pragma unroll
-                    for (int jv = 0; jv < SH::V; jv++) {
-                        const int64_t e = vec_elem<SH>(jv, sub);
-                        if (val[d] && (SH::FULL || e < k)) smem_st<SH::VB>(qrow + e * SH::BYTES, qr[d].w[jv]);
-                    }
-                }
-            }
+            if (cnt == 32) cta_tile<SH, D, true>(a, qbase, k, grp, sub, cnt, tu, tv, tr, chk);
+            else cta_tile<SH, D, false>(a, qbase, k, grp, sub, cnt, tu, tv, tr, chk);
         }
         __syncthreads();
         cta_copy_out(reinterpret_cast<unsigned char *>(a.Q) + q0 * row_bytes, qs, nrows * row_bytes);
@@ -339,7 +356,7 @@ __global__ void __launch_bounds__(THREADS, THREADS >= 1024 ? 1 : kCtaThreads / T
         __syncthreads();
         if (threadIdx.x == 0) atomicExch(a.locks + col, 0);
     }
-    if (bad) a.scratch->diverged = 1;
+    if (chk != chk) a.scratch->diverged = 1;
     if (a.count_updates && lane == 0 && done) atomicAdd(&a.scratch->updates, done);
 }
 
@@ -349,7 +366,8 @@ cudaError_t dispatch_cta_shape(const ShapeId &s, F &&f) {
     if (s.storage == S_ && s.L == L_ && s.V == V_ && s.VB == VB_ && s.full == FULL_)                \
         return f(Shape<S_, L_, V_, VB_, (bool)FULL_>{});
     MF_CCASE(kF32, 8, 1, 16, 1) MF_CCASE(kF32, 16, 1, 16, 1) MF_CCASE(kF32, 32, 1, 16, 1)
-    MF_CCASE(kF32, 32, 2, 16, 1) MF_CCASE(kF16, 4, 1, 16, 1) MF_CCASE(kF16, 8, 1, 16, 1)
+    MF_CCASE(kF32, 32, 2, 16, 1) MF_CCASE(kF32, 16, 2, 16, 1) MF_CCASE(kF32, 8, 4, 16, 1)
+    MF_CCASE(kF16, 8, 2, 16, 1) MF_CCASE(kF16, 4, 4, 16, 1) MF_CCASE(kBF16, 8, 2, 16, 1) MF_CCASE(kBF16, 4, 4, 16, 1) MF_CCASE(kF16, 4, 1, 16, 1) MF_CCASE(kF16, 8, 1, 16, 1)
     MF_CCASE(kF16, 16, 1, 16, 1) MF_CCASE(kF16, 32, 1, 16, 1) MF_CCASE(kBF16, 4, 1, 16, 1)
     MF_CCASE(kBF16, 8, 1, 16, 1) MF_CCASE(kBF16, 16, 1, 16, 1) MF_CCASE(kBF16, 32, 1, 16, 1)
     MF_CCASE(kF32, 32, 1, 4, 0) MF_CCASE(kF32, 32, 4, 4, 0) MF_CCASE(kF32, 32, 16, 4, 0) MF_CCASE(kF32, 32, 32, 4, 0)
@@ -533,7 +551,15 @@ int mf_ctx::run_wavefront(const ShapeId &, const UpdateArgs &ua, int *launches, 
         const int64_t max_rows = (n + c - 1) / c;  // balanced column groups
         const size_t smem = (size_t)(max_rows * row_bytes);
         if (smem > 227 * 1024) return fail(MF_EINVAL, "wavefront CTA: column group needs %zu B of shared memory", smem);
-        const ShapeId sh = select_shape(k, storage, 0);
+        // MF_OPT_VARIANT bits 8..11: 0 = tuned default, else the update shape select_shape(variant - 1)
+        // (lanes per rating); bits 12..15: ratings in flight per group, 0 = default, 1 or 2.  Defaults
+        // (r01, C2): k = 128 uses 8 lanes per rating (16 halves or 16 floats per lane) with one rating
+        // in flight -- fewer butterfly levels and broadcast shuffles per rating than the 16/32-lane
+        // shapes of batch-Hogwild! (f16 12.4 -> 13.6, f32 6.5 -> 7.7 G updates/s; profiles/r01_cta_shapes.log).
+        const int shape_sel = (variant >> 8) & 0xF, depth_sel = (variant >> 12) & 0xF;
+        const int def_shape = k == 128 ? (storage == kF32 ? 2 : 1) : 0;
+        const ShapeId sh = select_shape(k, storage, shape_sel ? shape_sel - 1 : def_shape);
+        const bool one_in_flight = depth_sel ? depth_sel == 1 : (k == 128 && !shape_sel);
         CK(dispatch_cta_shape(sh, [&](auto tag) -> cudaError_t {
             using SH = decltype(tag);
             constexpr int DD = (SH::FULL && (32 / SH::G) % 2 == 0) ? 2 : 1;  // 2 ratings in flight per group
@@ -547,6 +573,10 @@ int mf_ctx::run_wavefront(const ShapeId &, const UpdateArgs &ua, int *launches, 
             // MF_OPT_WAVE_CTA = 2: two 512-thread workers per SM, so one's block boundary (write-back,
             // lock hand-over, staging) overlaps the other's updates
             // (a 768-thread worker -- 85 registers, no spills -- measured 8% slower than 1024)
+            if constexpr (DD == 2) {
+                if (one_in_flight && wave_cta == 2) return launch(k_wavefront_cta<SH, 1, 512>, 512);
+                if (one_in_flight) return launch(k_wavefront_cta<SH, 1, 1024>, 1024);
+            }
             if (wave_cta == 2) return launch(k_wavefront_cta<SH, DD, 512>, 512);
             return launch(k_wavefront_cta<SH, DD, 1024>, 1024);
         }));

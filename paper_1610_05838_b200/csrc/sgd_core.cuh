@@ -259,11 +259,24 @@ __device__ __forceinline__ float group_dot(const float (&p)[SH::E], const float 
 template <class SH>
 __device__ __forceinline__ void sgd_step(float (&p)[SH::E], float (&q)[SH::E], float err, float eta, float lam) {
     const float a = 1.f - eta * lam, b = eta * err;
+    if constexpr (SH::E % 2 == 0) {
+        // sm_100 paired fp32 (FMUL2/FFMA2): each lane of the pair is rounded exactly as the scalar
+        // fmaf/fmul below, so results are bit-identical with half the issue slots
+        const float2 a2 = make_float2(a, a), b2 = make_float2(b, b);
 #pragma unroll
-    for (int e = 0; e < SH::E; e++) {
-        const float pe = p[e], qe = q[e];
-        p[e] = fmaf(b, qe, a * pe);
-        q[e] = fmaf(b, pe, a * qe);
+        for (int e = 0; e < SH::E; e += 2) {
+            const float2 pe = make_float2(p[e], p[e + 1]), qe = make_float2(q[e], q[e + 1]);
+            const float2 pn = __ffma2_rn(b2, qe, __fmul2_rn(a2, pe));
+            const float2 qn = __ffma2_rn(b2, pe, __fmul2_rn(a2, qe));
+            p[e] = pn.x, p[e + 1] = pn.y, q[e] = qn.x, q[e + 1] = qn.y;
+        }
+    } else {
+#pragma unroll
+        for (int e = 0; e < SH::E; e++) {
+            const float pe = p[e], qe = q[e];
+            p[e] = fmaf(b, qe, a * pe);
+            q[e] = fmaf(b, pe, a * qe);
+        }
     }
 }
 

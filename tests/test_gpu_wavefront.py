@@ -137,6 +137,43 @@ def test_wavefront_cta_exactly_once_conflict_free_and_rmse(mfmod):
     assert abs(got - trace[-1]) <= 0.005 * trace[-1], (got, trace[-1])
 
 
+_C3_TRACE = {}
+
+
+def _c3_oracle_trace(storage, E):
+    """Oracle test-RMSE trace on C3-1pct for `storage`, computed once per module."""
+    if storage not in _C3_TRACE:
+        cfg = datagen.CONFIGS["C3-1pct"]
+        (u, v, r), test = datagen.make(cfg)
+        order = oracle.shuffle_perm(cfg.seed_shuffle, len(u))
+        st = {0: oracle.F32, 1: oracle.F16}[storage]
+        _, tr = oracle.train(cfg.m, cfg.n, cfg.k, st, cfg.seed_init, u, v, r, cfg.alpha, cfg.beta, cfg.lam, E,
+                             order=order, test=test)
+        _C3_TRACE[storage] = tr
+    return _C3_TRACE[storage]
+
+
+# MF_OPT_VARIANT bits 8..11 = CTA update shape + 1, bits 12..15 = ratings in flight per group
+# (0 = tuned default: 8 lanes per rating, one in flight at k = 128)
+@pytest.mark.parametrize("storage,variant,wave_cta", [
+    (1, 0, 1), (1, 0, 2), (1, (1 << 8) | (2 << 12), 1), (1, (2 << 8) | (2 << 12), 1),
+    (0, 0, 1), (0, 0, 2), (0, (1 << 8) | (2 << 12), 1), (0, (2 << 8) | (2 << 12), 1)])
+def test_wavefront_cta_shapes_rmse(mfmod, storage, variant, wave_cta):
+    """Every CTA update shape / depth (fp16 and fp32 storage, 1x1024 and 2x512 workers per SM): exactly
+    once per epoch and test RMSE within 0.5% of the storage-matched serial oracle after 5 epochs."""
+    cfg = datagen.CONFIGS["C3-1pct"]
+    (u, v, r), test = datagen.make(cfg)
+    E = 5
+    gold = _c3_oracle_trace(storage, E)
+    with mfmod.MF(cfg.m, cfg.n, cfg.k, cfg.alpha, cfg.lam, cfg.seed_init, storage=storage, beta=cfg.beta,
+                  wave_cta=wave_cta, variant=variant, count_updates=1, seed_shuffle=cfg.seed_shuffle) as g:
+        g.load(u, v, r)
+        for _ in range(E):
+            assert g.epoch("wavefront").updates == len(u)
+        got = g.rmse(*test)
+    assert abs(got - gold[-1]) <= 0.005 * gold[-1], (got, gold[-1])
+
+
 @pytest.mark.parametrize("storage,k", [(0, 7), (0, 33), (0, 100), (1, 7), (1, 100), (2, 7), (2, 66)])
 def test_wavefront_cta_single_block_is_serial(mfmod, storage, k):
     """s = c = 1, N = 32 (one tile) and a masked L = 32 shape (one group per warp, one rating in flight):
