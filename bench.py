@@ -224,7 +224,7 @@ def main():
 
     (u, v, r), (tu, tv, tr) = datagen.make(cfg)
     N = len(u)
-    variant = a.variant if a.variant >= 0 else (16 if a.storage != "f32" else 0)
+    variant = a.variant if a.variant >= 0 else 0
     # inputs resident in HBM (torch tensors as device memory), loaded through the C ABI
     du, dv, dr = (torch.from_numpy(x).cuda() for x in (u, v, r))
     dtu, dtv, dtr = (torch.from_numpy(x).cuda() for x in (tu, tv, tr))
@@ -234,7 +234,7 @@ def main():
         """Device-timed steps (epoch + test RMSE) with inputs resident in HBM."""
         if schedule == "wavefront_cta":
             schedule, opts = "wavefront", dict(opts, wave_cta=1)
-        var = a.variant if a.variant >= 0 else (16 if storage != "f32" else 0)
+        var = a.variant if a.variant >= 0 else 0
         g = mf.MF(cfg.m, cfg.n, cfg.k, cfg.alpha, cfg.lam, cfg.seed_init, storage=storage, beta=cfg.beta,
                   seed_shuffle=cfg.seed_shuffle, device=local, stream=stream.cuda_stream, variant=var,
                   workers=a.workers, **opts)
@@ -257,10 +257,11 @@ def main():
         torch.cuda.synchronize()
         if clk:
             clk.__exit__(None, None, None)
+        var_eff = int(g.get(mf.MF_OPT_VARIANT))  # the auto fields resolved (hogwild L2 prefetch pick)
         g.close()
         ms_ = e0.elapsed_time(e1) / steps
         return {"ms": ms_, "value": N / (ms_ * 1e-3), "kernel_s": statistics.mean(kern), "launches": launches,
-                "rmse": rm, "workers": workers, "epochs_done": warmup + steps}
+                "rmse": rm, "workers": workers, "epochs_done": warmup + steps, "variant": var_eff}
 
     clk = Clocks(local)
     head = measure(a.storage, a.schedule, a.steps, a.warmup, clk=clk)
@@ -298,7 +299,7 @@ def main():
             res["alg_GBps"] = b_alg(cfg.k, st_) * N / res["kernel_s"] / 1e9
             res["frac_alg"] = res["alg_GBps"] / peak
             others[key] = {k_: res[k_] for k_ in ("value", "ms", "kernel_s", "rmse", "workers", "alg_GBps",
-                                                  "frac_alg", "epochs_done")}
+                                                  "frac_alg", "epochs_done", "variant")}
 
     # end to end through the public API from pinned host buffers
     hu, hv, hr = (torch.from_numpy(x).pin_memory() for x in (u, v, r))
@@ -339,7 +340,8 @@ def main():
         "warmup": a.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "f32", "storage": a.storage, "data": "synthetic",
         "config": workload_config(cfg, 1, a.storage, a.schedule),
-        "arm": {"workers": workers, "batch_f": 256, "variant": variant},
+        "arm": {"workers": workers, "batch_f": 256, "variant": head["variant"],
+                "l2_row_prefetch": ((head["variant"] >> 16) & 0xF) not in (0, 15)},
         "test_rmse": rmses[-1],
         "roofline": roof,
         "cpu_baseline": cpu,
@@ -384,7 +386,7 @@ def run_partitioned(a, cfg, rank, world, local):
     u += pb
     tu += pb
     N_loc = len(u)
-    variant = a.variant if a.variant >= 0 else (16 if a.storage != "f32" else 0)
+    variant = a.variant if a.variant >= 0 else 0
 
     def make_ctx():
         # a fresh NCCL unique id per communicator (an id bootstraps exactly one ncclCommInitRank)

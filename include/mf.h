@@ -79,7 +79,11 @@ typedef enum {
     MF_OPT_EPOCH = 11,        /* set the epoch index t used by the LR schedule */
     MF_OPT_PARTITIONS = 12,   /* MF_SCHED_PARTITIONED without NCCL: G logical partitions run on this GPU (loopback) */
     MF_OPT_SEED_SHUFFLE = 13, /* seed of the A-8 shuffle (default: the mf_create seed) */
-    MF_OPT_VARIANT = 14,      /* kernel variant selector for tuning (0 = default) */
+    MF_OPT_VARIANT = 14,      /* kernel variant selector for tuning (0 = default).  Bit fields: 0..3 group shape; 4..7
+                                 ratings in flight per batch-Hogwild! group (0 = auto: 2 for fp32, 1 for 16-bit rows);
+                                 8..15 wavefront-CTA shape; 16..19 batch-Hogwild! L2 row prefetch distance in steps
+                                 (0 = auto: MF_SCHED_HOGWILD epochs 0, 1, 2 run off, 1 step, off and the faster of the
+                                 last two is kept; 15 = off).  No setting changes what an update computes. */
     MF_OPT_TRACE = 15,        /* wavefront audit trace: 1 = record (worker, block, t_start, t_end) per block */
     MF_OPT_SUBEPOCHS = 16,    /* partitioned: passes S per epoch, each over 1/S of the shuffled samples with its own Latin square (0 = auto = 4) */
     MF_OPT_WAVE_CTA = 17,     /* wavefront worker: 0 = one warp, block processed serially; 1 = one 1024-thread CTA

@@ -282,6 +282,7 @@ extern "C" int mf_set_option(mf_ctx *ctx, int key, double value) {
             return MF_OK;
         case MF_OPT_VARIANT:
             ctx->variant = (int)iv;
+            ctx->pf_trials = 0, ctx->pf_pick = 0;
             return MF_OK;
         case MF_OPT_TRACE:
             ctx->trace = iv ? 1 : 0;
@@ -322,7 +323,10 @@ extern "C" int mf_get_option(const mf_ctx *ctx, int key, double *value) {
         case MF_OPT_EPOCH: *value = ctx->epoch; return MF_OK;
         case MF_OPT_PARTITIONS: *value = ctx->partitions; return MF_OK;
         case MF_OPT_SEED_SHUFFLE: *value = (double)ctx->seed_shuffle; return MF_OK;
-        case MF_OPT_VARIANT: *value = ctx->variant; return MF_OK;
+        case MF_OPT_VARIANT:  // the variant in effect: an auto prefetch field reports the setting picked
+            *value = ((ctx->variant >> 16) & 0xF) == 0 && ctx->pf_pick ? ctx->variant | (ctx->pf_pick << 16)
+                                                                      : ctx->variant;
+            return MF_OK;
         case MF_OPT_TRACE: *value = ctx->trace; return MF_OK;
         case MF_OPT_SUBEPOCHS: *value = ctx->subepochs ? ctx->subepochs : ctx->part_S; return MF_OK;
         case MF_OPT_WAVE_CTA: *value = ctx->wave_cta; return MF_OK;
@@ -362,6 +366,7 @@ extern "C" int mf_load_coo(mf_ctx *ctx, const int32_t *u, const int32_t *v, cons
     }
     RC(ctx->gather_q());
     ctx->drop_layouts();
+    ctx->pf_trials = 0, ctx->pf_pick = 0;  // a new workload re-runs the prefetch trials
     ctx->seg_valid = false;
     ctx->N = 0;
     const cudaMemcpyKind kind = is_device_ptr(u) ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
@@ -514,6 +519,7 @@ int mf_ctx::finish_epoch(int schedule, float eta, int launches, int workers_used
     float ms_all = 0.f, ms_k = 0.f;
     CK(cudaEventElapsedTime(&ms_all, events[0], events[3]));
     CK(cudaEventElapsedTime(&ms_k, events[1], events[2]));
+    last_kernel_ms = ms_k;
     const int32_t t = epoch;
     epoch++;
     if (stats) {
@@ -555,9 +561,24 @@ extern "C" int mf_epoch(mf_ctx *ctx, int schedule, mf_epoch_stats *stats) {
     UpdateArgs a = ctx->update_args(eta);
     int launches = 1, used = 0;
     CK(cudaEventRecord(ctx->events[1], st));
+    int pf_slot = -1;  // >= 0: this epoch is a prefetch trial (0 = off, 1 = on)
     if (schedule == MF_SCHED_HOGWILD) {
         const int w = ctx->workers > 0 ? ctx->workers : ctx->auto_workers();
-        CK(launch_hogwild(sh, a, w, ctx->variant, st, &used));
+        int var = ctx->variant;
+        if (((var >> 16) & 0xF) == 0) {
+            // Auto prefetch.  Whether an L2 prefetch of the next ratings' rows pays depends on where
+            // the rows live: it hides DRAM latency when Q misses L2 or hot rows queue (Yahoo shape
+            // +11%, Zipf-skewed Netflix shape +15%), and costs L2 request slots where the L2 is
+            // already the bottleneck (Netflix / Hugewiki shapes, -6..-16%).  It never
+            // changes what is computed, so the library times both and keeps the faster.
+            if (ctx->pf_pick) {
+                var |= ctx->pf_pick << 16;
+            } else {
+                pf_slot = ctx->pf_trials == 1 ? 1 : 0;
+                var |= (pf_slot ? 1 : 15) << 16;
+            }
+        }
+        CK(launch_hogwild(sh, a, w, var, st, &used));
     } else if (schedule == MF_SCHED_DETERMINISTIC) {
         a.u = ctx->wu;
         a.v = ctx->wv;
@@ -573,7 +594,12 @@ extern "C" int mf_epoch(mf_ctx *ctx, int schedule, mf_epoch_stats *stats) {
         launches = l;
     }
     CK(cudaEventRecord(ctx->events[2], st));
-    return ctx->finish_epoch(schedule, eta, launches, used, stats);
+    const int rc = ctx->finish_epoch(schedule, eta, launches, used, stats);
+    if (rc == MF_OK && pf_slot >= 0) {
+        ctx->pf_ms[pf_slot] = ctx->last_kernel_ms;
+        if (++ctx->pf_trials >= mf_ctx::kPfTrials) ctx->pf_pick = ctx->pf_ms[1] < 0.97f * ctx->pf_ms[0] ? 1 : 15;
+    }
+    return rc;
 }
 
 // -------------------------------------------------------------------- rmse --

@@ -35,6 +35,13 @@ struct mf_ctx {
     int wave_cta = 0;   // wavefront worker = CTA with shared-memory Q group (MF_OPT_WAVE_CTA)
     int variant = 0;
     int trace = 0;
+    // batch-Hogwild! L2 row prefetch, auto mode (MF_OPT_VARIANT bits 16..19 = 0): hogwild epochs
+    // 0, 1, 2 run prefetch off (a warm-up, not timed), on, off; the faster of the last two is kept
+    static constexpr int kPfTrials = 3;
+    int pf_trials = 0;
+    int pf_pick = 0;        // 0 = undecided, else the bits-16..19 value in use (15 = off, 1 = on)
+    float pf_ms[2] = {0.f, 0.f};
+    float last_kernel_ms = 0.f;
     cudaStream_t user_stream = nullptr;
 
     // device state

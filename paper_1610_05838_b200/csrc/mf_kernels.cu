@@ -113,6 +113,9 @@ __global__ void __launch_bounds__(kBlock) k_hogwild(UpdateArgs a) {
     const int ntile = (32 + gper - 1) / gper;     // samples per group per 32-sample tile
     unsigned long long done = 0;
     int bad = 0;
+    const int ahead = a.prefetch * D;
+    const uint32_t row_bytes = (uint32_t)k * SH::BYTES;
+    const bool pf_on = ahead > 0 && SH::FULL && (row_bytes % 16u) == 0u && (32 % gper) == 0;
 
     // Chunk claims run one chunk ahead and triple tiles one tile ahead, so neither the claim
     // atomic nor the 3 x 128-byte triple loads sit on the per-rating critical path.
@@ -185,6 +188,25 @@ __global__ void __launch_bounds__(kBlock) k_hogwild(UpdateArgs a) {
                     sv[d] = __shfl_sync(0xffffffffu, tv, s);
                     sr[d] = __shfl_sync(0xffffffffu, tr, s);
                     val[d] = grp < gper && s < cnt;
+                }
+                if (pf_on) {
+                    // L2 prefetch of the rows of the ratings `ahead` steps later (this tile or the next
+                    // one).  It moves no values into registers, so it adds memory-level parallelism
+                    // without adding Hogwild! workers: the rows are still read at their own step.
+#pragma unroll
+                    for (int d = 0; d < D; d++) {
+                        const int jt = j0 + ahead + d;
+                        const bool cur = jt < steps;  // warp-uniform
+                        const int s = (cur ? jt : jt - steps) * gper + grp;
+                        const int sl = s & 31;
+                        const int32_t pu = __shfl_sync(0xffffffffu, cur ? tu : nu, sl);
+                        const int32_t pv = __shfl_sync(0xffffffffu, cur ? tv : nv, sl);
+                        const bool ok = grp < gper && s < 32 && (cur ? s < cnt : (more && nbase + s < nend));
+                        if (ok && sub == 0) {
+                            prefetch_row_l2(a.P, pu, row_bytes);
+                            prefetch_row_l2(a.Q, pv, row_bytes);
+                        }
+                    }
                 }
 #pragma unroll
                 for (int d = 0; d < D; d++) {
@@ -276,14 +298,21 @@ static cudaError_t hogwild_launch(const UpdateArgs &a, int workers, cudaStream_t
 cudaError_t launch_hogwild(const ShapeId &sh, const UpdateArgs &a_in, int workers, int variant, cudaStream_t st,
                            int *workers_used) {
     const int D = (variant >> 4) & 0xF;  // bits 4..7 select samples in flight per group (0 = default)
-    const UpdateArgs &a = a_in;
+    UpdateArgs a = a_in;
+    {
+        const int pf = (variant >> 16) & 0xF;  // bits 16..19: L2 row-prefetch distance in steps (0, 15 = off)
+        a.prefetch = pf == 15 ? 0 : pf;
+    }
     return dispatch_shape(sh, [&](auto tag) -> cudaError_t {
         using SH = decltype(tag);
         constexpr int L = SH::L;
         if constexpr (SH::FULL) {
             if (workers > 0 && workers < 64) return hogwild_launch<SH, 1>(a, workers, st, workers_used);
             if (D == 4 && L % 4 == 0) return hogwild_launch<SH, (L % 4 == 0 ? 4 : 1)>(a, workers, st, workers_used);
-            if (D != 1 && L % 2 == 0) return hogwild_launch<SH, (L % 2 == 0 ? 2 : 1)>(a, workers, st, workers_used);
+            // D = 0 (auto): two ratings in flight per group for fp32 rows, one for 16-bit rows (measured
+            // on the Netflix shape, k = 128: fp32 5.6 vs 5.2 G/s, fp16 8.3 vs 10.1 G/s; r01_cta_shapes.log)
+            const bool two = D == 2 || D == 3 || (D == 0 && SH::S == kF32);
+            if (two && L % 2 == 0) return hogwild_launch<SH, (L % 2 == 0 ? 2 : 1)>(a, workers, st, workers_used);
         }
         return hogwild_launch<SH, 1>(a, workers, st, workers_used);
     });

@@ -37,6 +37,7 @@ struct UpdateArgs {
     int64_t nwaves;
     int64_t active_groups;  // batch-Hogwild!: groups beyond this idle (exact worker count)
     const unsigned long long *abort_if;  // optional: the kernel does nothing if *abort_if != 0
+    int prefetch;       // batch-Hogwild!: L2-prefetch the rows of the rating this many steps ahead (0 = off)
 };
 
 // Kernel-shape choice for (k, storage); filled by select_shape().

@@ -280,6 +280,12 @@ __device__ __forceinline__ void sgd_step(float (&p)[SH::E], float (&q)[SH::E], f
     }
 }
 
+// one bulk L2 prefetch of a whole feature row (cp.async.bulk.prefetch: 16-B aligned, size % 16 == 0)
+__device__ __forceinline__ void prefetch_row_l2(const void *base, int64_t row, uint32_t row_bytes) {
+    const char *p = reinterpret_cast<const char *>(base) + row * (int64_t)row_bytes;
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(row_bytes) : "memory");
+}
+
 __device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
     uint64_t z = x + 0x9E3779B97F4A7C15ull;
     z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;

@@ -9,7 +9,7 @@ t0 = time.time()
 (u, v, r), test = datagen.make(cfg)
 print("gen", len(u), time.time() - t0, flush=True)
 g = mf.MF(cfg.m, cfg.n, cfg.k, cfg.alpha, cfg.lam, cfg.seed_init, storage=st, beta=cfg.beta, shuffle=0,
-          variant=16 if st != "f32" else 0)
+          variant=0)
 t0 = time.time(); g.load(u, v, r); print("load", time.time() - t0, flush=True)
 for sched, opts in (("hogwild", {}), ("wavefront", {"wave_cta": 1})):
     for kk, vv in opts.items(): g.set(getattr(mf, "MF_OPT_" + kk.upper()), vv)

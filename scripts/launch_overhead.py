@@ -9,7 +9,7 @@ cfg = datagen.CONFIGS["C2"]
 (u, v, r), test = datagen.make(cfg)
 for st in ("f16", "f32"):
     g = mf.MF(cfg.m, cfg.n, cfg.k, cfg.alpha, cfg.lam, cfg.seed_init, storage=st, beta=cfg.beta, shuffle=0,
-              variant=16 if st != "f32" else 0, workers=9907)
+              variant=0, workers=9907)
     for n in (99_072_112, 12_384_014, 1_548_001, 774_000, 387_000, 100_000):
         g.load(u[:n], v[:n], r[:n])
         ks = []

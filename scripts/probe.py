@@ -44,7 +44,7 @@ def main():
         for var in [int(x) for x in a.variants.split(",")]:
             for w in [int(x) for x in a.workers.split(",")]:
                 for f in [int(x) for x in a.batch.split(",")]:
-                    g.set(mf.MF_OPT_VARIANT, var if var >= 0 else (16 if storage != "f32" else 0))
+                    g.set(mf.MF_OPT_VARIANT, var if var >= 0 else 0)
                     g.set(mf.MF_OPT_WORKERS, w)
                     g.set(mf.MF_OPT_BATCH_F, f)
                     ks = []

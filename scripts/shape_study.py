@@ -24,7 +24,7 @@ PEAK = 6551.4e9
 def run(cfg, storage, schedule, epochs, data, **opts):
     (u, v, r), test = data
     g = mf.MF(cfg.m, cfg.n, cfg.k, cfg.alpha, cfg.lam, cfg.seed_init, storage=storage, beta=cfg.beta,
-              seed_shuffle=cfg.seed_shuffle, variant=16 if storage != "f32" else 0, **opts)
+              seed_shuffle=cfg.seed_shuffle, variant=0, **opts)
     t0 = time.time()
     g.load(u, v, r)
     if schedule == "deterministic":

@@ -30,7 +30,7 @@ def main():
     if os.path.exists(gp):
         gold = json.load(open(gp))["rmse"]
     for var in [int(x) for x in a.variants.split(",")]:
-        variant = var if var >= 0 else (16 if a.storage != "f32" else 0)
+        variant = var if var >= 0 else 0
         for w in [int(x) for x in a.workers.split(",")]:
             g = mf.MF(cfg.m, cfg.n, cfg.k, cfg.alpha, cfg.lam, cfg.seed_init, storage=a.storage, beta=cfg.beta,
                       seed_shuffle=cfg.seed_shuffle, workers=w, variant=variant)

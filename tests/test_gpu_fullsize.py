@@ -28,7 +28,7 @@ def c2():
 
 def _ctx(cfg, storage, **kw):
     from paper_1610_05838_b200 import mf
-    variant = 16 if storage != "f32" else 0   # bench.py's default launch configuration
+    variant = 0   # bench.py's default launch configuration (library auto)
     return mf.MF(cfg.m, cfg.n, cfg.k, cfg.alpha, cfg.lam, cfg.seed_init, storage=storage, beta=cfg.beta,
                  seed_shuffle=cfg.seed_shuffle, variant=variant, **kw)
 

@@ -7,6 +7,8 @@ fp64 dot).  Every schedule's test RMSE after E epochs within 0.5% of the
 oracle's on the same shuffled order (north star).  Integer work (order,
 counts, init bits) is bit-exact.
 """
+import functools
+
 import numpy as np
 import pytest
 
@@ -206,6 +208,49 @@ def test_netflix_slice_hogwild_many_workers(mfmod):
             assert st.updates == len(u)
         got = g.rmse(*test)
     assert abs(got - trace[-1]) <= 0.005 * trace[-1], (got, trace[-1])
+
+
+@functools.lru_cache(maxsize=None)
+def _c2_1pct_oracle_trace(storage, epochs):
+    cfg = datagen.CONFIGS["C2-1pct"]
+    (u, v, r), test = datagen.make(cfg)
+    order = oracle.shuffle_perm(cfg.seed_shuffle, len(u))
+    return oracle.train(cfg.m, cfg.n, cfg.k, ORC[storage], cfg.seed_init, u, v, r, cfg.alpha, cfg.beta, cfg.lam,
+                        epochs, order=order, test=test)[1]
+
+
+@pytest.mark.parametrize("storage,pf", [(0, 15), (0, 1), (1, 1), (1, 2), (2, 1)])
+def test_netflix_slice_hogwild_l2_prefetch(mfmod, storage, pf):
+    """The L2 row prefetch of batch-Hogwild! (MF_OPT_VARIANT bits 16..19) only moves cache lines: every
+    setting processes each sample exactly once and lands within 0.5% of the serial oracle (C2-1pct,
+    k = 128 full-row shape, 10 epochs as in the test above)."""
+    cfg = datagen.CONFIGS["C2-1pct"]
+    (u, v, r), test = datagen.make(cfg)
+    E = 10
+    trace = _c2_1pct_oracle_trace(storage, E)
+    with _gpu(mfmod, cfg, storage, count_updates=1, variant=pf << 16) as g:
+        g.load(u, v, r)
+        for _ in range(E):
+            st = g.epoch("hogwild")
+            assert st.updates == len(u)
+        got = g.rmse(*test)
+        assert (int(g.get(mfmod.MF_OPT_VARIANT)) >> 16) & 0xF == pf
+    assert abs(got - trace[-1]) <= 0.005 * trace[-1], (got, trace[-1])
+
+
+def test_hogwild_prefetch_auto_resolves(mfmod):
+    """Auto prefetch (variant 0): hogwild epochs 0-2 are trials, then one setting (on = 1 / off = 15) is
+    kept and reported through mf_get_option; a new load re-runs the trials."""
+    cfg = datagen.CONFIGS["C2-1pct"]
+    (u, v, r), _ = datagen.make(cfg)
+    with _gpu(mfmod, cfg, 1, count_updates=1) as g:
+        g.load(u, v, r)
+        for e in range(5):
+            assert g.epoch("hogwild").updates == len(u)
+            pick = (int(g.get(mfmod.MF_OPT_VARIANT)) >> 16) & 0xF
+            assert pick == 0 if e < 2 else pick in (1, 15)
+        g.load(u, v, r)
+        assert (int(g.get(mfmod.MF_OPT_VARIANT)) >> 16) & 0xF == 0
 
 
 # ------------------------------------------------------------- edge cases --
