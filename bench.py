@@ -108,6 +108,27 @@ def load_traffic(storage, cfgname):
         return None
 
 
+def load_pattern_ceiling(cfg, storage):
+    """Best updates/s of scripts/sgd_mem_ceiling.cu (the update's exact row traffic -- triple stream,
+    p_u and q_v read + written through L2 -- without its arithmetic) for this workload's shape, from the
+    committed sweep profiles/r01c_mem_ceiling.jsonl (or None).  It is the memory system's ceiling for
+    batch-Hogwild!'s access pattern: above the HBM roofline when Q is L2-resident."""
+    row_bytes = cfg.k * (4 if storage == "f32" else 2)
+    try:
+        best, match = None, False
+        with open(os.path.join(ROOT, "profiles", "r01c_mem_ceiling.jsonl")) as f:
+            for line in f:
+                d = json.loads(line)
+                if "m" in d:
+                    match = (d["m"], d["n"], d["N"], d["row_bytes"]) == (cfg.m, cfg.n, cfg.n_train, row_bytes)
+                elif match:
+                    u = max(d["updates_per_s_D1"], d["updates_per_s_D2"])
+                    best = u if best is None else max(best, u)
+        return best
+    except Exception:
+        return None
+
+
 # ----------------------------------------------------------------- reference
 def run_reference(a, cfg):
     """The oracle as it stands (serial C++, 1 core) on a bounded sample of the same workload."""
@@ -287,6 +308,11 @@ def main():
     if traffic:
         roof["frac_dram_measured_bytes"] = traffic / k_s / 1e9 / peak
         roof["dram_bytes_per_update_measured"] = traffic / N
+    ceil = load_pattern_ceiling(cfg, a.storage)
+    if ceil:
+        roof["pattern_ceiling_updates_per_s"] = ceil
+        roof["frac_of_pattern_ceiling"] = (N / k_s) / ceil
+        roof["pattern_ceiling_source"] = "scripts/sgd_mem_ceiling.cu sweep, profiles/r01c_mem_ceiling.jsonl"
 
     # the other storage and the wavefront schedule (CTA workers, Q in shared memory), same workload
     others = {}

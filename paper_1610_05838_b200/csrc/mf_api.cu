@@ -282,7 +282,7 @@ extern "C" int mf_set_option(mf_ctx *ctx, int key, double value) {
             return MF_OK;
         case MF_OPT_VARIANT:
             ctx->variant = (int)iv;
-            ctx->pf_trials = 0, ctx->pf_pick = 0;
+            ctx->pf_hogwild.reset(), ctx->pf_wave_cta.reset(), ctx->last_pf_pick = 0;
             return MF_OK;
         case MF_OPT_TRACE:
             ctx->trace = iv ? 1 : 0;
@@ -324,8 +324,8 @@ extern "C" int mf_get_option(const mf_ctx *ctx, int key, double *value) {
         case MF_OPT_PARTITIONS: *value = ctx->partitions; return MF_OK;
         case MF_OPT_SEED_SHUFFLE: *value = (double)ctx->seed_shuffle; return MF_OK;
         case MF_OPT_VARIANT:  // the variant in effect: an auto prefetch field reports the setting picked
-            *value = ((ctx->variant >> 16) & 0xF) == 0 && ctx->pf_pick ? ctx->variant | (ctx->pf_pick << 16)
-                                                                      : ctx->variant;
+            *value = ((ctx->variant >> 16) & 0xF) == 0 && ctx->last_pf_pick ? ctx->variant | (ctx->last_pf_pick << 16)
+                                                                           : ctx->variant;
             return MF_OK;
         case MF_OPT_TRACE: *value = ctx->trace; return MF_OK;
         case MF_OPT_SUBEPOCHS: *value = ctx->subepochs ? ctx->subepochs : ctx->part_S; return MF_OK;
@@ -366,7 +366,7 @@ extern "C" int mf_load_coo(mf_ctx *ctx, const int32_t *u, const int32_t *v, cons
     }
     RC(ctx->gather_q());
     ctx->drop_layouts();
-    ctx->pf_trials = 0, ctx->pf_pick = 0;  // a new workload re-runs the prefetch trials
+    ctx->pf_hogwild.reset(), ctx->pf_wave_cta.reset(), ctx->last_pf_pick = 0;  // a new workload re-runs the trials
     ctx->seg_valid = false;
     ctx->N = 0;
     const cudaMemcpyKind kind = is_device_ptr(u) ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
@@ -561,24 +561,22 @@ extern "C" int mf_epoch(mf_ctx *ctx, int schedule, mf_epoch_stats *stats) {
     UpdateArgs a = ctx->update_args(eta);
     int launches = 1, used = 0;
     CK(cudaEventRecord(ctx->events[1], st));
-    int pf_slot = -1;  // >= 0: this epoch is a prefetch trial (0 = off, 1 = on)
+    // auto L2 prefetch (mf_ctx::AutoPf): the setting tried when "on" -- batch-Hogwild!: the next
+    // ratings' rows one step ahead (Yahoo shape +11%, Zipf-skewed Netflix +15%, Netflix / Hugewiki
+    // shapes -6..-16%); CTA wavefront: a tile's P rows when it is claimed, per 128-B line for 16-bit
+    // rows, one bulk prefetch per row for fp32 (+5..+13% on three shapes, -4% on a fourth)
+    mf_ctx::AutoPf *tune = nullptr;
+    int pf_on = 0, pf_slot = -1;
+    ctx->variant_eff = ctx->variant;
+    if (((ctx->variant >> 16) & 0xF) == 0) {
+        if (schedule == MF_SCHED_HOGWILD) tune = &ctx->pf_hogwild, pf_on = 1;
+        else if (schedule == MF_SCHED_WAVEFRONT && ctx->wave_cta)
+            tune = &ctx->pf_wave_cta, pf_on = ctx->storage == kF32 ? 1 : 2;
+        if (tune) ctx->variant_eff |= tune->next(pf_on, &pf_slot) << 16;
+    }
     if (schedule == MF_SCHED_HOGWILD) {
         const int w = ctx->workers > 0 ? ctx->workers : ctx->auto_workers();
-        int var = ctx->variant;
-        if (((var >> 16) & 0xF) == 0) {
-            // Auto prefetch.  Whether an L2 prefetch of the next ratings' rows pays depends on where
-            // the rows live: it hides DRAM latency when Q misses L2 or hot rows queue (Yahoo shape
-            // +11%, Zipf-skewed Netflix shape +15%), and costs L2 request slots where the L2 is
-            // already the bottleneck (Netflix / Hugewiki shapes, -6..-16%).  It never
-            // changes what is computed, so the library times both and keeps the faster.
-            if (ctx->pf_pick) {
-                var |= ctx->pf_pick << 16;
-            } else {
-                pf_slot = ctx->pf_trials == 1 ? 1 : 0;
-                var |= (pf_slot ? 1 : 15) << 16;
-            }
-        }
-        CK(launch_hogwild(sh, a, w, var, st, &used));
+        CK(launch_hogwild(sh, a, w, ctx->variant_eff, st, &used));
     } else if (schedule == MF_SCHED_DETERMINISTIC) {
         a.u = ctx->wu;
         a.v = ctx->wv;
@@ -595,9 +593,9 @@ extern "C" int mf_epoch(mf_ctx *ctx, int schedule, mf_epoch_stats *stats) {
     }
     CK(cudaEventRecord(ctx->events[2], st));
     const int rc = ctx->finish_epoch(schedule, eta, launches, used, stats);
-    if (rc == MF_OK && pf_slot >= 0) {
-        ctx->pf_ms[pf_slot] = ctx->last_kernel_ms;
-        if (++ctx->pf_trials >= mf_ctx::kPfTrials) ctx->pf_pick = ctx->pf_ms[1] < 0.97f * ctx->pf_ms[0] ? 1 : 15;
+    if (rc == MF_OK && tune) {
+        tune->record(pf_slot, pf_on, ctx->last_kernel_ms);
+        ctx->last_pf_pick = tune->pick;
     }
     return rc;
 }

@@ -35,12 +35,31 @@ struct mf_ctx {
     int wave_cta = 0;   // wavefront worker = CTA with shared-memory Q group (MF_OPT_WAVE_CTA)
     int variant = 0;
     int trace = 0;
-    // batch-Hogwild! L2 row prefetch, auto mode (MF_OPT_VARIANT bits 16..19 = 0): hogwild epochs
-    // 0, 1, 2 run prefetch off (a warm-up, not timed), on, off; the faster of the last two is kept
-    static constexpr int kPfTrials = 3;
-    int pf_trials = 0;
-    int pf_pick = 0;        // 0 = undecided, else the bits-16..19 value in use (15 = off, 1 = on)
-    float pf_ms[2] = {0.f, 0.f};
+    // L2 prefetch, auto mode (MF_OPT_VARIANT bits 16..19 = 0).  Whether a prefetch pays depends on
+    // where the rows live (it hides DRAM latency, and costs L2 request slots where the L2 is the
+    // bottleneck), and it never changes what an epoch computes, so the library times it: epochs 0, 1, 2
+    // of a schedule run off (a warm-up, not counted), on, off; the faster of the last two is kept.
+    struct AutoPf {
+        int trials = 0, pick = 0;  // pick: 0 = undecided, else the bits-16..19 value in use (15 = off)
+        float ms[2] = {0.f, 0.f};
+        int next(int on, int *slot) const {
+            if (pick) {
+                *slot = -1;
+                return pick;
+            }
+            *slot = trials == 1 ? 1 : 0;
+            return *slot ? on : 15;
+        }
+        void record(int slot, int on, float kernel_ms) {
+            if (slot < 0) return;
+            ms[slot] = kernel_ms;
+            if (++trials >= 3) pick = ms[1] < 0.97f * ms[0] ? on : 15;
+        }
+        void reset() { trials = 0, pick = 0; }
+    };
+    AutoPf pf_hogwild, pf_wave_cta;
+    int last_pf_pick = 0;   // pick of the last auto-tuned schedule run (reported by mf_get_option)
+    int variant_eff = 0;    // the variant the current epoch's launches use (auto fields resolved)
     float last_kernel_ms = 0.f;
     cudaStream_t user_stream = nullptr;
 

@@ -116,6 +116,8 @@ __global__ void __launch_bounds__(kBlock) k_hogwild(UpdateArgs a) {
     const int ahead = a.prefetch * D;
     const uint32_t row_bytes = (uint32_t)k * SH::BYTES;
     const bool pf_on = ahead > 0 && SH::FULL && (row_bytes % 16u) == 0u && (32 % gper) == 0;
+    const bool pf_ponly = a.prefetch_kind & 1;  // P rows only (Q rows left to the cache)
+    const bool pf_lane = (a.prefetch_kind & 2) && row_bytes == 16u * SH::L * SH::V;  // per-lane prefetch.global.L2
 
     // Chunk claims run one chunk ahead and triple tiles one tile ahead, so neither the claim
     // atomic nor the 3 x 128-byte triple loads sit on the per-rating critical path.
@@ -202,9 +204,18 @@ __global__ void __launch_bounds__(kBlock) k_hogwild(UpdateArgs a) {
                         const int32_t pu = __shfl_sync(0xffffffffu, cur ? tu : nu, sl);
                         const int32_t pv = __shfl_sync(0xffffffffu, cur ? tv : nv, sl);
                         const bool ok = grp < gper && s < 32 && (cur ? s < cnt : (more && nbase + s < nend));
-                        if (ok && sub == 0) {
+                        if (pf_lane) {  // every lane touches its own 16-B slice: the LSU merges them per line
+                            if (ok) {
+                                const char *pp = reinterpret_cast<const char *>(a.P) + (int64_t)pu * row_bytes;
+                                asm volatile("prefetch.global.L2 [%0];" ::"l"(pp + sub * 16));
+                                if (!pf_ponly) {
+                                    const char *qp = reinterpret_cast<const char *>(a.Q) + (int64_t)pv * row_bytes;
+                                    asm volatile("prefetch.global.L2 [%0];" ::"l"(qp + sub * 16));
+                                }
+                            }
+                        } else if (ok && sub == 0) {
                             prefetch_row_l2(a.P, pu, row_bytes);
-                            prefetch_row_l2(a.Q, pv, row_bytes);
+                            if (!pf_ponly) prefetch_row_l2(a.Q, pv, row_bytes);
                         }
                     }
                 }
@@ -302,6 +313,7 @@ cudaError_t launch_hogwild(const ShapeId &sh, const UpdateArgs &a_in, int worker
     {
         const int pf = (variant >> 16) & 0xF;  // bits 16..19: L2 row-prefetch distance in steps (0, 15 = off)
         a.prefetch = pf == 15 ? 0 : pf;
+        a.prefetch_kind = (variant >> 20) & 0x3;  // bits 20..21: 1 = P rows only, 2 = per-lane prefetch
     }
     return dispatch_shape(sh, [&](auto tag) -> cudaError_t {
         using SH = decltype(tag);

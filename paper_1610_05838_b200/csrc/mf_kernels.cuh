@@ -38,6 +38,7 @@ struct UpdateArgs {
     int64_t active_groups;  // batch-Hogwild!: groups beyond this idle (exact worker count)
     const unsigned long long *abort_if;  // optional: the kernel does nothing if *abort_if != 0
     int prefetch;       // batch-Hogwild!: L2-prefetch the rows of the rating this many steps ahead (0 = off)
+    int prefetch_kind;  // bit 0: P rows only; bit 1: per-lane prefetch.global.L2 instead of one bulk prefetch
 };
 
 // Kernel-shape choice for (k, storage); filled by select_shape().

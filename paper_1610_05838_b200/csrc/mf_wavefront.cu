@@ -64,6 +64,7 @@ struct WfArgs {
     int64_t *trace;       // optional, 4 per block
     DevScratch *scratch;
     int s, c, k, latin, count_updates;
+    int pf;               // CTA workers: L2 prefetch of a tile's P rows when it is claimed (0 off, 1 bulk, 2 per line)
     float eta, lam;
     int64_t n_cols;       // column groups are balanced segments [floor(g n / c), floor((g+1) n / c))
 };
@@ -340,6 +341,18 @@ __global__ void __launch_bounds__(THREADS, THREADS >= 1024 ? 1 : kCtaThreads / T
             const float tr = ok ? __ldg(a.r + i) : 0.f;
             const int cnt = (int)(hi - base < 32 ? hi - base : 32);
             if (lane == 0) done += cnt;
+            if (a.pf && ok) {
+                // every lane asks L2 for its own sample's P row: the tile's later steps find their rows
+                // on chip instead of waiting for DRAM one rating at a time
+                const char *pp = reinterpret_cast<const char *>(a.P) + (int64_t)tu * row_bytes;
+                if (a.pf == 1) {
+                    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(pp), "r"((uint32_t)row_bytes)
+                                 : "memory");
+                } else {
+                    for (int64_t off = 0; off < row_bytes; off += 128)
+                        asm volatile("prefetch.global.L2 [%0];" ::"l"(pp + off));
+                }
+            }
             if (cnt == 32) cta_tile<SH, D, true>(a, qbase, k, grp, sub, cnt, tu, tv, tr, chk);
             else cta_tile<SH, D, false>(a, qbase, k, grp, sub, cnt, tu, tv, tr, chk);
         }
@@ -556,7 +569,14 @@ int mf_ctx::run_wavefront(const ShapeId &, const UpdateArgs &ua, int *launches, 
         // (r01, C2): k = 128 uses 8 lanes per rating (16 halves or 16 floats per lane) with one rating
         // in flight -- fewer butterfly levels and broadcast shuffles per rating than the 16/32-lane
         // shapes of batch-Hogwild! (f16 12.4 -> 13.6, f32 6.5 -> 7.7 G updates/s; profiles/r01_cta_shapes.log).
-        const int shape_sel = (variant >> 8) & 0xF, depth_sel = (variant >> 12) & 0xF;
+        const int shape_sel = (variant_eff >> 8) & 0xF, depth_sel = (variant_eff >> 12) & 0xF;
+        // bits 16..19: P-row L2 prefetch per claimed tile (1 = bulk, 2 = per 128-B line, 0 / 15 = off;
+        // bulk needs 16-B multiple rows; mf_epoch resolves the auto value 0 before this point)
+        {
+            const int pf = (variant_eff >> 16) & 0xF;
+            a.pf = pf == 1 || pf == 2 ? pf : 0;
+        }
+        if (a.pf == 1 && row_bytes % 16) a.pf = 2;
         const int def_shape = k == 128 ? (storage == kF32 ? 2 : 1) : 0;
         const ShapeId sh = select_shape(k, storage, shape_sel ? shape_sel - 1 : def_shape);
         const bool one_in_flight = depth_sel ? depth_sel == 1 : (k == 128 && !shape_sel);
@@ -583,7 +603,7 @@ int mf_ctx::run_wavefront(const ShapeId &, const UpdateArgs &ua, int *launches, 
     } else {
         const ShapeId sh = warp_shape(k, storage);
         const int blocks = (s * 32 + kBlock - 1) / kBlock;
-        const int depth = ((variant >> 4) & 0xF) == 4 ? 4 : 2;  // samples of a block in flight per warp
+        const int depth = ((variant_eff >> 4) & 0xF) == 4 ? 4 : 2;  // samples of a block in flight per warp
         CK(dispatch_warp_shape(sh, [&](auto tag) -> cudaError_t {
             using SH = decltype(tag);
             if constexpr (SH::FULL) {

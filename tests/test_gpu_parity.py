@@ -251,6 +251,14 @@ def test_hogwild_prefetch_auto_resolves(mfmod):
             assert pick == 0 if e < 2 else pick in (1, 15)
         g.load(u, v, r)
         assert (int(g.get(mfmod.MF_OPT_VARIANT)) >> 16) & 0xF == 0
+    # the CTA wavefront tunes its own prefetch (on = per-line for 16-bit rows, bulk for fp32)
+    for storage, on in ((1, 2), (0, 1)):
+        with _gpu(mfmod, cfg, storage, count_updates=1, wave_cta=1) as g:
+            g.load(u, v, r)
+            for e in range(4):
+                assert g.epoch("wavefront").updates == len(u)
+                pick = (int(g.get(mfmod.MF_OPT_VARIANT)) >> 16) & 0xF
+                assert pick == 0 if e < 2 else pick in (on, 15)
 
 
 # ------------------------------------------------------------- edge cases --
