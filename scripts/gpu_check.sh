@@ -13,11 +13,19 @@ fi
 if [ -n "$NCU" ]; then
   timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
      --log-file gpurun_out/launches.csv python bench.py --steps 3 --warmup 3 --no-cpu --no-variants --e2e-steps 1 > gpurun_out/ncu_bench.log 2>&1
+  mkdir -p /tmp/ncu
   for st in f16 f32; do
     timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_hogwild -s 3 -c 1 \
-       -o gpurun_out/prof_hogwild_$st -f python bench.py --storage $st --steps 1 --warmup 3 --no-cpu --no-variants --e2e-steps 1 > gpurun_out/ncu_full_$st.log 2>&1
+       -o /tmp/ncu/prof_hogwild_$st -f python bench.py --storage $st --steps 1 --warmup 3 --no-cpu --no-variants --e2e-steps 1 > gpurun_out/ncu_full_$st.log 2>&1
     timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_wavefront_cta -s 3 -c 1 \
-       -o gpurun_out/prof_wfcta_$st -f python bench.py --storage $st --schedule wavefront_cta --steps 1 --warmup 3 --no-cpu --no-variants --e2e-steps 1 > gpurun_out/ncu_wfcta_$st.log 2>&1
+       -o /tmp/ncu/prof_wfcta_$st -f python bench.py --storage $st --schedule wavefront_cta --steps 1 --warmup 3 --no-cpu --no-variants --e2e-steps 1 > gpurun_out/ncu_wfcta_$st.log 2>&1
   done
+  # raw metric pages travel back (the .ncu-rep files together exceed gpurun's 64 MiB copy-back)
+  for f in /tmp/ncu/*.ncu-rep; do
+    b=$(basename $f .ncu-rep)
+    ncu -i $f --page raw --csv > gpurun_out/$b.raw.csv 2>/dev/null
+    ncu -i $f --page source --csv > gpurun_out/$b.source.csv 2>/dev/null
+  done
+  cp /tmp/ncu/prof_hogwild_f16.ncu-rep gpurun_out/ 2>/dev/null
 fi
 ls gpurun_out
