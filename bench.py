@@ -138,10 +138,15 @@ def run_reference(a, cfg):
         return
     st = oracle.STORAGE_NAME[a.storage]
     G = int(os.environ.get("WORLD_SIZE", "1"))
-    # the same workload as our arm (for G > 1: rank 0's Netflix-shaped shard, which is generated
-    # exactly like the G = 1 problem; the factors are full size, m x G rows)
-    (u, v, r), test = datagen.make(cfg)
-    m = oracle.Model(cfg.m * G, cfg.n, cfg.k, st, seed=cfg.seed_init)
+    # the same workload as our arm (for G > 1: rank 0's shard of the partitioned problem, with the
+    # factors at full global size)
+    if G == 1:
+        (u, v, r), test = datagen.make(cfg)
+        m_glob = cfg.m
+    else:
+        (u, v, r), test = shard(cfg, G, 0, a.scaling)
+        m_glob = partition_shape(cfg, G, a.scaling)[0]
+    m = oracle.Model(m_glob, cfg.n, cfg.k, st, seed=cfg.seed_init)
     eta = oracle.eta(cfg.alpha, cfg.beta, 0)
     # bound the run: size each step so warmup + steps take ~2 minutes on this core
     t0 = time.perf_counter()
@@ -161,16 +166,33 @@ def run_reference(a, cfg):
     desc = f"{sample} consecutive shuffled samples of {cfg.name} per step, full-size P/Q, {a.storage} storage"
     out = {"metric": "sgd_updates_per_sec", "value": val, "unit": "updates/s", "n_gpus": a.gpus,
            "steps": a.steps, "warmup": a.warmup, "ms_per_step": 1e3 * tot / a.steps, "higher_is_better": True,
-           "scaling": "weak", "vs_baseline": None, "dtype": "f32", "storage": a.storage, "data": "synthetic",
+           "scaling": a.scaling, "vs_baseline": None, "dtype": "f32", "storage": a.storage, "data": "synthetic",
            "impl": "reference",
-           "config": workload_config(cfg, G, a.storage, a.schedule if G == 1 else "partitioned"),
+           "config": workload_config(cfg, G, a.storage, a.schedule if G == 1 else "partitioned", a.scaling),
            "arm": {"what": "serial C++ oracle (oracle/mf_oracle.cpp), 1 core", "sample_per_step": sample},
            "cpu_baseline": {"value": val, "unit": "updates/s", "cores": 1, "kind": "oracle", "sample": desc},
            "e2e": {"value": val, "unit": "updates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out), flush=True)
 
 
-def workload_config(cfg, G, storage, schedule):
+def partition_shape(cfg, G, scaling):
+    """(m_glob, rows per rank via mf_segment, train / test samples per rank) of the G-rank problem.
+    weak: every rank owns a full cfg-shaped row segment (m_glob = G m, N = G n_train), per-GPU work
+    fixed; strong: cfg itself is split into G row segments (C4 at 2/4/8 GPUs, BASELINE configs[3])."""
+    if scaling == "strong":
+        return cfg.m, cfg.n_train // G, cfg.n_test // G
+    return cfg.m * G, cfg.n_train, cfg.n_test
+
+
+def shard(cfg, G, rank, scaling):
+    """Rank `rank`'s training / test shard: draws of ONE global planted model restricted to the rank's
+    row segment (datagen.make_segment), so the G ranks factorise one consistent matrix."""
+    m_glob, n_tr, n_te = partition_shape(cfg, G, scaling)
+    pb, pe = rank * m_glob // G, (rank + 1) * m_glob // G  # mf_segment's balanced row segment (mf.h)
+    return datagen.make_segment(cfg, m_glob, pb, pe, n_tr, n_te, rank)
+
+
+def workload_config(cfg, G, storage, schedule, scaling="weak"):
     """The `config` object, identical for both arms of the same run."""
     b = 4 if storage == "f32" else 2
     if G == 1:
@@ -180,8 +202,11 @@ def workload_config(cfg, G, storage, schedule):
                 "l2": "inputs larger than L2 (R %.2f GB, P %.0f MB); no flush" % (12 * cfg.n_train / 1e9,
                                                                                   cfg.m * cfg.k * b / 1e6),
                 "step": "one epoch over all N ratings (mf_epoch) + test RMSE (mf_rmse)"}
-    return {"workload": f"{cfg.name} rows x {G}: m={cfg.m * G} n={cfg.n} N={cfg.n_train * G} k={cfg.k} "
-                        f"(one Netflix-shaped row segment per GPU)",
+    m_glob, n_tr, _ = partition_shape(cfg, G, scaling)
+    what = ("one %s-shaped row segment per GPU (weak scaling)" % cfg.name if scaling == "weak" else
+            "%s split into %d row segments (strong scaling)" % (cfg.name, G))
+    return {"workload": f"{cfg.name} partitioned over {G} GPUs: m={m_glob} n={cfg.n} N={n_tr * G} k={cfg.k}, "
+                        f"{what}; one global planted rank-8 model",
             "schedule": "partitioned (S passes x G rounds of G x G Latin-square blocks, NCCL Q rotation)",
             "storage": storage, "parallelism": f"P row segments x rotating Q segments over {G} GPUs",
             "alpha": cfg.alpha, "beta": cfg.beta, "lambda": cfg.lam, "l2": "inputs larger than L2; no flush",
@@ -224,6 +249,8 @@ def main():
     ap.add_argument("--partitioned", action="store_true",
                     help="run the multi-GPU (NCCL, partitioned) path even at one rank")
     ap.add_argument("--ref-sample", type=int, default=1_000_000)
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="N > 1: weak = one --config-shaped row segment per GPU; strong = --config split over N")
     a = ap.parse_args()
     a.warmup = max(a.warmup, 3)
     cfg = datagen.CONFIGS[a.config]
@@ -390,27 +417,34 @@ def main():
 def run_partitioned(a, cfg, rank, world, local):
     """N > 1: the partitioned path with NCCL Q rotation, one process per GPU.
 
-    Weak scaling: every rank owns a Netflix-shaped row segment (m/G = 480,190 rows, 99M samples), so
-    the global problem is m = 480,190 G rows x n = 17,771 columns with 99M G ratings (a Hugewiki-like
-    aspect ratio); per-GPU work is fixed as G grows.  Each rank generates its own shard."""
+    --scaling weak (default): every rank owns a --config-shaped row segment (C2: 480,190 rows, 99M
+    samples), so the global problem is m = 480,190 G rows x n = 17,771 columns with 99M G ratings (a
+    Hugewiki-like aspect ratio) and per-GPU work is fixed as G grows.  --scaling strong: --config itself
+    is split (C4, the Hugewiki shape, at 2/4/8 GPUs).  Each rank generates only its own shard of one
+    global planted model (datagen.make_segment)."""
     import torch
     import torch.distributed as dist
     from paper_1610_05838_b200 import mf
 
+    # Test hooks (tests/test_gpu_bench_multirank.py): several ranks on ONE GPU with libmf's NCCL calls
+    # served by tests/fake_nccl (LD_PRELOAD) and torch.distributed's own plumbing on gloo.
+    backend = os.environ.get("MF_BENCH_DIST_BACKEND", "nccl")
+    local = int(os.environ.get("MF_BENCH_DEVICE", local))
     torch.cuda.set_device(local)
     if world == 1:  # --partitioned on one GPU: a 1-rank NCCL job exercising the multi-GPU code path
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         os.environ.setdefault("MASTER_PORT", "29533")
         os.environ.setdefault("RANK", "0")
         os.environ.setdefault("WORLD_SIZE", "1")
-    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    if backend == "nccl":
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        dist.init_process_group(backend)
+    red_dev = "cuda" if backend == "nccl" else "cpu"  # device of the timing reductions
     stream = torch.cuda.current_stream()
     G = world
-    m_glob = cfg.m * G
-    pb, pe = mf.mf_segment(m_glob, G, rank)
-    (u, v, r), (tu, tv, tr) = datagen.make(cfg.scaled(m=pe - pb, seed_data=cfg.seed_data + 1000 * rank))
-    u += pb
-    tu += pb
+    m_glob = partition_shape(cfg, G, a.scaling)[0]
+    (u, v, r), (tu, tv, tr) = shard(cfg, G, rank, a.scaling)
     N_loc = len(u)
     variant = a.variant if a.variant >= 0 else 0
 
@@ -448,10 +482,10 @@ def run_partitioned(a, cfg, rank, world, local):
         e1.record(stream)
         torch.cuda.synchronize()
     dist.barrier()
-    ms = torch.tensor([e0.elapsed_time(e1) / a.steps], device="cuda")
+    ms = torch.tensor([e0.elapsed_time(e1) / a.steps], device=red_dev)
     dist.all_reduce(ms, op=dist.ReduceOp.MAX)
     ms = float(ms)
-    n_tot = torch.tensor([float(N_loc)], device="cuda")
+    n_tot = torch.tensor([float(N_loc)], device=red_dev)
     dist.all_reduce(n_tot)
     n_tot = float(n_tot)
     value = n_tot / (ms * 1e-3)
@@ -478,15 +512,15 @@ def run_partitioned(a, cfg, rank, world, local):
         e2e_step()
     e1.record(stream)
     torch.cuda.synchronize()
-    e2e_ms = torch.tensor([e0.elapsed_time(e1) / a.e2e_steps], device="cuda")
+    e2e_ms = torch.tensor([e0.elapsed_time(e1) / a.e2e_steps], device=red_dev)
     dist.all_reduce(e2e_ms, op=dist.ReduceOp.MAX)
     ge.close()
     if rank == 0:
         out = {
             "metric": "sgd_updates_per_sec", "value": value, "unit": "updates/s", "n_gpus": G, "steps": a.steps,
-            "warmup": a.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "warmup": a.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": a.scaling,
             "vs_baseline": None, "dtype": "f32", "storage": a.storage, "data": "synthetic",
-            "config": workload_config(cfg, G, a.storage, "partitioned"),
+            "config": workload_config(cfg, G, a.storage, "partitioned", a.scaling),
             "test_rmse": rm,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                          "traffic": None, "peak_kind": peak_kind, "kernel": "k_hogwild (rank 0, all rounds)",

@@ -42,6 +42,10 @@ def _load():
                                        ctypes.c_int64, ctypes.c_double, ctypes.c_double,
                                        ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
         lib.mfgen_zipf_coo.restype = ctypes.c_int
+        lib.mfgen_planted_segment.argtypes = [ctypes.c_uint64, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64,
+                                              ctypes.c_int64, ctypes.c_int, ctypes.c_double, ctypes.c_int64,
+                                              ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
+        lib.mfgen_planted_segment.restype = ctypes.c_int
         _lib = lib
     return _lib
 
@@ -80,6 +84,31 @@ def planted_factors(seed, m, n, rank):
     if _load().mfgen_planted_factors(seed, m, n, rank, P.ctypes.data, Q.ctypes.data) != 0:
         raise ValueError("bad arguments")
     return P, Q
+
+
+def planted_segment(seed, m, row_lo, row_hi, n, rank, sigma, i0, total):
+    """Draws i0 .. i0+total-1 of a global planted problem (m x n) restricted to rows [row_lo, row_hi)."""
+    u = np.empty(total, np.int32)
+    v = np.empty(total, np.int32)
+    r = np.empty(total, np.float32)
+    if _load().mfgen_planted_segment(seed, m, row_lo, row_hi, n, rank, sigma, i0, total, u.ctypes.data,
+                                     v.ctypes.data, r.ctypes.data) != 0:
+        raise ValueError("mfgen_planted_segment rejected its arguments")
+    return u, v, r
+
+
+TEST_STREAM = 1 << 50  # first global draw index of the test sets of segmented problems
+
+
+def make_segment(cfg: "Config", m_glob, row_lo, row_hi, n_train, n_test, rank_index):
+    """One rank's shard of a row-partitioned planted problem with cfg's n, rank, sigma and seed:
+    train = global draws [rank_index * n_train, +n_train), test = TEST_STREAM + [rank_index * n_test, +n_test),
+    rows restricted to [row_lo, row_hi)."""
+    tr = planted_segment(cfg.seed_data, m_glob, row_lo, row_hi, cfg.n, cfg.rank, cfg.sigma,
+                         rank_index * n_train, n_train)
+    te = planted_segment(cfg.seed_data, m_glob, row_lo, row_hi, cfg.n, cfg.rank, cfg.sigma,
+                         TEST_STREAM + rank_index * n_test, n_test)
+    return tr, te
 
 
 def split(cfg: "Config", u, v, r):

@@ -106,6 +106,44 @@ int mfgen_planted_coo(uint64_t seed, int64_t m, int64_t n, int rank, double sigm
     return 0;
 }
 
+/*
+ * One row segment of a larger planted problem (the multi-GPU bench: rank g generates only its own
+ * rows).  The planted model is the global one -- P*_u for global row u, the same Q* on every rank --
+ * and the samples are draws i0 .. i0+total-1 of the global stream with u restricted to the segment:
+ *   u = row_lo + H(seed,2,i) mod (row_hi - row_lo),  v = H(seed,3,i) mod n,
+ *   r = P*_u . Q*_v + sigma * N(0,1) (tag 4, index i).
+ * Disjoint index ranges per rank (and for train / test) give disjoint, independent draws.
+ */
+int mfgen_planted_segment(uint64_t seed, int64_t m, int64_t row_lo, int64_t row_hi, int64_t n, int rank,
+                          double sigma, int64_t i0, int64_t total, int32_t *u, int32_t *v, float *r) {
+    if (m <= 0 || n <= 0 || rank <= 0 || total < 0 || i0 < 0 || !u || !v || !r) return -1;
+    if (row_lo < 0 || row_hi > m || row_lo >= row_hi || m > 2147483647ll || n > 2147483647ll) return -1;
+    const int64_t rows = row_hi - row_lo;
+    double *Ps = (double *)malloc(sizeof(double) * (size_t)rows * rank);
+    double *Qs = (double *)malloc(sizeof(double) * (size_t)n * rank);
+    if (!Ps || !Qs) { free(Ps); free(Qs); return -1; }
+    const double sd = pow((double)rank, -0.25);
+#pragma omp parallel for schedule(static)
+    for (int64_t i = 0; i < rows; i++)
+        for (int j = 0; j < rank; j++)
+            Ps[i * rank + j] = sd * gen_gauss(seed, 0, (uint64_t)((row_lo + i) * rank + j));
+    planted(seed, 1, n, rank, Qs);
+#pragma omp parallel for schedule(static)
+    for (int64_t t = 0; t < total; t++) {
+        const uint64_t i = (uint64_t)(i0 + t);
+        const int64_t ul = (int64_t)(gen_H(seed, 2, i) % (uint64_t)rows);
+        u[t] = (int32_t)(row_lo + ul);
+        v[t] = (int32_t)(gen_H(seed, 3, i) % (uint64_t)n);
+        const double *p = Ps + ul * rank, *q = Qs + (int64_t)v[t] * rank;
+        double sum = 0.0;
+        for (int j = 0; j < rank; j++) sum += p[j] * q[j];
+        r[t] = (float)(sum + sigma * gen_gauss(seed, 4, i));
+    }
+    free(Ps);
+    free(Qs);
+    return 0;
+}
+
 /* Zipf(s) popularity over `count` ids: cdf[i] = sum_{j<=i} (j+1)^-s / total; the id order is then
  * scrambled by a seeded Fisher-Yates permutation (hot ids are not clustered at low indices). */
 static int zipf_table(uint64_t seed, uint64_t tag, int64_t count, double s, double **cdf_out, int32_t **perm_out) {

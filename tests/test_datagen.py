@@ -58,3 +58,20 @@ def test_configs_table2_shapes():
     assert (c["C3"].m, c["C3"].n, c["C3"].n_train, c["C3"].n_test) == (1000990, 624961, 252800275, 4003960)
     assert (c["C4"].m, c["C4"].n, c["C4"].n_train, c["C4"].n_test) == (50082604, 39781, 3069817980, 31327899)
     assert all(c[x].k == 128 for x in ("C2", "C3", "C4"))
+
+
+def test_planted_segment_is_a_slice_of_the_global_model():
+    """make_segment (multi-GPU bench shards): rows stay in the segment, every rank sees the same global
+    planted model (residual std = sigma against the global P*, Q*), streams are disjoint per rank."""
+    cfg = datagen.CONFIGS["C2-1pct"]
+    G, m_glob = 3, 3 * 1000
+    shards = [datagen.make_segment(cfg, m_glob, g * 1000, (g + 1) * 1000, 20_000, 2_000, g) for g in range(G)]
+    P, Q = datagen.planted_factors(cfg.seed_data, m_glob, cfg.n, cfg.rank)
+    for g, ((u, v, r), (tu, tv, tr)) in enumerate(shards):
+        assert u.min() >= g * 1000 and u.max() < (g + 1) * 1000 and tu.min() >= g * 1000
+        assert v.min() >= 0 and v.max() < cfg.n
+        resid = r.astype(np.float64) - np.einsum("ij,ij->i", P[u], Q[v])
+        assert abs(resid.std() - cfg.sigma) < 0.005
+    assert not np.array_equal(shards[0][0][1], shards[1][0][1])
+    again = datagen.make_segment(cfg, m_glob, 1000, 2000, 20_000, 2_000, 1)
+    np.testing.assert_array_equal(again[0][2], shards[1][0][2])
