@@ -65,6 +65,7 @@ struct WfArgs {
     DevScratch *scratch;
     int s, c, k, latin, count_updates;
     int pf;               // CTA workers: L2 prefetch of a tile's P rows when it is claimed (0 off, 1 bulk, 2 per line)
+    int tma;              // CTA workers: stage the Q group with bulk async copies (TMA engine) instead of a thread loop
     float eta, lam;
     int64_t n_cols;       // column groups are balanced segments [floor(g n / c), floor((g+1) n / c))
 };
@@ -227,6 +228,48 @@ __device__ __forceinline__ void cta_copy_out(unsigned char *dst, const unsigned 
     }
 }
 
+// Bulk async staging of the Q group (the TMA engine's non-tensor copies, cp.async.bulk): one thread
+// moves the whole group between global and shared memory in 64-KB pieces while the rest of the CTA
+// waits on an mbarrier (copy-in) or proceeds (copy-out, which only the lock release waits for).  The
+// thread-loop copy above keeps ~12 dependent 16-B loads per thread in sequence for a 200-KB group
+// (12-14 us per block on the Yahoo shape, scripts/wavefront_timeline.py).  Needs 16-B aligned
+// addresses and a 16-B multiple size.
+__device__ __forceinline__ void mbar_init(uint32_t bar) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_copy_in(uint32_t dst, const void *src, uint32_t nbytes, uint32_t bar) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(nbytes) : "memory");
+    for (uint32_t off = 0; off < nbytes; off += 65536u) {
+        const uint32_t len = nbytes - off < 65536u ? nbytes - off : 65536u;
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                         dst + off),
+                     "l"(reinterpret_cast<const char *>(src) + off), "r"(len), "r"(bar)
+                     : "memory");
+    }
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+    uint32_t done = 0;
+    while (!done)
+        asm volatile(
+            "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+            : "=r"(done)
+            : "r"(bar), "r"(parity)
+            : "memory");
+}
+__device__ __forceinline__ void bulk_copy_out(void *dst, uint32_t src, uint32_t nbytes) {
+    for (uint32_t off = 0; off < nbytes; off += 65536u) {
+        const uint32_t len = nbytes - off < 65536u ? nbytes - off : 65536u;
+        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(reinterpret_cast<char *>(dst) +
+                                                                                          off),
+                     "r"(src + off), "r"(len)
+                     : "memory");
+    }
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // the writes are performed
+    asm volatile("fence.proxy.async.global;" ::: "memory");    // ... and ordered before the release
+}
+
 // One 32-sample tile of a block (lane i of the warp holds sample base+i: tu, tv relative to the
 // group's first column, tr).  G groups of L lanes, D ratings in flight per group.  FULLTILE: cnt == 32,
 // no sample predicates (every tile but a block's last).  chk accumulates err * 0, which is NaN iff
@@ -294,8 +337,9 @@ __device__ __forceinline__ void cta_tile(const WfArgs &a, uint32_t qbase, int k,
 
 template <class SH, int D, int THREADS>
 __global__ void __launch_bounds__(THREADS, THREADS >= 1024 ? 1 : kCtaThreads / THREADS) k_wavefront_cta(WfArgs a) {
-    extern __shared__ __align__(16) unsigned char qs[];
+    extern __shared__ __align__(128) unsigned char qs[];
     __shared__ int s_col, s_next;
+    __shared__ __align__(8) uint64_t s_bar;  // Q-group copy-in completion (a.tma)
     constexpr int L = SH::L;
     const int lane = threadIdx.x & 31, grp = lane / L, sub = lane % L;
     const int w = blockIdx.x;
@@ -306,6 +350,8 @@ __global__ void __launch_bounds__(THREADS, THREADS >= 1024 ? 1 : kCtaThreads / T
     const uint32_t qbase = (uint32_t)__cvta_generic_to_shared(qs);
     float chk = 0.f;
     unsigned long long done = 0;
+    if (a.tma && threadIdx.x == 0) mbar_init((uint32_t)__cvta_generic_to_shared(&s_bar));
+    __syncthreads();
     for (int j = 0; j < c; j++) {
         if (threadIdx.x == 0) {
             const int col = a.latin ? a.seq[(a.seq[c + w] + j) % c] : a.seq[(int64_t)w * c + j];
@@ -319,8 +365,17 @@ __global__ void __launch_bounds__(THREADS, THREADS >= 1024 ? 1 : kCtaThreads / T
         const int64_t q0 = seg_begin(a.n_cols, c, col);
         const int64_t nrows = seg_begin(a.n_cols, c, col + 1) - q0;
         const unsigned char *qg = reinterpret_cast<const unsigned char *>(a.Q) + q0 * row_bytes;
-        cta_copy_in(qs, qg, nrows * row_bytes);
-        __syncthreads();
+        if (a.tma) {
+            if (threadIdx.x == 0) {
+                asm volatile("fence.proxy.async.global;" ::: "memory");  // acquired state -> async proxy
+                bulk_copy_in(qbase, qg, (uint32_t)(nrows * row_bytes), (uint32_t)__cvta_generic_to_shared(&s_bar));
+            }
+            // every group has >= 1 row (c <= n), so block j completes the barrier's phase j
+            mbar_wait((uint32_t)__cvta_generic_to_shared(&s_bar), (uint32_t)j & 1u);
+        } else {
+            cta_copy_in(qs, qg, nrows * row_bytes);
+            __syncthreads();
+        }
         const int64_t t0 = a.trace ? globaltimer() : 0;
         const int64_t blk = (int64_t)w * c + col;
         const int64_t lo = a.off[blk], hi = a.off[blk + 1];
@@ -356,8 +411,16 @@ __global__ void __launch_bounds__(THREADS, THREADS >= 1024 ? 1 : kCtaThreads / T
             if (cnt == 32) cta_tile<SH, D, true>(a, qbase, k, grp, sub, cnt, tu, tv, tr, chk);
             else cta_tile<SH, D, false>(a, qbase, k, grp, sub, cnt, tu, tv, tr, chk);
         }
-        __syncthreads();
-        cta_copy_out(reinterpret_cast<unsigned char *>(a.Q) + q0 * row_bytes, qs, nrows * row_bytes);
+        if (a.tma) {
+            // this thread's st.shared to the group must be visible to the async proxy that reads it
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            __syncthreads();
+            if (threadIdx.x == 0)
+                bulk_copy_out(reinterpret_cast<unsigned char *>(a.Q) + q0 * row_bytes, qbase, (uint32_t)(nrows * row_bytes));
+        } else {
+            __syncthreads();
+            cta_copy_out(reinterpret_cast<unsigned char *>(a.Q) + q0 * row_bytes, qs, nrows * row_bytes);
+        }
         if (a.trace && threadIdx.x == 0) {
             int64_t *tr = a.trace + 4 * blk;
             tr[0] = w;
@@ -577,6 +640,8 @@ int mf_ctx::run_wavefront(const ShapeId &, const UpdateArgs &ua, int *launches, 
             a.pf = pf == 1 || pf == 2 ? pf : 0;
         }
         if (a.pf == 1 && row_bytes % 16) a.pf = 2;
+        // bits 20..21: Q-group staging, 0 = bulk async copies when rows are 16-B multiples, 2 = thread loop
+        a.tma = ((variant_eff >> 20) & 0x3) != 2 && row_bytes % 16 == 0 && ((uintptr_t)Q & 15) == 0;
         const int def_shape = k == 128 ? (storage == kF32 ? 2 : 1) : 0;
         const ShapeId sh = select_shape(k, storage, shape_sel ? shape_sel - 1 : def_shape);
         const bool one_in_flight = depth_sel ? depth_sel == 1 : (k == 128 && !shape_sel);

@@ -10,7 +10,7 @@
 // allows for that shape.  Swept over groups in flight per SM and rows in flight per group.
 //
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o /tmp/sgd_mem_ceiling scripts/sgd_mem_ceiling.cu
-//   /tmp/sgd_mem_ceiling m n N row_bytes
+//   /tmp/sgd_mem_ceiling m n N row_bytes [p_only]
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -31,7 +31,9 @@ __global__ void fill_idx(int32_t *u, int32_t *v, float *r, int64_t N, uint32_t m
 }
 
 // L lanes per row (row = L * 16 * V bytes), D updates in flight per group; warps walk 32-sample tiles
-template <int L, int V, int D>
+// QG: also read + write q_v in global memory (batch-Hogwild!); false: P rows only (the CTA wavefront,
+// whose Q group lives in shared memory)
+template <int L, int V, int D, bool QG = true>
 __global__ void __launch_bounds__(256) rmw(const int32_t *__restrict__ u, const int32_t *__restrict__ v,
                                            const float *__restrict__ r, int64_t N, uint4 *P, uint4 *Q,
                                            int64_t active_warps, unsigned long long *ctr) {
@@ -67,7 +69,7 @@ __global__ void __launch_bounds__(256) rmw(const int32_t *__restrict__ u, const 
                     for (int j = 0; j < V; j++) {
                         if (val[d]) {
                             pw[d][j] = __ldcg(P + (int64_t)su[d] * L * V + j * L + sub);
-                            qw[d][j] = __ldcg(Q + (int64_t)sv[d] * L * V + j * L + sub);
+                            if (QG) qw[d][j] = __ldcg(Q + (int64_t)sv[d] * L * V + j * L + sub);
                         }
                     }
 #pragma unroll
@@ -75,11 +77,11 @@ __global__ void __launch_bounds__(256) rmw(const int32_t *__restrict__ u, const 
 #pragma unroll
                     for (int j = 0; j < V; j++) {
                         if (val[d]) {
-                            uint4 a = pw[d][j], b = qw[d][j];
+                            uint4 a = pw[d][j], b = QG ? qw[d][j] : pw[d][j];
                             a.x += 1u; a.y += 1u; a.z += 1u; a.w += 1u;
                             b.x += 1u; b.y += 1u; b.z += 1u; b.w += 1u;
                             __stcg(P + (int64_t)su[d] * L * V + j * L + sub, a);
-                            __stcg(Q + (int64_t)sv[d] * L * V + j * L + sub, b);
+                            if (QG) __stcg(Q + (int64_t)sv[d] * L * V + j * L + sub, b);
                         }
                     }
             }
@@ -88,7 +90,7 @@ __global__ void __launch_bounds__(256) rmw(const int32_t *__restrict__ u, const 
     if (acc == -1.f) ctr[1] = 1;  // keep the r stream alive
 }
 
-template <int L, int V, int D>
+template <int L, int V, int D, bool QG>
 static double run(const int32_t *u, const int32_t *v, const float *r, int64_t N, uint4 *P, uint4 *Q,
                   int warps_per_sm, int sms, unsigned long long *ctr) {
     const int64_t warps = (int64_t)warps_per_sm * sms;
@@ -100,7 +102,7 @@ static double run(const int32_t *u, const int32_t *v, const float *r, int64_t N,
     for (int rep = 0; rep < 3; rep++) {
         cudaMemset(ctr, 0, 16);
         cudaEventRecord(a);
-        rmw<L, V, D><<<blocks, 256>>>(u, v, r, N, P, Q, warps, ctr);
+        rmw<L, V, D, QG><<<blocks, 256>>>(u, v, r, N, P, Q, warps, ctr);
         cudaEventRecord(b);
         cudaEventSynchronize(b);
         float ms = 0;
@@ -115,18 +117,19 @@ static double run(const int32_t *u, const int32_t *v, const float *r, int64_t N,
     return N / (best * 1e-3);
 }
 
-template <int L, int V>
+template <int L, int V, bool QG = true>
 static void sweep(const char *label, const int32_t *u, const int32_t *v, const float *r, int64_t N, uint4 *P,
                   uint4 *Q, int sms, unsigned long long *ctr, int row_bytes) {
+    const double bytes = QG ? 12 + 4.0 * row_bytes : 12 + 2.0 * row_bytes;  // global bytes per update
     for (int wps : {16, 24, 32, 48, 64}) {
-        const double u1 = run<L, V, 1>(u, v, r, N, P, Q, wps, sms, ctr);
-        const double u2 = run<L, V, 2>(u, v, r, N, P, Q, wps, sms, ctr);
+        const double u1 = run<L, V, 1, QG>(u, v, r, N, P, Q, wps, sms, ctr);
+        const double u2 = run<L, V, 2, QG>(u, v, r, N, P, Q, wps, sms, ctr);
         const int G = 32 / L;
-        printf("{\"shape\": \"%s\", \"row_bytes\": %d, \"warps_per_sm\": %d, \"in_flight_D1\": %d, "
-               "\"updates_per_s_D1\": %.4g, \"in_flight_D2\": %d, \"updates_per_s_D2\": %.4g, "
+        printf("{\"shape\": \"%s\", \"rows\": \"%s\", \"row_bytes\": %d, \"warps_per_sm\": %d, "
+               "\"in_flight_D1\": %d, \"updates_per_s_D1\": %.4g, \"in_flight_D2\": %d, \"updates_per_s_D2\": %.4g, "
                "\"l2_GBps_D1\": %.1f, \"l2_GBps_D2\": %.1f}\n",
-               label, row_bytes, wps, wps * sms * G, u1, 2 * wps * sms * G, u2, u1 * (12 + 4.0 * row_bytes) / 1e9,
-               u2 * (12 + 4.0 * row_bytes) / 1e9);
+               label, QG ? "p+q" : "p", row_bytes, wps, wps * sms * G, u1, 2 * wps * sms * G, u2, u1 * bytes / 1e9,
+               u2 * bytes / 1e9);
         fflush(stdout);
     }
 }
@@ -154,12 +157,17 @@ int main(int argc, char **argv) {
     cudaDeviceSynchronize();
     printf("{\"m\": %lld, \"n\": %lld, \"N\": %lld, \"row_bytes\": %d, \"sms\": %d}\n", (long long)m, (long long)n,
            (long long)N, row_bytes, sms);
-    if (row_bytes == 256) {
+    const bool p_only = argc > 5 && atoi(argv[5]) != 0;
+    if (row_bytes == 256 && !p_only) {
         sweep<16, 1>("L16xV1", u, v, r, N, P, Q, sms, ctr, row_bytes);
         sweep<8, 2>("L8xV2", u, v, r, N, P, Q, sms, ctr, row_bytes);
-    } else if (row_bytes == 512) {
+    } else if (row_bytes == 512 && !p_only) {
         sweep<32, 1>("L32xV1", u, v, r, N, P, Q, sms, ctr, row_bytes);
         sweep<16, 2>("L16xV2", u, v, r, N, P, Q, sms, ctr, row_bytes);
+    } else if (row_bytes == 256) {
+        sweep<8, 2, false>("L8xV2", u, v, r, N, P, Q, sms, ctr, row_bytes);
+    } else if (row_bytes == 512) {
+        sweep<8, 4, false>("L8xV4", u, v, r, N, P, Q, sms, ctr, row_bytes);
     }
     return 0;
 }
