@@ -30,11 +30,13 @@ static constexpr int kWarpsPerBlock = kBlock / 32;
 // exactly; generic shapes (full = 0) mask lanes beyond k.
 #define MF_FAST_SHAPES(X)                                                                                \
     X(kF32, 8, 1, 16, 1) X(kF32, 16, 1, 16, 1) X(kF32, 32, 1, 16, 1) X(kF32, 32, 2, 16, 1)               \
-    X(kF32, 16, 2, 16, 1) X(kF32, 8, 4, 16, 1)                                                           \
+    X(kF32, 16, 2, 16, 1) X(kF32, 8, 4, 16, 1) X(kF32, 16, 1, 8, 1) X(kF32, 32, 1, 8, 1) X(kF32, 32, 1, 4, 1) \
     X(kF16, 4, 1, 16, 1) X(kF16, 8, 1, 16, 1) X(kF16, 16, 1, 16, 1) X(kF16, 32, 1, 16, 1)                \
-    X(kF16, 8, 2, 16, 1) X(kF16, 32, 1, 8, 1) X(kF16, 4, 4, 16, 1)                                       \
+    X(kF16, 8, 2, 16, 1) X(kF16, 32, 1, 8, 1) X(kF16, 4, 4, 16, 1) X(kF16, 8, 1, 8, 1) X(kF16, 16, 1, 4, 1) \
+    X(kF16, 16, 1, 8, 1) X(kF16, 32, 1, 4, 1)                                                            \
     X(kBF16, 4, 1, 16, 1) X(kBF16, 8, 1, 16, 1) X(kBF16, 16, 1, 16, 1) X(kBF16, 32, 1, 16, 1)            \
-    X(kBF16, 8, 2, 16, 1) X(kBF16, 32, 1, 8, 1) X(kBF16, 4, 4, 16, 1)
+    X(kBF16, 8, 2, 16, 1) X(kBF16, 32, 1, 8, 1) X(kBF16, 4, 4, 16, 1) X(kBF16, 8, 1, 8, 1)              \
+    X(kBF16, 16, 1, 4, 1) X(kBF16, 16, 1, 8, 1) X(kBF16, 32, 1, 4, 1)
 #define MF_GENERIC_SHAPES(X)                                                                             \
     X(kF32, 32, 1, 4, 0) X(kF32, 32, 4, 4, 0) X(kF32, 32, 16, 4, 0) X(kF32, 32, 32, 4, 0)                \
     X(kF16, 32, 1, 4, 0) X(kF16, 32, 4, 4, 0) X(kF16, 32, 16, 4, 0)                                      \
@@ -61,8 +63,19 @@ ShapeId select_shape(int k, int storage, int variant) {
             if (variant == 2) return {storage, 8, 4, 16, 1};
             return {storage, 32, 1, 16, 1};
         }
-        if (k == 32) return {storage, 8, 1, 16, 1};
-        if (k == 64) return {storage, 16, 1, 16, 1};
+        // k = 32 / 64: at the A-10 worker count a group of 16 lanes (8-byte vectors at k = 32) keeps
+        // twice the warps of an 8-lane group per rating in flight, which hides the update's arithmetic
+        // latency (Netflix shape, one rating in flight per group: k = 32 11.6 -> 14.9, k = 64 9.1 ->
+        // 10.5 G updates/s; profiles/r01c_smallk_probe.log)
+        if (k == 32) {
+            if (variant == 1) return {storage, 8, 1, 16, 1};
+            if (variant == 2) return {storage, 32, 1, 4, 1};
+            return {storage, 16, 1, 8, 1};
+        }
+        if (k == 64) {
+            if (variant == 1) return {storage, 32, 1, 8, 1};
+            return {storage, 16, 1, 16, 1};
+        }
         if (k == 256) return {storage, 32, 2, 16, 1};
     } else {
         if (k == 128) {
@@ -71,8 +84,18 @@ ShapeId select_shape(int k, int storage, int variant) {
             if (variant == 3) return {storage, 4, 4, 16, 1};
             return {storage, 16, 1, 16, 1};
         }
-        if (k == 32) return {storage, 4, 1, 16, 1};
-        if (k == 64) return {storage, 8, 1, 16, 1};
+        // 16-bit rows, k = 32 / 64: 16 lanes per rating with 4- / 8-byte vectors (k = 32 11.9 -> 13.9,
+        // k = 64 13.3 -> 13.9 G updates/s over the 4- / 8-lane 16-byte shapes)
+        if (k == 32) {
+            if (variant == 1) return {storage, 8, 1, 8, 1};
+            if (variant == 2) return {storage, 4, 1, 16, 1};
+            return {storage, 16, 1, 4, 1};
+        }
+        if (k == 64) {
+            if (variant == 1) return {storage, 8, 1, 16, 1};
+            if (variant == 2) return {storage, 32, 1, 4, 1};
+            return {storage, 16, 1, 8, 1};
+        }
         if (k == 256) return {storage, 32, 1, 16, 1};
     }
     return select_generic_shape(k, storage);
@@ -321,9 +344,10 @@ cudaError_t launch_hogwild(const ShapeId &sh, const UpdateArgs &a_in, int worker
         if constexpr (SH::FULL) {
             if (workers > 0 && workers < 64) return hogwild_launch<SH, 1>(a, workers, st, workers_used);
             if (D == 4 && L % 4 == 0) return hogwild_launch<SH, (L % 4 == 0 ? 4 : 1)>(a, workers, st, workers_used);
-            // D = 0 (auto): two ratings in flight per group for fp32 rows, one for 16-bit rows (measured
-            // on the Netflix shape, k = 128: fp32 5.6 vs 5.2 G/s, fp16 8.3 vs 10.1 G/s; r01_cta_shapes.log)
-            const bool two = D == 2 || D == 3 || (D == 0 && SH::S == kF32);
+            // D = 0 (auto): two ratings in flight per group for fp32 rows of k >= 128, one otherwise
+            // (Netflix shape: k = 128 fp32 5.6 vs 5.2 G/s, fp16 8.3 vs 10.1; k = 32 / 64 fp32 one in
+            // flight +28% / +15%; r01_cta_shapes.log, r01c_smallk_probe.log)
+            const bool two = D == 2 || D == 3 || (D == 0 && SH::S == kF32 && SH::KMAX >= 128);
             if (two && L % 2 == 0) return hogwild_launch<SH, (L % 2 == 0 ? 2 : 1)>(a, workers, st, workers_used);
         }
         return hogwild_launch<SH, 1>(a, workers, st, workers_used);

@@ -119,7 +119,7 @@ def test_c1_deterministic_bit_reproducible_and_multi_epoch(mfmod, c1):
     assert outs[0][2] == pytest.approx(trace[-1], rel=1e-5)
 
 
-@pytest.mark.parametrize("k", [2, 7, 33, 64, 100, 128, 256])
+@pytest.mark.parametrize("k", [2, 7, 32, 33, 64, 100, 128, 256])
 @pytest.mark.parametrize("storage", [0, 1])
 def test_deterministic_k_sweep_ragged(mfmod, k, storage):
     """Generic (masked) and fast (vectorised) shapes; N not a multiple of 32 or 256."""
@@ -235,6 +235,24 @@ def test_netflix_slice_hogwild_l2_prefetch(mfmod, storage, pf):
             assert st.updates == len(u)
         got = g.rmse(*test)
         assert (int(g.get(mfmod.MF_OPT_VARIANT)) >> 16) & 0xF == pf
+    assert abs(got - trace[-1]) <= 0.005 * trace[-1], (got, trace[-1])
+
+
+@pytest.mark.parametrize("k,storage", [(32, 0), (32, 1), (64, 0), (64, 1)])
+def test_netflix_slice_hogwild_small_k(mfmod, k, storage):
+    """The k = 32 / 64 batch-Hogwild! shapes (16 lanes per rating, 4- / 8-byte vectors): exactly once per
+    epoch, test RMSE within 0.5% of the storage-matched serial oracle after 10 epochs (C2-1pct)."""
+    cfg = datagen.CONFIGS["C2-1pct"].scaled(k=k)
+    (u, v, r), test = datagen.make(cfg)
+    order = oracle.shuffle_perm(cfg.seed_shuffle, len(u))
+    E = 10
+    _, trace = oracle.train(cfg.m, cfg.n, cfg.k, ORC[storage], cfg.seed_init, u, v, r, cfg.alpha, cfg.beta,
+                            cfg.lam, E, order=order, test=test)
+    with _gpu(mfmod, cfg, storage, count_updates=1) as g:
+        g.load(u, v, r)
+        for _ in range(E):
+            assert g.epoch("hogwild").updates == len(u)
+        got = g.rmse(*test)
     assert abs(got - trace[-1]) <= 0.005 * trace[-1], (got, trace[-1])
 
 
