@@ -584,7 +584,10 @@ extern "C" int mf_epoch(mf_ctx *ctx, int schedule, mf_epoch_stats *stats) {
         a.wave_off = ctx->wave_off;
         a.nwaves = ctx->nwaves;
         int l = 0;
-        CK(launch_waves(sh, a, st, &l));
+        // MF_OPT_VARIANT bits 24..25: 0 = 1024-thread CTAs, 2 samples per group and step; 1 = one
+        // sample; 2 = 256-thread CTAs and the fenced barrier (r01 form)
+        const int wsel = (ctx->variant >> 24) & 0x3;
+        CK(launch_waves(sh, a, st, &l, wsel == 2 ? 0 : wsel == 1 ? 1 : 2));
         used = 0;
     } else {  // wavefront
         int l = 0;

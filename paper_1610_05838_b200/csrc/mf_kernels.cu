@@ -376,52 +376,108 @@ __device__ __forceinline__ void grid_barrier(DevScratch *s, unsigned nblocks) {
     __syncthreads();
 }
 
-template <class SH>
-__global__ void __launch_bounds__(kBlock) k_waves(UpdateArgs a) {
+// Leaner barrier for one CTA per SM: arrival by a release atomic, wait by acquire loads (no separate
+// membar on either side); the CTA barriers around it order the other threads' stores and loads.
+__device__ __forceinline__ void grid_barrier_ra(DevScratch *s, unsigned nblocks) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned g;
+        asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(g) : "l"(&s->bar_gen) : "memory");
+        unsigned prev;
+        asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], 1;" : "=r"(prev) : "l"(&s->bar_count) : "memory");
+        if (prev == nblocks - 1) {
+            asm volatile("st.relaxed.gpu.global.u32 [%0], 0;" ::"l"(&s->bar_count) : "memory");
+            asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(&s->bar_gen), "r"(g + 1) : "memory");
+        } else {
+            unsigned cur;
+            do {
+                asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(cur) : "l"(&s->bar_gen) : "memory");
+            } while (cur == g);
+        }
+    }
+    __syncthreads();
+}
+
+// D samples of the same wave per group and step (a wave's samples are pairwise independent, so any
+// number may be in flight -- unlike batch-Hogwild! there is no staleness to bound); the per-rating
+// arithmetic (lane_dot, then the butterfly) is the same for every D, so results do not depend on it.
+template <class SH, int BLOCK = kBlock, int D = 1>
+__global__ void __launch_bounds__(BLOCK) k_waves(UpdateArgs a) {
     constexpr int L = SH::L;
     const int lane = threadIdx.x & 31, sub = lane % L;
     const int k = SH::FULL ? SH::KMAX : a.k;
-    const int64_t groups = (int64_t)gridDim.x * kBlock / L;
-    const int64_t gid = ((int64_t)blockIdx.x * kBlock + threadIdx.x) / L;
+    const int64_t groups = (int64_t)gridDim.x * BLOCK / L;
+    const int64_t gid = ((int64_t)blockIdx.x * BLOCK + threadIdx.x) / L;
     int bad = 0;
     unsigned long long done = 0;
     for (int64_t w = 0; w < a.nwaves; w++) {
         const int64_t lo = a.wave_off[w], hi = a.wave_off[w + 1];
         // warp-uniform trip count so the full-warp shuffles stay converged
         const int64_t warp_first = lo + (gid - (lane / L));
-        for (int64_t s0 = warp_first; s0 < hi; s0 += groups) {
-            const int64_t s = s0 + lane / L;
-            const bool val = s < hi;
-            const int32_t su = val ? __ldg(a.u + s) : 0;
-            const int32_t sv = val ? __ldg(a.v + s) : 0;
-            const float sr = val ? __ldg(a.r + s) : 0.f;
-            RowRaw<SH> pr, qr;
-            load_row<SH>(a.P, su, k, sub, val, pr);
-            load_row<SH>(a.Q, sv, k, sub, val, qr);
-            float p[SH::E], q[SH::E];
-            widen_row<SH>(pr, p);
-            widen_row<SH>(qr, q);
-            const float err = sr - group_dot<SH>(p, q);
-            if (val && !isfinite(err)) bad = 1;
-            sgd_step<SH>(p, q, err, a.eta, a.lam);
-            narrow_row<SH>(p, pr);
-            narrow_row<SH>(q, qr);
-            store_row<SH>(a.P, su, k, sub, val, pr);
-            store_row<SH>(a.Q, sv, k, sub, val, qr);
-            if (val && sub == 0) done++;
+        for (int64_t s0 = warp_first; s0 < hi; s0 += D * groups) {
+            int32_t su[D], sv[D];
+            float sr[D], dot[D];
+            bool val[D];
+            RowRaw<SH> pr[D], qr[D];
+#pragma unroll
+            for (int d = 0; d < D; d++) {
+                const int64_t s = s0 + d * groups + lane / L;
+                val[d] = s < hi;
+                su[d] = val[d] ? __ldg(a.u + s) : 0;
+                sv[d] = val[d] ? __ldg(a.v + s) : 0;
+                sr[d] = val[d] ? __ldg(a.r + s) : 0.f;
+                load_row<SH>(a.P, su[d], k, sub, val[d], pr[d]);
+                load_row<SH>(a.Q, sv[d], k, sub, val[d], qr[d]);
+            }
+#pragma unroll
+            for (int d = 0; d < D; d++) {
+                float p[SH::E], q[SH::E];
+                widen_row<SH>(pr[d], p);
+                widen_row<SH>(qr[d], q);
+                dot[d] = lane_dot<SH>(p, q);
+            }
+            group_allreduce<SH, D>(dot);
+#pragma unroll
+            for (int d = 0; d < D; d++) {
+                const float err = sr[d] - dot[d];
+                if (val[d] && !isfinite(err)) bad = 1;
+                float p[SH::E], q[SH::E];
+                widen_row<SH>(pr[d], p);
+                widen_row<SH>(qr[d], q);
+                sgd_step<SH>(p, q, err, a.eta, a.lam);
+                narrow_row<SH>(p, pr[d]);
+                narrow_row<SH>(q, qr[d]);
+                store_row<SH>(a.P, su[d], k, sub, val[d], pr[d]);
+                store_row<SH>(a.Q, sv[d], k, sub, val[d], qr[d]);
+                if (val[d] && sub == 0) done++;
+            }
         }
-        grid_barrier(a.scratch, gridDim.x);
+        if (BLOCK == kBlock) grid_barrier(a.scratch, gridDim.x);
+        else grid_barrier_ra(a.scratch, gridDim.x);
     }
     if (bad) a.scratch->diverged = 1;
     if (a.count_updates && done) atomicAdd(&a.scratch->updates, done);
 }
 
-cudaError_t launch_waves(const ShapeId &sh, const UpdateArgs &a, cudaStream_t st, int *launches) {
+cudaError_t launch_waves(const ShapeId &sh, const UpdateArgs &a, cudaStream_t st, int *launches, int big) {
     return dispatch_shape(sh, [&](auto tag) -> cudaError_t {
         using SH = decltype(tag);
         int dev = 0, sms = 0, per_sm = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (big) {  // one 1024-thread CTA per SM: a quarter of the barrier arrivals; big = 2: two per group
+            const void *kern = (const void *)k_waves<SH, 1024, 1>;
+            if constexpr (SH::FULL) {
+                if (big == 2) kern = (const void *)k_waves<SH, 1024, 2>;
+            }
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 1024, 0);
+            if (per_sm >= 1) {
+                UpdateArgs args = a;
+                void *kargs[] = {&args};
+                if (launches) *launches = 1;
+                return cudaLaunchCooperativeKernel(kern, dim3(sms), dim3(1024), kargs, 0, st);
+            }
+        }
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_waves<SH>, kBlock, 0);
         if (per_sm < 1) return cudaErrorLaunchOutOfResources;
         // the largest wave decides how many groups are useful

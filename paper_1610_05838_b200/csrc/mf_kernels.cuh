@@ -49,7 +49,7 @@ struct ShapeId {
 // launchers (return cudaError_t; grid sizing inside)
 cudaError_t launch_hogwild(const ShapeId &sh, const UpdateArgs &a, int workers, int variant, cudaStream_t st,
                            int *workers_used);
-cudaError_t launch_waves(const ShapeId &sh, const UpdateArgs &a, cudaStream_t st, int *launches);
+cudaError_t launch_waves(const ShapeId &sh, const UpdateArgs &a, cudaStream_t st, int *launches, int big = 0);
 cudaError_t launch_rmse(const ShapeId &sh, const int32_t *u, const int32_t *v, const float *r, int64_t n,
                         const void *P, const void *Q, int k, double *partials, int nparts, double *out,
                         cudaStream_t st, int do_sqrt = 1);

@@ -119,6 +119,26 @@ def test_c1_deterministic_bit_reproducible_and_multi_epoch(mfmod, c1):
     assert outs[0][2] == pytest.approx(trace[-1], rel=1e-5)
 
 
+@pytest.mark.parametrize("storage,cfgname", [(0, "C2-1pct"), (1, "C2-1pct"), (2, "C1"), (1, "C2-zipf-1pct")])
+def test_deterministic_executions_bitwise_equal(mfmod, storage, cfgname):
+    """The deterministic schedule's executions (MF_OPT_VARIANT bits 24..25): 1024-thread CTAs with two
+    samples of a wave per group (default), with one, and 256-thread CTAs with the fenced barrier apply
+    the same updates wave by wave with the same per-rating arithmetic, so their factors agree bit for
+    bit (3 epochs)."""
+    cfg = datagen.CONFIGS[cfgname]
+    (u, v, r), _ = datagen.make(cfg)
+    out = []
+    for var in (0, 1 << 24, 2 << 24):
+        with _gpu(mfmod, cfg, storage, count_updates=1, variant=var) as g:
+            g.load(u, v, r)
+            for _ in range(3):
+                assert g.epoch("deterministic").updates == len(u)
+            out.append(g.factors())
+    for P, Q in out[1:]:
+        np.testing.assert_array_equal(P, out[0][0])
+        np.testing.assert_array_equal(Q, out[0][1])
+
+
 @pytest.mark.parametrize("k", [2, 7, 32, 33, 64, 100, 128, 256])
 @pytest.mark.parametrize("storage", [0, 1])
 def test_deterministic_k_sweep_ragged(mfmod, k, storage):
