@@ -642,7 +642,12 @@ int mf_ctx::run_wavefront(const ShapeId &, const UpdateArgs &ua, int *launches, 
         if (a.pf == 1 && row_bytes % 16) a.pf = 2;
         // bits 20..21: Q-group staging, 0 = bulk async copies when rows are 16-B multiples, 2 = thread loop
         a.tma = ((variant_eff >> 20) & 0x3) != 2 && row_bytes % 16 == 0 && ((uintptr_t)Q & 15) == 0;
-        const int def_shape = k == 128 ? (storage == kF32 ? 2 : 1) : 0;
+        // (k = 32 / 64 keep the 16-byte-vector shapes: 4 / 8 lanes (16-bit rows), 8 / 16 lanes (fp32) --
+        // batch-Hogwild!'s 16-lane narrow-vector defaults for those k are not CTA-worker shapes)
+        const int def_shape = k == 128  ? (storage == kF32 ? 2 : 1)
+                              : k == 32 ? (storage == kF32 ? 1 : 2)
+                              : k == 64 ? (storage == kF32 ? 0 : 1)
+                                        : 0;
         const ShapeId sh = select_shape(k, storage, shape_sel ? shape_sel - 1 : def_shape);
         const bool one_in_flight = depth_sel ? depth_sel == 1 : (k == 128 && !shape_sel);
         CK(dispatch_cta_shape(sh, [&](auto tag) -> cudaError_t {

@@ -17,14 +17,18 @@ def main():
     cfg = datagen.CONFIGS["C1"]
     (u, v, r), test = datagen.make(cfg)
     for storage in ("f32", "f16", "bf16"):
-        for k in (cfg.k, 7, 128):
-            for sched, opts in (("hogwild", {}), ("deterministic", {}), ("wavefront", {}),
-                                ("wavefront", {"wave_cta": 1}), ("wavefront", {"wave_cta": 2}),
+        for k in (cfg.k, 7, 64, 128):
+            for sched, opts in (("hogwild", {}), ("hogwild", {"variant": 1 << 16}),
+                                ("deterministic", {}), ("deterministic", {"variant": 1 << 24}),
+                                ("deterministic", {"variant": 2 << 24}), ("wavefront", {}),
+                                ("wavefront", {"wave_cta": 1}), ("wavefront", {"wave_cta": 1, "variant": 1 << 16}),
+                                ("wavefront", {"wave_cta": 1, "variant": 2 << 16}),
+                                ("wavefront", {"wave_cta": 1, "variant": 2 << 20}), ("wavefront", {"wave_cta": 2}),
                                 ("partitioned", {"partitions": 3})):
                 g = mf.MF(cfg.m, cfg.n, k, cfg.alpha, cfg.lam, cfg.seed_init, storage=storage, beta=cfg.beta,
                           count_updates=1, trace=1, **opts)
                 g.load(u, v, r)
-                for _ in range(2):
+                for _ in range(4):  # epochs 0-2 are the auto-prefetch trials, 3 runs the pick
                     st = g.epoch(sched)
                     assert st.updates == len(u), (storage, k, sched, opts, st.updates)
                 g.rmse(*test)
