@@ -83,7 +83,13 @@ typedef enum {
                                  ratings in flight per batch-Hogwild! group (0 = auto: 2 for fp32, 1 for 16-bit rows);
                                  8..15 wavefront-CTA shape; 16..19 batch-Hogwild! L2 row prefetch distance in steps
                                  (0 = auto: MF_SCHED_HOGWILD epochs 0, 1, 2 run off, 1 step, off and the faster of the
-                                 last two is kept; 15 = off).  No setting changes what an update computes. */
+                                 last two is kept; 15 = off); for CTA wavefront workers 1 = bulk, 2 = per-line
+                                 P-row prefetch per tile (0 = auto as above).  20..21: CTA Q-group staging, 2 = thread
+                                 loop instead of bulk async copies.  24..25: deterministic execution, 0 = 1024-thread
+                                 CTAs with 2 samples of a wave per group, 1 = 1 sample, 2 = 256-thread CTAs (identical
+                                 results).  26..27: CTA in-block clamp, samples per concurrent group 0 -> 16, 1 -> 32,
+                                 2 -> 64, 3 -> 8.  Only bits 26..27 change what is computed (how many of a block's
+                                 ratings are in flight at once; lock-free inside a block as batch-Hogwild!). */
     MF_OPT_TRACE = 15,        /* wavefront audit trace: 1 = record (worker, block, t_start, t_end) per block */
     MF_OPT_SUBEPOCHS = 16,    /* partitioned: passes S per epoch, each over 1/S of the shuffled samples with its own Latin square (0 = auto = 4) */
     MF_OPT_WAVE_CTA = 17,     /* wavefront worker: 0 = one warp, block processed serially; 1 = one 1024-thread CTA

@@ -65,6 +65,7 @@ struct WfArgs {
     DevScratch *scratch;
     int s, c, k, latin, count_updates;
     int pf;               // CTA workers: L2 prefetch of a tile's P rows when it is claimed (0 off, 1 bulk, 2 per line)
+    int min_per_group;    // CTA workers: in-block concurrency clamp, samples per concurrent group
     int tma;              // CTA workers: stage the Q group with bulk async copies (TMA engine) instead of a thread loop
     float eta, lam;
     int64_t n_cols;       // column groups are balanced segments [floor(g n / c), floor((g+1) n / c))
@@ -177,6 +178,7 @@ __global__ void __launch_bounds__(kBlock) k_wavefront(WfArgs a) {
 // a block: P rows of the band and Q rows of the group are owned by this CTA alone).  The group is
 // copied back to global memory before the column lock is released.
 constexpr int kCtaThreads = 1024;
+constexpr int64_t kCtaMinPerGroup = 16;  // in-block concurrency clamp: samples per concurrent group
 
 // Q rows in shared memory are addressed with 32-bit shared-window offsets (ld/st.shared): no
 // generic-to-shared conversion per access.  volatile keeps this thread's st before its next ld of
@@ -384,9 +386,15 @@ __global__ void __launch_bounds__(THREADS, THREADS >= 1024 ? 1 : kCtaThreads / T
         // the group's Q rows: C3-1pct test RMSE +2.0% vs +0.3%, and 4-7% slower on C2.  Prefetching the
         // next tile's triples costs registers under the 64-per-thread cap of a 1024-thread CTA: f16
         // spills and drops from 12.0 to 10.8 G updates/s on C2.)
+        // In-block concurrency clamp (the A-10 reading applied inside a block): at most one group per
+        // kCtaMinPerGroup samples of the block updates at a time, so every group processes >= that
+        // many of the block's ratings.  Full-size shapes are not clamped (Netflix: 4,523 samples per
+        // block for 128 groups; Yahoo: 2,184); 1% slices are (C3-1pct: 115 samples per block, where all
+        // 128-256 groups at once left test RMSE +1.2..1.6% behind serial SGD at k = 32).
         for (;;) {
-            int t = 0;
-            if (lane == 0) t = atomicAdd(&s_next, 32);
+            int t = 0x3fffffff;  // warp w claims iff w * G * kCtaMinPerGroup < block size (w = 0 always)
+            if (lane == 0 && ((threadIdx.x >> 5) == 0 || (int64_t)(threadIdx.x >> 5) * SH::G * a.min_per_group < hi - lo))
+                t = atomicAdd(&s_next, 32);
             const int64_t base = lo + __shfl_sync(0xffffffffu, t, 0);
             if (base >= hi) break;  // warp-uniform
             const int64_t i = base + lane;
@@ -640,6 +648,10 @@ int mf_ctx::run_wavefront(const ShapeId &, const UpdateArgs &ua, int *launches, 
             a.pf = pf == 1 || pf == 2 ? pf : 0;
         }
         if (a.pf == 1 && row_bytes % 16) a.pf = 2;
+        {  // bits 26..27: in-block clamp, samples per concurrent group 0 -> 16, 1 -> 32, 2 -> 64, 3 -> 8
+            const int sel = (variant_eff >> 26) & 0x3;
+            a.min_per_group = sel == 0 ? (int)kCtaMinPerGroup : sel == 1 ? 32 : sel == 2 ? 64 : 8;
+        }
         // bits 20..21: Q-group staging, 0 = bulk async copies when rows are 16-B multiples, 2 = thread loop
         a.tma = ((variant_eff >> 20) & 0x3) != 2 && row_bytes % 16 == 0 && ((uintptr_t)Q & 15) == 0;
         // (k = 32 / 64 keep the 16-byte-vector shapes: 4 / 8 lanes (16-bit rows), 8 / 16 lanes (fp32) --

@@ -183,21 +183,23 @@ def test_wavefront_cta_shapes_rmse(mfmod, storage, variant, wave_cta):
 @pytest.mark.parametrize("storage,k", [(0, 32), (1, 32), (0, 64), (1, 64), (0, 256), (1, 256)])
 def test_wavefront_cta_k_sweep_rmse(mfmod, storage, k):
     """The CTA wavefront at the C5 k values other than 128 (its own default shapes per k): exactly once
-    per epoch, test RMSE within 0.5% of the storage-matched serial oracle after 5 epochs (C3-1pct)."""
+    per epoch, test RMSE within 0.5% of the storage-matched serial oracle after 5 epochs (C3-1pct;
+    its 115-sample blocks are where the in-block concurrency clamp acts)."""
     cfg = datagen.CONFIGS["C3-1pct"].scaled(k=k)
     (u, v, r), test = datagen.make(cfg)
     E = 5
-    order = oracle.shuffle_perm(cfg.seed_shuffle, len(u))
     st = {0: oracle.F32, 1: oracle.F16}[storage]
+    order = oracle.shuffle_perm(cfg.seed_shuffle, len(u))
     _, gold = oracle.train(cfg.m, cfg.n, cfg.k, st, cfg.seed_init, u, v, r, cfg.alpha, cfg.beta, cfg.lam, E,
                            order=order, test=test)
+    gate = 0.005
     with mfmod.MF(cfg.m, cfg.n, cfg.k, cfg.alpha, cfg.lam, cfg.seed_init, storage=storage, beta=cfg.beta,
                   wave_cta=1, count_updates=1, seed_shuffle=cfg.seed_shuffle) as g:
         g.load(u, v, r)
         for _ in range(E):
             assert g.epoch("wavefront").updates == len(u)
         got = g.rmse(*test)
-    assert abs(got - gold[-1]) <= 0.005 * gold[-1], (got, gold[-1])
+    assert abs(got - gold[-1]) <= gate * gold[-1], (got, gold[-1], gate)
 
 
 @pytest.mark.parametrize("storage,k,variant", [(0, 7, 0), (0, 33, 0), (0, 100, 0), (1, 7, 0), (1, 100, 0),
