@@ -347,7 +347,8 @@ def main():
         other_st = "f32" if a.storage != "f32" else "f16"
         for key, st_, sch, opts in ((f"hogwild/{other_st}", other_st, "hogwild", {}),
                                     (f"wavefront_cta/{a.storage}", a.storage, "wavefront", {"wave_cta": 1}),
-                                    (f"wavefront_cta/{other_st}", other_st, "wavefront", {"wave_cta": 1})):
+                                    (f"wavefront_cta/{other_st}", other_st, "wavefront", {"wave_cta": 1}),
+                                    (f"deterministic/{a.storage}", a.storage, "deterministic", {})):
             res = measure(st_, sch, max(3, a.steps // 5), 3, **opts)
             res["alg_GBps"] = b_alg(cfg.k, st_) * N / res["kernel_s"] / 1e9
             res["frac_alg"] = res["alg_GBps"] / peak

@@ -42,6 +42,7 @@ struct mf_ctx {
     struct AutoPf {
         int trials = 0, pick = 0;  // pick: 0 = undecided, else the bits-16..19 value in use (15 = off)
         float ms[2] = {0.f, 0.f};
+        float keep_on = 0.97f;     // "on" is kept iff ms_on < keep_on * ms_off (the prior: > 1 favours on)
         int next(int on, int *slot) const {
             if (pick) {
                 *slot = -1;
@@ -53,11 +54,14 @@ struct mf_ctx {
         void record(int slot, int on, float kernel_ms) {
             if (slot < 0) return;
             ms[slot] = kernel_ms;
-            if (++trials >= 3) pick = ms[1] < 0.97f * ms[0] ? on : 15;
+            if (++trials >= 3) pick = ms[1] < keep_on * ms[0] ? on : 15;
         }
         void reset() { trials = 0, pick = 0; }
     };
-    AutoPf pf_hogwild, pf_wave_cta;
+    // batch-Hogwild! keeps the prefetch only when it is clearly faster (it loses 6-16% where L2 is the
+    // limit); the CTA wavefront keeps it unless clearly slower (it won on 5 of 6 measured shape /
+    // storage pairs, by 2-13%), so one noisy trial epoch does not flip a small gain
+    AutoPf pf_hogwild, pf_wave_cta{0, 0, {0.f, 0.f}, 1.03f};
     int last_pf_pick = 0;   // pick of the last auto-tuned schedule run (reported by mf_get_option)
     int variant_eff = 0;    // the variant the current epoch's launches use (auto fields resolved)
     float last_kernel_ms = 0.f;
