@@ -139,7 +139,12 @@ int mf_epoch_host(mf_ctx *ctx, int schedule, const int32_t *u, const int32_t *v,
 
 /* Test RMSE sqrt(sum (r - p_u.q_v)^2 / nnz) over the given triples: fp32 dot, fp64 sum,
  * deterministic reduction order.  nnz >= 1.  In the partitioned NCCL mode the call is collective and
- * every rank passes its local test triples (u in its row segment); all ranks get the global value. */
+ * every rank passes its local test triples (u in its row segment; nnz = 0 allowed, the global count
+ * must be >= 1); all ranks get the global value.
+ * Collective calls (mf_epoch, mf_rmse, mf_get_factors with NCCL attached) agree on their status: every
+ * rank returns the most negative status any rank had, and a rank whose own arguments, state or test
+ * triples are invalid still takes part, so its peers are never left blocked in NCCL (mf_last_error of
+ * a rank that did nothing wrong says which status a peer had). */
 int mf_rmse(mf_ctx *ctx, const int32_t *u, const int32_t *v, const float *r, int64_t nnz, double *out);
 
 /* Copy factors to caller host buffers, widened to fp32, row-major (P: m x k, Q: n x k); either may be NULL.

@@ -536,8 +536,24 @@ int mf_ctx::finish_epoch(int schedule, float eta, int launches, int workers_used
     return MF_OK;
 }
 
+static int epoch_local(mf_ctx *ctx, int schedule, mf_epoch_stats *stats);
+
 extern "C" int mf_epoch(mf_ctx *ctx, int schedule, mf_epoch_stats *stats) {
     if (!ctx) return MF_EINVAL;
+    if (!ctx->is_distributed()) return epoch_local(ctx, schedule, stats);
+    // collective: a precondition failure on any rank is agreed before the exchange rounds start, and
+    // the outcome (e.g. divergence on one rank) after they end
+    int pre = MF_OK;
+    if (schedule != MF_SCHED_PARTITIONED)
+        pre = ctx->fail(MF_EINVAL, "with NCCL attached only MF_SCHED_PARTITIONED is available");
+    else if (ctx->N <= 0 || !ctx->P)
+        pre = ctx->fail(MF_ESTATE, "mf_epoch before mf_load_coo");
+    RC(ctx->agree(pre));
+    CK(cudaSetDevice(ctx->device));
+    return ctx->agree(ctx->epoch_partitioned(stats));
+}
+
+static int epoch_local(mf_ctx *ctx, int schedule, mf_epoch_stats *stats) {
     if (schedule < MF_SCHED_HOGWILD || schedule > MF_SCHED_PARTITIONED)
         return ctx->fail(MF_EINVAL, "unknown schedule %d", schedule);
     if (ctx->N <= 0 || !ctx->P) return ctx->fail(MF_ESTATE, "mf_epoch before mf_load_coo");
@@ -549,8 +565,6 @@ extern "C" int mf_epoch(mf_ctx *ctx, int schedule, mf_epoch_stats *stats) {
     if (schedule == MF_SCHED_DETERMINISTIC) RC(ctx->build_waves());
     if (schedule == MF_SCHED_WAVEFRONT) RC(ctx->build_wavefront());
     if (schedule == MF_SCHED_PARTITIONED) return ctx->epoch_partitioned(stats);
-    if (ctx->is_distributed())
-        return ctx->fail(MF_EINVAL, "with NCCL attached only MF_SCHED_PARTITIONED is available");
     RC(ctx->gather_q());
     ctx->seg_valid = false;
     cudaStream_t st = ctx->stream();
@@ -606,10 +620,25 @@ extern "C" int mf_epoch(mf_ctx *ctx, int schedule, mf_epoch_stats *stats) {
 // -------------------------------------------------------------------- rmse --
 extern "C" int mf_rmse(mf_ctx *ctx, const int32_t *u, const int32_t *v, const float *r, int64_t nnz, double *out) {
     if (!ctx || !out) return MF_EINVAL;
-    if (!u || !v || !r || nnz <= 0) return ctx->fail(MF_EINVAL, "mf_rmse: null pointer or nnz <= 0");
-    RC(ctx->ensure_factors());
+    const bool dist = ctx->is_distributed();
+    if (!dist) {
+        if (!u || !v || !r || nnz <= 0) return ctx->fail(MF_EINVAL, "mf_rmse: null pointer or nnz <= 0");
+        RC(ctx->ensure_factors());
+    } else {
+        // collective: every rank enters the all-gather / all-reduce or none does.  A rank may hold an
+        // empty test shard (nnz = 0); the global count must be > 0.
+        int pre = (nnz < 0 || (nnz > 0 && (!u || !v || !r))) ? ctx->fail(MF_EINVAL, "mf_rmse: null pointer or nnz < 0")
+                                                              : ctx->ensure_factors();
+        RC(ctx->agree(pre));
+    }
     CK(cudaSetDevice(ctx->device));
     RC(ctx->gather_q());
+    RC(dev_alloc(ctx, &ctx->partials, rmse_parts(), "alloc partials"));
+    RC(dev_alloc(ctx, &ctx->d_out, 2, "alloc out"));
+    if (dist && nnz == 0) {  // the same collective sequence as a non-empty shard: validation, sums, outcome
+        RC(ctx->agree(MF_OK));
+        return ctx->agree(ctx->rmse_partitioned(0, out));
+    }
     cudaStream_t st = ctx->stream();
     if (nnz > ctx->cap_t) {
         dev_free(&ctx->tu);
@@ -621,8 +650,6 @@ extern "C" int mf_rmse(mf_ctx *ctx, const int32_t *u, const int32_t *v, const fl
         RC(dev_alloc(ctx, &ctx->tr, nnz, "alloc test r"));
         ctx->cap_t = nnz;
     }
-    RC(dev_alloc(ctx, &ctx->partials, rmse_parts(), "alloc partials"));
-    RC(dev_alloc(ctx, &ctx->d_out, 2, "alloc out"));
     const cudaMemcpyKind kind = is_device_ptr(u) ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
     CK(cudaMemcpyAsync(ctx->tu, u, sizeof(int32_t) * nnz, kind, st));
     CK(cudaMemcpyAsync(ctx->tv, v, sizeof(int32_t) * nnz, kind, st));
@@ -631,10 +658,15 @@ extern "C" int mf_rmse(mf_ctx *ctx, const int32_t *u, const int32_t *v, const fl
     CK(launch_validate_rows(ctx->tu, ctx->tv, ctx->tr, nnz, ctx->p_begin, ctx->p_end, ctx->n, ctx->scratch, st));
     CK(cudaMemcpyAsync(ctx->h_scratch, ctx->scratch, sizeof(DevScratch), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
-    if (ctx->h_scratch->bad) return ctx->fail(MF_EINVAL, "mf_rmse: %llu invalid test samples",
-                                              (unsigned long long)ctx->h_scratch->bad);
+    if (dist) {
+        RC(ctx->agree(ctx->h_scratch->bad ? ctx->fail(MF_EINVAL, "mf_rmse: %llu invalid test samples",
+                                                      (unsigned long long)ctx->h_scratch->bad)
+                                          : MF_OK));
+    } else if (ctx->h_scratch->bad) {
+        return ctx->fail(MF_EINVAL, "mf_rmse: %llu invalid test samples", (unsigned long long)ctx->h_scratch->bad);
+    }
     if (ctx->p_begin != 0) CK(launch_rebase(ctx->tu, nnz, (int32_t)ctx->p_begin, st));
-    if (ctx->is_distributed()) return ctx->rmse_partitioned(nnz, out);
+    if (dist) return ctx->agree(ctx->rmse_partitioned(nnz, out));
     const ShapeId sh = select_shape(ctx->k, ctx->storage, 0);
     CK(launch_rmse(sh, ctx->tu, ctx->tv, ctx->tr, nnz, ctx->P, ctx->Q, ctx->k, ctx->partials, rmse_parts(),
                    ctx->d_out, st));
@@ -683,7 +715,7 @@ int mf_ctx::copy_in(void *X, int64_t count, const float *src) {
 
 extern "C" int mf_get_factors(mf_ctx *ctx, float *P, float *Q) {
     if (!ctx) return MF_EINVAL;
-    RC(ctx->ensure_factors());
+    RC(ctx->agree(ctx->ensure_factors()));  // collective with NCCL: the all-gather below
     CK(cudaSetDevice(ctx->device));
     RC(ctx->gather_q());
     if (P) RC(ctx->copy_out(ctx->P, ctx->p_rows() * ctx->k, P));

@@ -166,6 +166,8 @@ struct mf_ctx {
 
     // mf_wavefront.cu
     int build_wavefront();
+    int agree(int local);  // distributed: every rank returns the worst status any rank had (collective)
+    double *agree_buf = nullptr;
     int run_wavefront(const mf::ShapeId &sh, const mf::UpdateArgs &a, int *launches, int *workers_used);
     void release_wavefront();
 

@@ -178,11 +178,12 @@ extern "C" int mf_attach_nccl(mf_ctx *ctx, const void *id128, int rank, int worl
 
 // ---------------------------------------------------------------- layout ----
 void mf_ctx::release_partition() {
-    for (void *p : {(void *)bu, (void *)bv, (void *)br, gather_tmp})
+    for (void *p : {(void *)bu, (void *)bv, (void *)br, gather_tmp, (void *)agree_buf})
         if (p) cudaFree(p);
     bu = bv = nullptr;
     br = nullptr;
     gather_tmp = nullptr;
+    agree_buf = nullptr;
     for (auto *vec : {&q_cur, &q_next})
         for (void *p : *vec)
             if (p) cudaFree(p);
@@ -488,17 +489,45 @@ int mf_ctx::exchange_half(const std::vector<int32_t> &want, int h) {
     return MF_OK;
 }
 
+// Collective status agreement: each rank contributes its local status; every rank
+// returns the most negative status any rank had.  A rank that fails an argument check, a validation or
+// diverges therefore still enters the collective, its peers are never left blocked in an NCCL call,
+// and all ranks report the same outcome.  One all-reduce of a per-code count vector (fp64 sum).
+int mf_ctx::agree(int local) {
+    if (!is_distributed()) return local;
+    constexpr int kCodes = 8;  // statuses 0 .. -7
+    if (!agree_buf) CK(cudaMalloc((void **)&agree_buf, sizeof(double) * kCodes));
+    double h[kCodes] = {0};
+    if (local < 0 && local > -kCodes) h[-local] = 1.0;
+    cudaStream_t st = stream();
+    CK(cudaMemcpyAsync(agree_buf, h, sizeof h, cudaMemcpyHostToDevice, st));
+    NK(ncclAllReduce(agree_buf, agree_buf, kCodes, ncclFloat64, ncclSum, nccl->comm, st));
+    CK(cudaMemcpyAsync(h, agree_buf, sizeof h, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    for (int c = kCodes - 1; c >= 1; c--)
+        if (h[c] > 0) {
+            if (local == -c) return local;  // keep this rank's own message
+            return fail(-c, "a peer rank failed this collective call with %s", mf_status_string(-c));
+        }
+    return local;  // (a local status outside the code range is returned unchanged)
+}
+
 int mf_ctx::rmse_partitioned(int64_t nnz, double *out) {
-    // caller (mf_rmse) validated the local test triples, rebased u and gathered Q
+    // caller (mf_rmse) validated the local test triples, rebased u and gathered Q; nnz may be 0 here
     cudaStream_t st = stream();
     const ShapeId sh = select_shape(k, storage, 0);
-    CK(launch_rmse(sh, tu, tv, tr, nnz, P, Q, k, partials, rmse_parts(), d_out, st, 0));
+    if (nnz > 0) {
+        CK(launch_rmse(sh, tu, tv, tr, nnz, P, Q, k, partials, rmse_parts(), d_out, st, 0));
+    } else {
+        CK(cudaMemsetAsync(d_out, 0, sizeof(double), st));
+    }
     double cnt = (double)nnz;
     CK(cudaMemcpyAsync(d_out + 1, &cnt, sizeof(double), cudaMemcpyHostToDevice, st));
     NK(ncclAllReduce(d_out, d_out, 2, ncclFloat64, ncclSum, nccl->comm, st));
     double h[2];
     CK(cudaMemcpyAsync(h, d_out, sizeof h, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
+    if (!(h[1] > 0)) return fail(MF_EINVAL, "mf_rmse: the test shards of all ranks are empty");
     *out = std::sqrt(h[0] / h[1]);
     return MF_OK;
 }

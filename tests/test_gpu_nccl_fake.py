@@ -82,3 +82,36 @@ def test_multirank_partitioned_matches_oracle_block_sweep(fake_nccl, tmp_path, G
     assert np.linalg.norm(P - ref.P) / np.linalg.norm(ref.P) <= 1e-5
     assert np.linalg.norm(res[0]["Q"] - ref.Q) / np.linalg.norm(ref.Q) <= 1e-5
     assert float(res[0]["rmse"]) == pytest.approx(ref.rmse(tu, tv, tr), rel=1e-5)
+
+
+def test_collective_status_agreement(fake_nccl, tmp_path):
+    """mf_epoch / mf_rmse / mf_get_factors with NCCL attached are collective: a call that is invalid on
+    one rank only returns the same status on every rank and leaves no rank blocked (SURVEY §8(b));
+    a rank with an empty test shard still joins the global RMSE."""
+    from paper_1610_05838_b200 import mf
+    G = 2
+    cfg = datagen.CONFIGS["C1"]
+    (u, v, r), (tu, tv, tr) = datagen.make(cfg)
+    data = tmp_path / "d.npz"
+    np.savez(data, u=u, v=v, r=r, tu=tu, tv=tv, tr=tr, m=cfg.m, n=cfg.n, k=cfg.k)
+    uid_file, out = str(tmp_path / "uid"), str(tmp_path / "out")
+    env = dict(os.environ, LD_PRELOAD=fake_nccl, PYTHONPATH=os.path.dirname(HERE))
+    procs = [subprocess.Popen([sys.executable, os.path.join(HERE, "_fake_nccl_status.py"), str(g), str(G), uid_file,
+                               str(data), out], env=env) for g in range(G)]
+    try:
+        rcs = [p.wait(timeout=120) for p in procs]
+    finally:
+        for p in procs:
+            if p.poll() is None:
+                p.kill()
+        uid = open(uid_file, "rb").read().split(b"\0")[0].decode() if os.path.exists(uid_file) else None
+        if uid and os.path.exists(uid):
+            os.remove(uid)
+    assert rcs == [0] * G
+    res = [np.load(f"{out}_{g}.npz") for g in range(G)]
+    want = [mf.MF_ESTATE, mf.MF_EINVAL, 0, mf.MF_EINVAL]
+    for g in range(G):
+        assert list(res[g]["codes"]) == want, (g, list(res[g]["codes"]))
+    # the global RMSE with rank 1's test shard empty is rank 0's shard's RMSE, on both ranks
+    assert float(res[0]["rmse"][0]) == float(res[1]["rmse"][0])
+    np.testing.assert_array_equal(res[0]["Q"], res[1]["Q"])
