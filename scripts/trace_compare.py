@@ -1,0 +1,43 @@
+"""Development tool: per-epoch test RMSE of every single-GPU schedule on a full-size shape.
+
+The deterministic schedule reproduces serial SGD over the stored order (D-3; pinned to the
+oracle at 1e-5 on the slices the oracle can run), so at sizes where the CPU oracle would take hours its
+trace shows where the parallel schedules stand relative to serial SGD.
+
+python scripts/trace_compare.py [--cfg C3] [--storage f16] [--epochs 20]
+"""
+import argparse
+import json
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import datagen  # noqa: E402
+from paper_1610_05838_b200 import mf  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--cfg", default="C3")
+    ap.add_argument("--storage", default="f16")
+    ap.add_argument("--epochs", type=int, default=20)
+    ap.add_argument("--scheds", default="deterministic,hogwild,wavefront_cta")
+    a = ap.parse_args()
+    cfg = datagen.CONFIGS[a.cfg]
+    (u, v, r), test = datagen.make(cfg)
+    for sch in a.scheds.split(","):
+        opts = {"wave_cta": 1} if sch == "wavefront_cta" else {}
+        name = "wavefront" if sch == "wavefront_cta" else sch
+        with mf.MF(cfg.m, cfg.n, cfg.k, cfg.alpha, cfg.lam, cfg.seed_init, storage=a.storage, beta=cfg.beta,
+                   seed_shuffle=cfg.seed_shuffle, **opts) as g:
+            g.load(u, v, r)
+            tr = []
+            for _ in range(a.epochs):
+                g.epoch(name)
+                tr.append(g.rmse(*test))
+        print(json.dumps({"cfg": cfg.name, "storage": a.storage, "schedule": sch, "rmse": tr}), flush=True)
+
+
+if __name__ == "__main__":
+    main()
