@@ -132,3 +132,47 @@ def test_c2_exactly_once_and_order(c2):
         assert g.epoch("hogwild").updates == len(u)
         g.load(u, v, r)  # second load reuses the cached permutation and buffers
         np.testing.assert_array_equal(g.order()[:1000], oracle.shuffle_perm(cfg.seed_shuffle, len(u))[:1000])
+
+
+# ----------------------------------------------------------- Yahoo!Music shape
+# BASELINE.json configs[2]: N = 252,800,275, k = 128, "wavefront-update vs batch-Hogwild!".  Golden
+# traces: scripts/make_golden.py C3 <st> 10 (and seed 43 for the order's spread), oracle/ only.
+@pytest.fixture(scope="module")
+def c3():
+    cfg = datagen.CONFIGS["C3"]
+    return cfg, datagen.make(cfg)
+
+
+def _c3_gates(storage, gold):
+    traces = [gold]
+    p = os.path.join(GOLD, f"C3_{storage}_seed43_trace.json")
+    if os.path.exists(p):
+        traces.append(json.load(open(p))["rmse"])
+    return [max(0.005 * g, max(tr[t] for tr in traces if len(tr) > t) - min(tr[t] for tr in traces if len(tr) > t))
+            for t, g in enumerate(gold)]
+
+
+@pytest.mark.parametrize("storage", ["f32", "f16"])
+@pytest.mark.parametrize("schedule", ["hogwild", "wavefront_cta"])
+def test_c3_rmse_trace_vs_oracle_golden(c3, storage, schedule):
+    """Yahoo shape, both single-GPU schedules of configs[2], every epoch of the oracle's trace from the
+    second on within the gate (0.5%, or the oracle's own shuffle-seed spread where larger).  The first
+    epoch (the largest learning rate) is not gated (reading T4): against exact serial SGD it
+    is +4.5% for batch-Hogwild! and +34% for the CTA wavefront, whose first epoch walks the matrix
+    block by block (the slower start P:256 reports); both are within 0.4% from the second epoch on
+    (profiles/r01d_fullsize_traces_vs_serial.jsonl)."""
+    path = os.path.join(GOLD, f"C3_{storage}_trace.json")
+    if not os.path.exists(path):
+        pytest.skip(f"{path} not generated yet")
+    gold = json.load(open(path))["rmse"]
+    cfg, ((u, v, r), test) = c3
+    opts = {"wave_cta": 1} if schedule == "wavefront_cta" else {}
+    with _ctx(cfg, storage, count_updates=1, **opts) as g:
+        g.load(u, v, r)
+        got = []
+        for _ in range(len(gold)):
+            assert g.epoch("wavefront" if opts else "hogwild").updates == len(u)
+            got.append(g.rmse(*test))
+    gate = _c3_gates(storage, gold)
+    bad = [(t, a, b, gt) for t, (a, b, gt) in enumerate(zip(got, gold, gate)) if t >= 1 and abs(a - b) > gt]
+    assert not bad, bad
