@@ -326,6 +326,47 @@ def test_errors_and_divergence(mfmod):
             assert e.value.status == mf.MF_EDIVERGED
 
 
+@pytest.mark.parametrize("storage", [0, 1])
+@pytest.mark.parametrize("m_,n_,N,k", [(1, 1, 1, 128), (1, 1, 7, 32), (1, 5, 9, 64), (6, 1, 9, 128), (3, 2, 40, 7),
+                                      (3, 2, 29, 7)])
+def test_degenerate_shapes_every_schedule_is_serial(mfmod, storage, m_, n_, N, k):
+    """One row and/or one column (every rating depends on the previous one) and a tiny ragged problem:
+    each schedule, in its serial configuration, must reproduce the oracle's serial epochs on the
+    stored order -- batch-Hogwild! with one worker, the deterministic waves, the paper's wavefront
+    with s = c = 1, the streamed epoch with one worker, the CTA wavefront with s = c = 1 (k = 7, one
+    tile) and the
+    loopback partitioned path with one partition and one worker (one column)."""
+    rng = np.random.default_rng(m_ * 100 + n_ * 10 + N)
+    u = rng.integers(0, m_, N).astype(np.int32)
+    v = rng.integers(0, n_, N).astype(np.int32)
+    r = rng.normal(size=N).astype(np.float32)
+    st = ORC[storage]
+    ref = oracle.Model(m_, n_, k, st, seed=5)
+    for t in range(2):
+        ref.epoch(u, v, r, oracle.eta(0.05, 0.3, t), 0.02)
+    Pr, Qr = ref.factors_f32()
+    tol = TOL[storage]
+    runs = [("hogwild", {"workers": 1}), ("deterministic", {}), ("wavefront", {"wave_rows": 1, "wave_cols": 1}),
+            ("host", {"workers": 1})]
+    if k == 7 and N <= 32:  # a masked 32-lane CTA shape, one rating at a time, one 32-sample tile
+        runs.append(("wavefront", {"wave_cta": 1, "wave_rows": 1, "wave_cols": 1}))
+    if n_ == 1:  # one column: the partition's lower / upper half-segment split keeps the stored order
+        runs.append(("partitioned", {"partitions": 1, "workers": 1, "subepochs": 1}))
+    for sched, opts in runs:
+        with mfmod.MF(m_, n_, k, 0.05, 0.02, 5, storage=storage, beta=0.3, shuffle=0, count_updates=1,
+                      **opts) as g:
+            for _ in range(2):
+                if sched == "host":
+                    g.epoch_host(u, v, r)
+                else:
+                    if _ == 0:
+                        g.load(u, v, r)
+                    assert g.epoch(sched).updates == N, sched
+            P, Q = g.factors()
+        for X, R in ((P, Pr), (Q, Qr)):
+            assert np.linalg.norm(X - R) <= tol * np.linalg.norm(R), (sched, opts)
+
+
 def test_device_pointers_accepted(mfmod, c1):
     """Inputs already in HBM (torch CUDA tensors) give the same order and result as host arrays."""
     import torch
