@@ -176,3 +176,24 @@ def test_c3_rmse_trace_vs_oracle_golden(c3, storage, schedule):
     gate = _c3_gates(storage, gold)
     bad = [(t, a, b, gt) for t, (a, b, gt) in enumerate(zip(got, gold, gate)) if t >= 1 and abs(a - b) > gt]
     assert not bad, bad
+
+
+# ------------------------------------------------------------ Hugewiki shape
+def test_c4_full_size_exactly_once_beyond_int32():
+    """The largest configured problem on one GPU (BASELINE.json configs[3], Hugewiki-shaped: N =
+    3,069,817,980 > 2^31 samples, m = 50M rows, P = 12.8 GB in fp16): batch-Hogwild! and the CTA
+    wavefront each process every sample exactly once per epoch (64-bit sample counts, offsets and row
+    addresses) and the test RMSE improves on the initial factors'."""
+    cfg = datagen.CONFIGS["C4"]
+    (u, v, r), test = datagen.make(cfg)
+    assert len(u) > 2 ** 31
+    with _ctx(cfg, "f16", count_updates=1, shuffle=0) as g:
+        g.load(u, v, r)
+        r0 = g.rmse(*test)
+        assert g.epoch("hogwild").updates == len(u)
+        r1 = g.rmse(*test)
+        from paper_1610_05838_b200 import mf
+        g.set(mf.MF_OPT_WAVE_CTA, 1)
+        assert g.epoch("wavefront").updates == len(u)
+        r2 = g.rmse(*test)
+    assert r1 < 0.5 * r0 and r2 < r1, (r0, r1, r2)
