@@ -2,12 +2,16 @@
 synthetic workload (BASELINE.json configs[1]), k = 128, on one B200 (or G B200s, partitioned).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--storage f16|f32|bf16] [--config C2] [--schedule hogwild]
+                    [--storage f16|f32|bf16] [--config C2] [--schedule hogwild|wavefront_cta|...]
+                    [--scaling weak|strong]
 
 One step = one epoch of the hot path over the whole training set (N = 99,072,112 updates) followed by
 the test-RMSE evaluation, both in libmf.so's kernels.  Prints ONE JSON line (rank 0).
 `value` is device-timed with inputs resident in HBM; `e2e` repeats the step through the public C ABI
-from pinned HOST buffers (mf_load_coo H2D + validation + A-8 shuffle, mf_epoch, mf_rmse, result D2H).
+from pinned HOST buffers (batch-Hogwild!: mf_epoch_host streams R from host memory every step, H2D
+overlapped with the update kernel; other schedules: mf_load_coo H2D + validation + A-8 shuffle,
+mf_epoch), then mf_rmse with the test set from host memory and the result D2H.
+N > 1 (torchrun): the partitioned path with NCCL Q rotation, one process per GPU, max-over-ranks time.
 `--impl reference` times the CPU oracle (the only reference this paper-only task has) on a bounded
 sample of the same workload.
 """
