@@ -112,7 +112,7 @@ def load_traffic(storage, cfgname):
         return None
 
 
-def load_pattern_ceiling(cfg, storage):
+def load_pattern_ceiling(cfg, storage, p_only=False):
     """Best updates/s of scripts/sgd_mem_ceiling.cu (the update's exact row traffic -- triple stream,
     p_u and q_v read + written through L2 -- without its arithmetic) for this workload's shape, from the
     committed sweep profiles/r01c_mem_ceiling.jsonl (or None).  It is the memory system's ceiling for
@@ -120,7 +120,8 @@ def load_pattern_ceiling(cfg, storage):
     row_bytes = cfg.k * (4 if storage == "f32" else 2)
     try:
         best, match = None, False
-        with open(os.path.join(ROOT, "profiles", "r01c_mem_ceiling.jsonl")) as f:
+        name = "r01c_mem_ceiling_p_only.jsonl" if p_only else "r01c_mem_ceiling.jsonl"
+        with open(os.path.join(ROOT, "profiles", name)) as f:
             for line in f:
                 d = json.loads(line)
                 if "m" in d:
@@ -356,8 +357,13 @@ def main():
             res = measure(st_, sch, max(3, a.steps // 5), 3, **opts)
             res["alg_GBps"] = b_alg(cfg.k, st_) * N / res["kernel_s"] / 1e9
             res["frac_alg"] = res["alg_GBps"] / peak
+            # against the memory-pattern ceiling of the kernel's own global traffic (p+q rows for
+            # batch-Hogwild!, p rows only for the CTA wavefront whose Q group is on chip)
+            ceil = load_pattern_ceiling(cfg, st_, p_only=(sch == "wavefront")) if sch != "deterministic" else None
+            res["frac_of_pattern_ceiling"] = (N / res["kernel_s"]) / ceil if ceil else None
             others[key] = {k_: res[k_] for k_ in ("value", "ms", "kernel_s", "rmse", "workers", "alg_GBps",
-                                                  "frac_alg", "epochs_done", "variant")}
+                                                  "frac_alg", "epochs_done", "variant",
+                                                  "frac_of_pattern_ceiling")}
 
     # end to end through the public API from pinned host buffers
     hu, hv, hr = (torch.from_numpy(x).pin_memory() for x in (u, v, r))
