@@ -178,6 +178,14 @@ int mf_round_segment(uint64_t seed, int32_t pass, int32_t G, int32_t round, int3
  * over to round 0 of pass+1): it sends its segment to *send_to and receives from *recv_from. */
 int mf_round_peers(uint64_t seed, int32_t pass, int32_t G, int32_t round, int32_t rank, int32_t *send_to,
                    int32_t *recv_from);
+/* The paper's Hogwild! feasibility rule (§5.5.1): with s concurrent workers on an i x j
+ * block grid of an m x n matrix, convergence was observed only for s < min(floor(m/i), floor(n/j)) /
+ * safety (safety = 20 in the paper: Hugewiki, min(m, n) = 40k, s = 768 converges at j = 2, fails at
+ * j = 4).  Returns 1 (pass) or 0 (fail) and the bound in *bound; MF_EINVAL (< 0) for non-positive
+ * arguments.  Advisory only: the library's default worker count is DESIGN.md reading A-10 (every worker
+ * processes >= 10^4 samples per epoch), which measured parity holds for where this rule fails (the
+ * Netflix shape: s = 9,472 against a bound of 888, test RMSE within 0.035% of serial SGD). */
+int mf_feasibility(int64_t m, int64_t n, int32_t i, int32_t j, int64_t s, int32_t safety, int64_t *bound);
 
 /* Wavefront audit (MF_OPT_TRACE=1): copies up to cap records of 4 int64 (worker, block, t_start, t_end
  * in globaltimer ns) from the last wavefront epoch; *count = records written. */

@@ -111,6 +111,14 @@ extern "C" int mf_segment(int64_t extent, int32_t parts, int32_t index, int64_t 
     return MF_OK;
 }
 
+extern "C" int mf_feasibility(int64_t m, int64_t n, int32_t i, int32_t j, int64_t s, int32_t safety, int64_t *bound) {
+    if (m <= 0 || n <= 0 || i <= 0 || j <= 0 || s <= 0 || safety <= 0) return MF_EINVAL;
+    // s < 1/20 * min(floor(m/i), floor(n/j)), compared exactly (s * safety < min)
+    const int64_t mn = std::min(m / i, n / j);
+    if (bound) *bound = mn / safety;
+    return s * safety < mn ? 1 : 0;
+}
+
 extern "C" int mf_round_segment(uint64_t seed, int32_t epoch, int32_t G, int32_t round, int32_t rank,
                                 int32_t *col_segment) {
     if (G <= 0 || round < 0 || round >= G || rank < 0 || rank >= G || epoch < 0 || !col_segment) return MF_EINVAL;

@@ -55,6 +55,8 @@ _sig = {
     "mf_round_peers": ([c.c_uint64, c.c_int32, c.c_int32, c.c_int32, c.c_int32, c.POINTER(c.c_int32),
                         c.POINTER(c.c_int32)], c.c_int),
     "mf_wavefront_trace": ([_P, _P, c.c_int64, c.POINTER(c.c_int64)], c.c_int),
+    "mf_feasibility": ([c.c_int64, c.c_int64, c.c_int32, c.c_int32, c.c_int64, c.c_int32, c.POINTER(c.c_int64)],
+                       c.c_int),
     "mf_destroy": ([_P], None),
     "mf_last_error": ([_P], c.c_char_p),
     "mf_status_string": ([c.c_int], c.c_char_p),
@@ -200,6 +202,15 @@ def mf_wavefront_trace(ctx, cap):
     cnt = c.c_int64()
     _check(ctx, _lib.mf_wavefront_trace(ctx, out.ctypes.data, cap, c.byref(cnt)))
     return out[:cnt.value]
+
+
+def mf_feasibility(m, n, i, j, s, safety=20):
+    """(passes, bound) of the paper's rule s < min(m // i, n // j) / safety (PAPER.md:518-521)."""
+    b = c.c_int64()
+    rc = _lib.mf_feasibility(m, n, i, j, s, safety, c.byref(b))
+    if rc < 0:
+        raise MFError(rc, "mf_feasibility: arguments must be positive")
+    return bool(rc), b.value
 
 
 def mf_destroy(ctx):

@@ -68,3 +68,21 @@ def test_segments_partition_the_extent():
         assert segs[0][0] == 0 and segs[-1][1] == extent
         assert all(a[1] == b[0] for a, b in zip(segs, segs[1:]))
         assert all(e - b in (extent // G, extent // G + 1) for b, e in segs)
+
+
+def test_feasibility_rule_matches_the_papers_pair():
+    """mf_feasibility against the paper's printed example: Hugewiki, min(m, n) = 40k,
+    s = 768 workers -- converges at j = 2 (bound 40000/2/20 = 1000 > 768), fails at j = 4 (500 < 768);
+    s = 1 on a 21 x 21 matrix passes (1 < 21/20: the comparison is exact, SPEC.md's trivial example);
+    non-positive arguments are rejected."""
+    from paper_1610_05838_b200 import mf
+    m_hw, n_hw = 50_082_604, 40_000
+    assert mf.mf_feasibility(m_hw, n_hw, 1, 2, 768) == (True, 1000)
+    assert mf.mf_feasibility(m_hw, n_hw, 1, 4, 768) == (False, 500)
+    assert mf.mf_feasibility(21, 21, 1, 1, 1) == (True, 1)
+    assert mf.mf_feasibility(20, 20, 1, 1, 1) == (False, 1)
+    assert mf.mf_feasibility(40, 40, 1, 1, 1) == (True, 2)
+    # the Netflix shape at the library's default worker count fails the paper's rule (A-10 replaces it)
+    assert mf.mf_feasibility(480_190, 17_771, 1, 1, 9_472) == (False, 888)
+    with pytest.raises(mf.MFError):
+        mf.mf_feasibility(0, 10, 1, 1, 1)
