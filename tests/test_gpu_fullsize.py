@@ -199,3 +199,40 @@ def test_c4_full_size_exactly_once_beyond_int32():
         assert g.epoch("wavefront").updates == len(u)
         r2 = g.rmse(*test)
     assert r1 < 0.5 * r0 and r2 < r1, (r0, r1, r2)
+
+
+# ------------------------------------------------- Hugewiki shape, parity slice
+# the C4 parity config is C4-rows/10 (m = 5,008,260, n = 39,781 kept, N = 306,981,798).
+# Golden: scripts/make_golden.py C4-rows10 f32 10 (and seed 43), oracle/ only.
+@pytest.fixture(scope="module")
+def c4r10():
+    cfg = datagen.CONFIGS["C4-rows10"]
+    return cfg, datagen.make(cfg)
+
+
+@pytest.mark.parametrize("schedule,G", [("hogwild", 1), ("partitioned", 2), ("partitioned", 4), ("partitioned", 8)])
+def test_c4_rows10_rmse_trace_vs_oracle_golden(c4r10, schedule, G):
+    """BASELINE.json configs[3] (R-block grid partition at 2 / 4 / 8 GPUs) at its parity size: the
+    partitioned schedule with G partitions (the loopback transport: the same layout, Latin-square
+    rounds, passes and pipelined half-segment hand-over as G GPUs, run on this one) and batch-Hogwild!
+    track the serial oracle within the gate from the second epoch on (reading T4)."""
+    path = os.path.join(GOLD, "C4-rows10_f32_trace.json")
+    if not os.path.exists(path):
+        pytest.skip(f"{path} not generated yet")
+    gold = json.load(open(path))["rmse"]
+    cfg, ((u, v, r), test) = c4r10
+    opts = {"partitions": G} if schedule == "partitioned" else {}
+    with _ctx(cfg, "f32", count_updates=1, **opts) as g:
+        g.load(u, v, r)
+        got = []
+        for _ in range(len(gold)):
+            assert g.epoch(schedule).updates == len(u)
+            got.append(g.rmse(*test))
+    traces = [gold]
+    p = os.path.join(GOLD, "C4-rows10_f32_seed43_trace.json")
+    if os.path.exists(p):
+        traces.append(json.load(open(p))["rmse"])
+    gate = [max(0.005 * x, max(tr[t] for tr in traces if len(tr) > t) - min(tr[t] for tr in traces if len(tr) > t))
+            for t, x in enumerate(gold)]
+    bad = [(t, a, b, gt) for t, (a, b, gt) in enumerate(zip(got, gold, gate)) if t >= 1 and abs(a - b) > gt]
+    assert not bad, bad
