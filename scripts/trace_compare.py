@@ -22,13 +22,21 @@ def main():
     ap.add_argument("--cfg", default="C3")
     ap.add_argument("--storage", default="f16")
     ap.add_argument("--epochs", type=int, default=20)
-    ap.add_argument("--scheds", default="deterministic,hogwild,wavefront_cta")
+    ap.add_argument("--scheds", default="deterministic,hogwild,wavefront_cta",
+                    help="comma list; partitioned:G runs G loopback partitions")
     a = ap.parse_args()
     cfg = datagen.CONFIGS[a.cfg]
     (u, v, r), test = datagen.make(cfg)
     for sch in a.scheds.split(","):
         opts = {"wave_cta": 1} if sch == "wavefront_cta" else {}
         name = "wavefront" if sch == "wavefront_cta" else sch
+        if sch.startswith("partitioned:"):  # loopback partitions, e.g. partitioned:8 or partitioned:8:16 (S)
+            f = sch.split(":")
+            name, opts = "partitioned", {"partitions": int(f[1])}
+            if len(f) > 2 and f[2]:
+                opts["subepochs"] = int(f[2])
+            if len(f) > 3:  # partitioned:G:S:workers
+                opts["workers"] = int(f[3])
         with mf.MF(cfg.m, cfg.n, cfg.k, cfg.alpha, cfg.lam, cfg.seed_init, storage=a.storage, beta=cfg.beta,
                    seed_shuffle=cfg.seed_shuffle, **opts) as g:
             g.load(u, v, r)
