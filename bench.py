@@ -532,6 +532,9 @@ def run_partitioned(a, cfg, rank, world, local):
             "warmup": a.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": a.scaling,
             "vs_baseline": None, "dtype": "f32", "storage": a.storage, "data": "synthetic",
             "config": workload_config(cfg, G, a.storage, "partitioned", a.scaling),
+            "arm": {"workers_per_partition": st.workers, "q_segment_cols": cfg.n // G,
+                    "in_flight_per_q_column": st.workers / max(1, cfg.n // G),
+                    "note": "accuracy falls with in-flight ratings per Q-segment column (DESIGN.md 5.5)"},
             "test_rmse": rm,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                          "traffic": None, "peak_kind": peak_kind, "kernel": "k_hogwild (rank 0, all rounds)",
