@@ -3,7 +3,7 @@
 python scripts/c4probe.py C4 f16
 """
 import os, sys, time, json
-sys.path.insert(0, "/root/repo")
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
 import datagen
 from paper_1610_05838_b200 import mf

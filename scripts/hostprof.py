@@ -1,12 +1,15 @@
+"""Host vs device time of partitioned epochs on one GPU (1 loopback partition, S passes): how far the
+host stays ahead of the launches.  Development tool."""
+import os
 import sys, time
-sys.path.insert(0, "/root/repo")
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import datagen
 from paper_1610_05838_b200 import mf
 cfg = datagen.CONFIGS["C2"]
 (u, v, r), test = datagen.make(cfg)
 for S in (4, 64):
     g = mf.MF(cfg.m, cfg.n, cfg.k, cfg.alpha, cfg.lam, cfg.seed_init, storage="f16", beta=cfg.beta, shuffle=0,
-              variant=16, partitions=1, subepochs=S)
+              variant=0, partitions=1, subepochs=S)
     g.load(u, v, r)
     g.epoch("partitioned")
     for _ in range(3):
