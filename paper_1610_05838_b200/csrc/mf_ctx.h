@@ -38,7 +38,8 @@ struct mf_ctx {
     // L2 prefetch, auto mode (MF_OPT_VARIANT bits 16..19 = 0).  Whether a prefetch pays depends on
     // where the rows live (it hides DRAM latency, and costs L2 request slots where the L2 is the
     // bottleneck), and it never changes what an epoch computes, so the library times it: epochs 0, 1, 2
-    // of a schedule run off (a warm-up, not counted), on, off; the faster of the last two is kept.
+    // of a schedule run off (a warm-up, not counted), on, off, and "on" is kept iff its epoch took less
+    // than keep_on x the "off" epoch.
     struct AutoPf {
         int trials = 0, pick = 0;  // pick: 0 = undecided, else the bits-16..19 value in use (15 = off)
         float ms[2] = {0.f, 0.f};
