@@ -65,7 +65,8 @@ typedef enum {
 typedef enum {
     MF_OPT_STORAGE = 0,       /* feature storage: 0 fp32, 1 fp16, 2 bf16; math is fp32. Before the first load. */
     MF_OPT_BETA = 1,          /* beta of the LR schedule (default 0) */
-    MF_OPT_WORKERS = 2,       /* batch-Hogwild! concurrent workers (groups); 0 = auto (A-10) */
+    MF_OPT_WORKERS = 2,       /* batch-Hogwild! concurrent ratings, also per partition of MF_SCHED_PARTITIONED; 0 = auto
+                                 (A-10: every worker processes >= 10^4 samples per epoch, capped by residency) */
     MF_OPT_BATCH_F = 3,       /* samples per batch-Hogwild! chunk, multiple of 32 (default 256) */
     MF_OPT_WAVE_ROWS = 4,     /* wavefront workers s = row bands (0 = auto) */
     MF_OPT_WAVE_COLS = 5,     /* wavefront column blocks c >= s (0 = auto) */
@@ -80,11 +81,11 @@ typedef enum {
     MF_OPT_PARTITIONS = 12,   /* MF_SCHED_PARTITIONED without NCCL: G logical partitions run on this GPU (loopback) */
     MF_OPT_SEED_SHUFFLE = 13, /* seed of the A-8 shuffle (default: the mf_create seed) */
     MF_OPT_VARIANT = 14,      /* kernel variant selector for tuning (0 = default).  Bit fields: 0..3 group shape; 4..7
-                                 ratings in flight per batch-Hogwild! group (0 = auto: 2 for fp32, 1 for 16-bit rows);
-                                 8..15 wavefront-CTA shape; 16..19 batch-Hogwild! L2 row prefetch distance in steps
-                                 (0 = auto: MF_SCHED_HOGWILD epochs 0, 1, 2 run off, 1 step, off and the faster of the
-                                 last two is kept; 15 = off); for CTA wavefront workers 1 = bulk, 2 = per-line
-                                 P-row prefetch per tile (0 = auto as above).  20..21: CTA Q-group staging, 2 = thread
+                                 ratings in flight per batch-Hogwild! group (0 = auto: 2 for fp32 rows of k >= 128,
+                                 else 1); 8..15 wavefront-CTA shape; 16..19 batch-Hogwild! L2 row prefetch distance
+                                 in steps (0 = auto: MF_SCHED_HOGWILD epochs 0, 1, 2 run off, 1 step, off and the
+                                 prefetch is kept iff its epoch was > 3% faster; 15 = off); for CTA wavefront workers
+                                 1 = bulk, 2 = per-line P-row prefetch per tile (0 = auto: kept unless > 3% slower).  20..21: CTA Q-group staging, 2 = thread
                                  loop instead of bulk async copies.  24..25: deterministic execution, 0 = 1024-thread
                                  CTAs with 2 samples of a wave per group, 1 = 1 sample, 2 = 256-thread CTAs (identical
                                  results).  26..27: CTA in-block clamp, samples per concurrent group 0 -> 16, 1 -> 32,
