@@ -96,7 +96,11 @@ typedef enum {
     MF_OPT_WAVE_CTA = 17,     /* wavefront worker: 0 = one warp, block processed serially; 1 = one 1024-thread CTA
                                  per SM with the column group's Q rows staged in shared memory, lock-free inside the block;
                                  2 = as 1 with two 512-thread CTA workers per SM */
-    MF_OPT_STREAM_CHUNK = 18  /* mf_epoch_host: samples per streamed chunk (default 2^23) */
+    MF_OPT_STREAM_CHUNK = 18, /* mf_epoch_host: samples per streamed chunk (default 2^23) */
+    MF_OPT_PART_SPLIT = 19    /* partitioned: 0 = one launch per block, its workers spread over the whole Q segment, the
+                                 hand-over after it (default); 1 = each block as two half-segment sub-blocks, the lower
+                                 half's hand-over overlapping the upper half's updates -- twice the ratings in flight per
+                                 Q column, so further from serial SGD */
 } mf_option;
 
 typedef struct {

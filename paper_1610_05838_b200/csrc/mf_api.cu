@@ -297,6 +297,11 @@ extern "C" int mf_set_option(mf_ctx *ctx, int key, double value) {
             ctx->wave_cta = (int)iv;
             ctx->wf_valid = false;
             return MF_OK;
+        case MF_OPT_PART_SPLIT:
+            if (iv < 0 || iv > 1) return ctx->fail(MF_EINVAL, "part split must be 0 or 1");
+            ctx->part_split = (int)iv;
+            ctx->part_valid = false;
+            return MF_OK;
         case MF_OPT_STREAM_CHUNK:
             if (iv < 32 || iv > (1ll << 34)) return ctx->fail(MF_EINVAL, "stream chunk must be in [32, 2^34]");
             ctx->stream_chunk = iv;
@@ -331,6 +336,7 @@ extern "C" int mf_get_option(const mf_ctx *ctx, int key, double *value) {
         case MF_OPT_SUBEPOCHS: *value = ctx->subepochs ? ctx->subepochs : ctx->part_S; return MF_OK;
         case MF_OPT_WAVE_CTA: *value = ctx->wave_cta; return MF_OK;
         case MF_OPT_STREAM_CHUNK: *value = (double)ctx->stream_chunk; return MF_OK;
+        case MF_OPT_PART_SPLIT: *value = ctx->part_split; return MF_OK;
         default: return MF_EINVAL;
     }
 }

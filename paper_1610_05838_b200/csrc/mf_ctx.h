@@ -32,6 +32,7 @@ struct mf_ctx {
     int count_updates = 0;
     int partitions = 0;
     int subepochs = 0;  // passes per epoch of the partitioned schedule (MF_OPT_SUBEPOCHS; 0 = 4)
+    int part_split = 0; // partitioned: 1 = blocks as two half-segment sub-blocks, pipelined hand-over (MF_OPT_PART_SPLIT)
     int wave_cta = 0;   // wavefront worker = CTA with shared-memory Q group (MF_OPT_WAVE_CTA)
     int variant = 0;
     int trace = 0;

@@ -51,7 +51,7 @@ __device__ __forceinline__ int seg_of(int64_t x, int64_t extent, int parts) {
 // sample i is floor(i * S / n), i.e. every epoch is S passes over consecutive slices of the shuffled
 // order; each block is split into the samples of the lower and upper half of its column segment
 __global__ void k_part_keys(const int32_t *u, const int32_t *v, int64_t n, int64_t m_rows, int64_t n_cols, int G,
-                            int rows_split, int S, uint32_t *keys, uint32_t *idx) {
+                            int rows_split, int S, int half_split, uint32_t *keys, uint32_t *idx) {
     const int local = rows_split ? G : 1;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
         const int rs = rows_split ? seg_of(u[i], m_rows, G) : 0;
@@ -59,7 +59,7 @@ __global__ void k_part_keys(const int32_t *u, const int32_t *v, int64_t n, int64
         const int cs = seg_of(v[i], n_cols, G);
         // half: the column segment's lower / upper half of rows (pipelined exchange)
         const int64_t qb = ((int64_t)cs * n_cols) / G, qe = ((int64_t)(cs + 1) * n_cols) / G;
-        const int half = v[i] >= qb + (qe - qb) / 2 ? 1 : 0;
+        const int half = half_split && v[i] >= qb + (qe - qb) / 2 ? 1 : 0;
         keys[i] = (uint32_t)(((((int64_t)s * local + rs) * G + cs) << 1) | half);
         idx[i] = (uint32_t)i;
     }
@@ -256,7 +256,7 @@ int mf_ctx::build_partition() {
     CK(cudaMallocAsync((void **)&doff, sizeof(int64_t) * (nb + 1), st));
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((N + 255) / 256, 148 * 16));
     // loopback: rows are global, split into G segments; NCCL: u is already local to this rank's segment
-    k_part_keys<<<grid, 256, 0, st>>>(u, v, N, m, n, G, is_distributed() ? 0 : 1, S, k0, i0);
+    k_part_keys<<<grid, 256, 0, st>>>(u, v, N, m, n, G, is_distributed() ? 0 : 1, S, part_split, k0, i0);
     CK(cudaGetLastError());
     int bits = 1;
     while (bits < 32 && (1ull << bits) < (uint64_t)nb) bits++;
@@ -421,7 +421,11 @@ int mf_ctx::epoch_partitioned(mf_epoch_stats *stats) {
                 for (int g = 0; g < G; g++) next[g] = sigma(pn, G, g, 0);
             }
             for (int h = 0; h < 2; h++) {
-                if (recv_pending) CK(cudaStreamWaitEvent(st, ev_recv[h], 0));
+                if (recv_pending && part_split) CK(cudaStreamWaitEvent(st, ev_recv[h], 0));
+                if (recv_pending && !part_split && h == 0) {  // one launch over the whole segment: both halves
+                    CK(cudaStreamWaitEvent(st, ev_recv[0], 0));
+                    CK(cudaStreamWaitEvent(st, ev_recv[1], 0));
+                }
                 for (int li = 0; li < L; li++) {
                     const int g = is_distributed() ? rank : li;
                     const size_t b = blk(s, li, want[g], h);

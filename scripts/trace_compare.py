@@ -35,8 +35,10 @@ def main():
             name, opts = "partitioned", {"partitions": int(f[1])}
             if len(f) > 2 and f[2]:
                 opts["subepochs"] = int(f[2])
-            if len(f) > 3:  # partitioned:G:S:workers
+            if len(f) > 3 and f[3]:  # partitioned:G:S:workers
                 opts["workers"] = int(f[3])
+            if len(f) > 4:  # partitioned:G:S:workers:split
+                opts["part_split"] = int(f[4])
         with mf.MF(cfg.m, cfg.n, cfg.k, cfg.alpha, cfg.lam, cfg.seed_init, storage=a.storage, beta=cfg.beta,
                    seed_shuffle=cfg.seed_shuffle, **opts) as g:
             g.load(u, v, r)

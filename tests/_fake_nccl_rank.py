@@ -1,7 +1,7 @@
 """One rank of the multi-process partitioned run used by tests/test_gpu_nccl_fake.py.
 
 Runs under LD_PRELOAD=libfakenccl.so (tests/fake_nccl/), so several ranks can share one GPU.
-argv: rank world uid_file data.npz out_prefix epochs
+argv: rank world uid_file data.npz out_prefix epochs [part_split]
 """
 import os
 import sys
@@ -13,7 +13,8 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
 
 def main():
-    rank, world, uid_file, data, out, epochs = sys.argv[1:]
+    rank, world, uid_file, data, out, epochs = sys.argv[1:7]
+    split = int(sys.argv[7]) if len(sys.argv) > 7 else 0
     rank, world, epochs = int(rank), int(world), int(epochs)
     from paper_1610_05838_b200 import mf
     d = np.load(data)
@@ -31,7 +32,8 @@ def main():
         while not os.path.exists(uid_file):
             time.sleep(0.01)
         uid = open(uid_file, "rb").read()
-    g = mf.MF(m, n, k, alpha, lam, seed, beta=beta, seed_shuffle=seed_sh, workers=1, count_updates=1)
+    g = mf.MF(m, n, k, alpha, lam, seed, beta=beta, seed_shuffle=seed_sh, workers=1, count_updates=1,
+              part_split=split)
     mf.mf_attach_nccl(g.h, uid, rank, world)
     pb, pe = mf.mf_segment(m, world, rank)
     mine = (u >= pb) & (u < pe)

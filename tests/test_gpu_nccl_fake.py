@@ -3,8 +3,8 @@
 Real NCCL refuses two ranks on one device, and this environment gives one GPU per box, so the ranks
 run with tests/fake_nccl (LD_PRELOAD), a host-staged stand-in for the NCCL calls libmf makes
 (grouped send/recv, all-gather, all-reduce) that keeps their pairing and stream-ordering semantics.
-Everything else is the production path: mf_attach_nccl, local-row layout, pipelined half-segment
-hand-over on the comm stream, collective mf_rmse / mf_get_factors.  With one worker per block the
+Everything else is the production path: mf_attach_nccl, local-row layout, the hand-over on the comm
+stream (whole blocks, and the pipelined half-segment form), collective mf_rmse / mf_get_factors.  With one worker per block the
 run must equal the serial oracle over the (epoch, pass, round, rank, half) order reconstructed from
 the ranks' stored orders and libmf's round schedule.
 """
@@ -31,8 +31,8 @@ def fake_nccl(tmp_path_factory):
     return str(out)
 
 
-@pytest.mark.parametrize("G", [2, 3])
-def test_multirank_partitioned_matches_oracle_block_sweep(fake_nccl, tmp_path, G):
+@pytest.mark.parametrize("G,split", [(2, 0), (3, 0), (2, 1), (3, 1)])
+def test_multirank_partitioned_matches_oracle_block_sweep(fake_nccl, tmp_path, G, split):
     from paper_1610_05838_b200 import mf
     cfg = datagen.CONFIGS["C1"]
     (u, v, r), (tu, tv, tr) = datagen.make(cfg)
@@ -43,7 +43,7 @@ def test_multirank_partitioned_matches_oracle_block_sweep(fake_nccl, tmp_path, G
     uid_file, out = str(tmp_path / "uid"), str(tmp_path / "out")
     env = dict(os.environ, LD_PRELOAD=fake_nccl, PYTHONPATH=os.path.dirname(HERE))
     procs = [subprocess.Popen([sys.executable, os.path.join(HERE, "_fake_nccl_rank.py"), str(g), str(G), uid_file,
-                               str(data), out, str(E)], env=env) for g in range(G)]
+                               str(data), out, str(E), str(split)], env=env) for g in range(G)]
     try:
         rcs = [p.wait(timeout=300) for p in procs]
     finally:
@@ -69,7 +69,7 @@ def test_multirank_partitioned_matches_oracle_block_sweep(fake_nccl, tmp_path, G
                     pos = np.arange(len(o))
                     c = mf.mf_round_segment(cfg.seed_shuffle, e * S + s, G, rnd, g)
                     mid = cs[c][0] + (cs[c][1] - cs[c][0]) // 2
-                    for lo, hi in ((cs[c][0], mid), (mid, cs[c][1])):
+                    for lo, hi in (((cs[c][0], mid), (mid, cs[c][1])) if split else ((cs[c][0], cs[c][1]),)):
                         sel = ((pos * S) // len(o) == s) & (v[o] >= lo) & (v[o] < hi)
                         order.append(o[sel])
         order = np.concatenate(order)

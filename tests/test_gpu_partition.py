@@ -19,9 +19,10 @@ def mf():
     return mf
 
 
-def _block_sweep_order(mf, perm, u, v, m, n, G, seed, e, S=4):
+def _block_sweep_order(mf, perm, u, v, m, n, G, seed, e, S=4, split=0):
     """Caller indices in processing order: pass s (stored positions [s N/S, (s+1) N/S)) -> round ->
-    partition -> block samples in stored order; pass s of epoch e uses Latin square e*S + s."""
+    partition -> block samples in stored order (split = 1: the lower half of the block's columns, then
+    the upper half); pass s of epoch e uses Latin square e*S + s."""
     us, vs = u[perm], v[perm]
     N = len(perm)
     pas = (np.arange(N) * S) // N
@@ -33,21 +34,22 @@ def _block_sweep_order(mf, perm, u, v, m, n, G, seed, e, S=4):
             for g in range(G):
                 c = mf.mf_round_segment(seed, e * S + s, G, rnd, g)
                 mid = cs[c][0] + (cs[c][1] - cs[c][0]) // 2  # lower half first, then upper half
-                for lo, hi in ((cs[c][0], mid), (mid, cs[c][1])):
+                for lo, hi in (((cs[c][0], mid), (mid, cs[c][1])) if split else ((cs[c][0], cs[c][1]),)):
                     sel = (pas == s) & (us >= rs[g][0]) & (us < rs[g][1]) & (vs >= lo) & (vs < hi)
                     out.append(perm[np.nonzero(sel)[0]])
     return np.concatenate(out)
 
 
+@pytest.mark.parametrize("split", [0, 1])
 @pytest.mark.parametrize("G", [1, 2, 3, 4])
 @pytest.mark.parametrize("storage", [0, 1])
-def test_loopback_serial_blocks_match_oracle_block_sweep(mf, G, storage):
+def test_loopback_serial_blocks_match_oracle_block_sweep(mf, G, storage, split):
     cfg = datagen.CONFIGS["C1"]
     (u, v, r), test = datagen.make(cfg)
     E = 2
     st = {0: oracle.F32, 1: oracle.F16}[storage]
     with mf.MF(cfg.m, cfg.n, cfg.k, cfg.alpha, cfg.lam, cfg.seed_init, storage=storage, beta=cfg.beta,
-               seed_shuffle=cfg.seed_shuffle, partitions=G, workers=1, count_updates=1) as g:
+               seed_shuffle=cfg.seed_shuffle, partitions=G, workers=1, count_updates=1, part_split=split) as g:
         g.load(u, v, r)
         perm = g.order()
         for _ in range(E):
@@ -58,7 +60,7 @@ def test_loopback_serial_blocks_match_oracle_block_sweep(mf, G, storage):
     ref = oracle.Model(cfg.m, cfg.n, cfg.k, st, seed=cfg.seed_init)
     for e in range(E):
         ref.epoch(u, v, r, oracle.eta(cfg.alpha, cfg.beta, e), cfg.lam,
-                  _block_sweep_order(mf, perm, u, v, cfg.m, cfg.n, G, cfg.seed_shuffle, e))
+                  _block_sweep_order(mf, perm, u, v, cfg.m, cfg.n, G, cfg.seed_shuffle, e, split=split))
     Pr, Qr = ref.factors_f32()
     tol = {0: 1e-5, 1: 2e-3}[storage]
     assert np.linalg.norm(P - Pr) / np.linalg.norm(Pr) <= tol
