@@ -236,8 +236,8 @@ int mf_ctx::build_partition() {
     cudaStream_t st = stream();
     // passes per epoch: auto = 4.  Serial block-sweep simulation on C2-1pct, 10 epochs, test RMSE vs
     // the shuffled serial order: S = 1 costs +10..+20%; S = 4 is within 0.05% for G <= 4 and +0.37% at
-    // G = 8 (S = 8: 0.00%).  Every pass costs 2G launches (~40 us fixed each at this size), so the
-    // throughput default is 4; MF_OPT_SUBEPOCHS = G buys the last 0.4% at G = 8.
+    // G = 8 (S = 8: 0.00%).  Every pass costs G launches (2G with MF_OPT_PART_SPLIT = 1; ~35 us fixed
+    // each at this size), so the throughput default is 4.
     const int S_req = subepochs > 0 ? subepochs : 4;
     const int S = (int)std::max<int64_t>(1, std::min<int64_t>(S_req, std::max<int64_t>(1, N)));
     const int64_t nb = (int64_t)S * local * G * 2;
