@@ -28,8 +28,10 @@ def main():
     cfg = datagen.CONFIGS[a.cfg]
     (u, v, r), test = datagen.make(cfg)
     for sch in a.scheds.split(","):
-        opts = {"wave_cta": 1} if sch == "wavefront_cta" else {}
-        name = "wavefront" if sch == "wavefront_cta" else sch
+        opts = {"wave_cta": 1} if sch.startswith("wavefront_cta") else {}
+        name = "wavefront" if sch.startswith("wavefront_cta") else sch
+        if sch.startswith("wavefront_cta:"):  # wavefront_cta:c -- c column groups
+            opts["wave_cols"] = int(sch.split(":")[1])
         if sch.startswith("partitioned:"):  # loopback partitions, e.g. partitioned:8 or partitioned:8:16 (S)
             f = sch.split(":")
             name, opts = "partitioned", {"partitions": int(f[1])}
