@@ -243,36 +243,46 @@ def _c2_1pct_oracle_trace(storage, epochs):
 def test_netflix_slice_hogwild_l2_prefetch(mfmod, storage, pf):
     """The L2 row prefetch of batch-Hogwild! (MF_OPT_VARIANT bits 16..19) only moves cache lines: every
     setting processes each sample exactly once and lands within 0.5% of the serial oracle (C2-1pct,
-    k = 128 full-row shape, 10 epochs as in the test above)."""
+    k = 128 full-row shape, 10 epochs as in the test above; median of 3 runs, see _hogwild_median)."""
     cfg = datagen.CONFIGS["C2-1pct"]
     (u, v, r), test = datagen.make(cfg)
     E = 10
     trace = _c2_1pct_oracle_trace(storage, E)
-    with _gpu(mfmod, cfg, storage, count_updates=1, variant=pf << 16) as g:
-        g.load(u, v, r)
-        for _ in range(E):
-            st = g.epoch("hogwild")
-            assert st.updates == len(u)
-        got = g.rmse(*test)
-        assert (int(g.get(mfmod.MF_OPT_VARIANT)) >> 16) & 0xF == pf
+    got = _hogwild_median(mfmod, cfg, storage, (u, v, r), test, E, variant=pf << 16,
+                          check=lambda g: (int(g.get(mfmod.MF_OPT_VARIANT)) >> 16) & 0xF == pf)
     assert abs(got - trace[-1]) <= 0.005 * trace[-1], (got, trace[-1])
+
+
+def _hogwild_median(mfmod, cfg, storage, train, test, E, reps=3, check=None, **opts):
+    """Median test RMSE of `reps` independent batch-Hogwild! runs (E epochs each, every one exactly once
+    per epoch).  Lock-free runs differ from run to run: on the 1% Netflix slice (178 columns) fp16
+    repeats spread -0.39..+0.29% around the serial oracle (scripts/hogwild_repeatability.py), so a
+    single run can touch a 0.5% gate that the schedule meets; the median of three does not."""
+    u, v, r = train
+    vals = []
+    for _ in range(reps):
+        with _gpu(mfmod, cfg, storage, count_updates=1, **opts) as g:
+            g.load(u, v, r)
+            for _ in range(E):
+                assert g.epoch("hogwild").updates == len(u)
+            vals.append(g.rmse(*test))
+            if check is not None:
+                assert check(g)
+    return float(np.median(vals))
 
 
 @pytest.mark.parametrize("k,storage", [(32, 0), (32, 1), (64, 0), (64, 1)])
 def test_netflix_slice_hogwild_small_k(mfmod, k, storage):
     """The k = 32 / 64 batch-Hogwild! shapes (16 lanes per rating, 4- / 8-byte vectors): exactly once per
-    epoch, test RMSE within 0.5% of the storage-matched serial oracle after 10 epochs (C2-1pct)."""
+    epoch, test RMSE within 0.5% of the storage-matched serial oracle after 10 epochs (C2-1pct; median
+    of 3 runs)."""
     cfg = datagen.CONFIGS["C2-1pct"].scaled(k=k)
     (u, v, r), test = datagen.make(cfg)
     order = oracle.shuffle_perm(cfg.seed_shuffle, len(u))
     E = 10
     _, trace = oracle.train(cfg.m, cfg.n, cfg.k, ORC[storage], cfg.seed_init, u, v, r, cfg.alpha, cfg.beta,
                             cfg.lam, E, order=order, test=test)
-    with _gpu(mfmod, cfg, storage, count_updates=1) as g:
-        g.load(u, v, r)
-        for _ in range(E):
-            assert g.epoch("hogwild").updates == len(u)
-        got = g.rmse(*test)
+    got = _hogwild_median(mfmod, cfg, storage, (u, v, r), test, E)
     assert abs(got - trace[-1]) <= 0.005 * trace[-1], (got, trace[-1])
 
 
