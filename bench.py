@@ -340,7 +340,8 @@ def main():
     if traffic:
         roof["frac_dram_measured_bytes"] = traffic / k_s / 1e9 / peak
         roof["dram_bytes_per_update_measured"] = traffic / N
-    ceil = load_pattern_ceiling(cfg, a.storage)
+    ceil = (load_pattern_ceiling(cfg, a.storage, p_only=(a.schedule == "wavefront_cta"))
+            if a.schedule in ("hogwild", "wavefront_cta") else None)
     if ceil:
         roof["pattern_ceiling_updates_per_s"] = ceil
         roof["frac_of_pattern_ceiling"] = (N / k_s) / ceil
