@@ -62,11 +62,17 @@ CONFIGS = {
                  seed_data=3, epochs=10),
     "C3-1pct": Config("C3-1pct", 10_010, 6_250, 2_528_003, 40_040, 128, 0.08, 0.2, 0.05, 0.1,
                       seed_data=3, epochs=10),
+    # Yahoo-shaped 10% slice: rows, columns and samples /10 -> same degrees as C3 (fp16 / fp32 goldens)
+    "C3-10pct": Config("C3-10pct", 100_099, 62_496, 25_280_028, 400_396, 128, 0.08, 0.2, 0.05, 0.1,
+                       seed_data=3, epochs=10),
     # configs[3]: Hugewiki-shaped
     "C4": Config("C4", 50_082_604, 39_781, 3_069_817_980, 31_327_899, 128, 0.08, 0.3, 0.03, 0.1,
                  seed_data=4, epochs=10),
     "C4-rows10": Config("C4-rows10", 5_008_260, 39_781, 306_981_798, 3_132_790, 128, 0.08, 0.3, 0.03, 0.1,
                         seed_data=4, epochs=10),
+    # rows and samples /100, n kept (per-segment c / n_seg of the partitioned path as at full size)
+    "C4-rows100": Config("C4-rows100", 500_826, 39_781, 30_698_180, 313_279, 128, 0.08, 0.3, 0.03, 0.1,
+                         seed_data=4, epochs=10),
     "C4-rows1000": Config("C4-rows1000", 50_083, 398, 3_069_818, 31_328, 128, 0.08, 0.3, 0.03, 0.1,
                           seed_data=4, epochs=10),
 }

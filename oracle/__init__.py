@@ -14,53 +14,74 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SO = os.path.join(_HERE, "liboracle.so")
+_SO_F16C = os.path.join(_HERE, "liboracle_f16c.so")
 _SRC = os.path.join(_HERE, "mf_oracle.cpp")
 _lib = None
+# ORACLE_F16C=1 (golden-writing scripts only): the same source built with -mf16c, so the host
+# compiler's _Float16 casts become the F16C instructions vcvtps2ph / vcvtph2ps (IEEE binary16
+# round-to-nearest-even under the default MXCSR, as the software routines are) -- ~4x faster fp16
+# epochs.  tests/test_oracle.py checks the two builds bit for bit (all 65,536 halves, sampled
+# fp32 patterns, and fp16 / bf16 epochs).  The default build, and every timing of the oracle,
+# stays the plain one.
+_USE_F16C = os.environ.get("ORACLE_F16C", "0") == "1"
 
 F32, F16, BF16, F64 = 0, 1, 2, 3
 STORAGE_DTYPE = {F32: np.float32, F16: np.uint16, BF16: np.uint16, F64: np.float64}
 STORAGE_NAME = {"f32": F32, "fp32": F32, "f16": F16, "fp16": F16, "bf16": BF16, "f64": F64}
 
 
-def build(force: bool = False) -> str:
-    if force or not os.path.exists(_SO) or os.path.getmtime(_SO) < os.path.getmtime(_SRC):
-        subprocess.check_call(["g++", "-O2", "-std=c++17", "-ffp-contract=off", "-fno-fast-math",
-                               "-fPIC", "-shared", "-o", _SO, _SRC])
-    return _SO
+def build(force: bool = False, f16c: bool = False) -> str:
+    so = _SO_F16C if f16c else _SO
+    if force or not os.path.exists(so) or os.path.getmtime(so) < os.path.getmtime(_SRC):
+        subprocess.check_call(["g++", "-O2", "-std=c++17", "-ffp-contract=off", "-fno-fast-math"]
+                              + (["-mf16c"] if f16c else []) + ["-fPIC", "-shared", "-o", so, _SRC])
+    return so
+
+
+def host_has_f16c() -> bool:
+    try:
+        with open("/proc/cpuinfo") as f:
+            return " f16c" in f.read()
+    except OSError:
+        return False
 
 
 def lib():
     global _lib
     if _lib is None:
-        build()
-        L = ctypes.CDLL(_SO)
-        c = ctypes
-        L.orc_lr.argtypes = [c.c_double, c.c_double, c.c_int32]; L.orc_lr.restype = c.c_double
-        L.orc_eta.argtypes = [c.c_double, c.c_double, c.c_int32]; L.orc_eta.restype = c.c_float
-        L.orc_f32_to_f16.argtypes = [c.c_float]; L.orc_f32_to_f16.restype = c.c_uint16
-        L.orc_f16_to_f32.argtypes = [c.c_uint16]; L.orc_f16_to_f32.restype = c.c_float
-        L.orc_f32_to_bf16.argtypes = [c.c_float]; L.orc_f32_to_bf16.restype = c.c_uint16
-        L.orc_bf16_to_f32.argtypes = [c.c_uint16]; L.orc_bf16_to_f32.restype = c.c_float
-        L.orc_splitmix64.argtypes = [c.c_uint64]; L.orc_splitmix64.restype = c.c_uint64
-        L.orc_init.argtypes = [c.c_uint64, c.c_int64, c.c_int32, c.c_uint32, c.c_int32, c.c_void_p]
-        L.orc_init.restype = None
-        L.orc_shuffle_perm.argtypes = [c.c_uint64, c.c_int64, c.c_void_p]; L.orc_shuffle_perm.restype = None
-        L.orc_epoch.argtypes = [c.c_int32, c.c_int32, c.c_void_p, c.c_void_p, c.c_void_p, c.c_void_p,
-                                c.c_void_p, c.c_void_p, c.c_int64, c.c_float, c.c_float]
-        L.orc_epoch.restype = c.c_int
-        L.orc_epoch_f64.argtypes = [c.c_int32, c.c_void_p, c.c_void_p, c.c_void_p, c.c_void_p,
-                                    c.c_void_p, c.c_void_p, c.c_int64, c.c_double, c.c_double]
-        L.orc_epoch_f64.restype = c.c_int
-        L.orc_rmse.argtypes = [c.c_int32, c.c_int32, c.c_void_p, c.c_void_p, c.c_void_p, c.c_void_p,
-                               c.c_void_p, c.c_int64]
-        L.orc_rmse.restype = c.c_double
-        L.orc_loss.argtypes = [c.c_int32, c.c_int32, c.c_void_p, c.c_void_p, c.c_void_p, c.c_void_p,
-                               c.c_void_p, c.c_int64, c.c_double]
-        L.orc_loss.restype = c.c_double
-        L.orc_waves.argtypes = [c.c_int64, c.c_int64, c.c_void_p, c.c_void_p, c.c_void_p, c.c_int64, c.c_void_p]
-        L.orc_waves.restype = c.c_int64
-        _lib = L
+        _lib = load(_USE_F16C and host_has_f16c())
     return _lib
+
+
+def load(f16c: bool = False):
+    """Load one build of the oracle (a fresh ctypes handle; f16c=True is the golden-writing build)."""
+    L = ctypes.CDLL(build(f16c=f16c))
+    c = ctypes
+    L.orc_lr.argtypes = [c.c_double, c.c_double, c.c_int32]; L.orc_lr.restype = c.c_double
+    L.orc_eta.argtypes = [c.c_double, c.c_double, c.c_int32]; L.orc_eta.restype = c.c_float
+    L.orc_f32_to_f16.argtypes = [c.c_float]; L.orc_f32_to_f16.restype = c.c_uint16
+    L.orc_f16_to_f32.argtypes = [c.c_uint16]; L.orc_f16_to_f32.restype = c.c_float
+    L.orc_f32_to_bf16.argtypes = [c.c_float]; L.orc_f32_to_bf16.restype = c.c_uint16
+    L.orc_bf16_to_f32.argtypes = [c.c_uint16]; L.orc_bf16_to_f32.restype = c.c_float
+    L.orc_splitmix64.argtypes = [c.c_uint64]; L.orc_splitmix64.restype = c.c_uint64
+    L.orc_init.argtypes = [c.c_uint64, c.c_int64, c.c_int32, c.c_uint32, c.c_int32, c.c_void_p]
+    L.orc_init.restype = None
+    L.orc_shuffle_perm.argtypes = [c.c_uint64, c.c_int64, c.c_void_p]; L.orc_shuffle_perm.restype = None
+    L.orc_epoch.argtypes = [c.c_int32, c.c_int32, c.c_void_p, c.c_void_p, c.c_void_p, c.c_void_p,
+                            c.c_void_p, c.c_void_p, c.c_int64, c.c_float, c.c_float]
+    L.orc_epoch.restype = c.c_int
+    L.orc_epoch_f64.argtypes = [c.c_int32, c.c_void_p, c.c_void_p, c.c_void_p, c.c_void_p,
+                                c.c_void_p, c.c_void_p, c.c_int64, c.c_double, c.c_double]
+    L.orc_epoch_f64.restype = c.c_int
+    L.orc_rmse.argtypes = [c.c_int32, c.c_int32, c.c_void_p, c.c_void_p, c.c_void_p, c.c_void_p,
+                           c.c_void_p, c.c_int64]
+    L.orc_rmse.restype = c.c_double
+    L.orc_loss.argtypes = [c.c_int32, c.c_int32, c.c_void_p, c.c_void_p, c.c_void_p, c.c_void_p,
+                           c.c_void_p, c.c_int64, c.c_double]
+    L.orc_loss.restype = c.c_double
+    L.orc_waves.argtypes = [c.c_int64, c.c_int64, c.c_void_p, c.c_void_p, c.c_void_p, c.c_int64, c.c_void_p]
+    L.orc_waves.restype = c.c_int64
+    return L
 
 
 def _p(a):

@@ -9,7 +9,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 SO = os.path.join(HERE, "libmf.so")
 SOURCES = ["mf_api.cu", "mf_kernels.cu", "mf_wavefront.cu", "mf_partition.cu", "mf_stream.cu"]
-HEADERS = ["mf_ctx.h", "mf_kernels.cuh", "sgd_core.cuh"]
+HEADERS = ["mf_ctx.h", "mf_kernels.cuh", "sgd_core.cuh", "mf_host_util.h"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2", "--expt-relaxed-constexpr",

@@ -143,6 +143,30 @@ void mf_ctx::drop_layouts() {
     part_valid = false;
 }
 
+// Each schedule other than batch-Hogwild! keeps its own reordered copy of R (12 B per sample: wave
+// order, wavefront blocks, partition blocks).  Only the schedule being run keeps its copy, so the
+// footprint is at most two copies of R (the stored order + one layout) whatever the call sequence.
+int mf_ctx::drop_other_layouts(int schedule) {
+    if (schedule != MF_SCHED_DETERMINISTIC && wu) {
+        dev_free(&wu);
+        dev_free(&wv);
+        dev_free(&wr);
+        dev_free(&wave_off);
+        nwaves = -1;
+    }
+    if (schedule != MF_SCHED_WAVEFRONT && fu) release_wavefront();
+    if (schedule != MF_SCHED_PARTITIONED && bu && !is_distributed()) {
+        const int rc = gather_q();  // the partitioned layout may hold the current Q in its segments
+        if (rc != MF_OK) return rc;
+        for (void *p : {(void *)bu, (void *)bv, (void *)br})
+            if (p) cudaFree(p);
+        bu = bv = nullptr;
+        br = nullptr;
+        part_valid = false;
+    }
+    return MF_OK;
+}
+
 void mf_ctx::release() {
     if (dev_ready) cudaSetDevice(device);
     drop_layouts();
@@ -150,9 +174,6 @@ void mf_ctx::release() {
     dev_free(&v);
     dev_free(&r);
     dev_free(&perm);
-    dev_free(&stg_u);
-    dev_free(&stg_v);
-    dev_free(&stg_r);
     dev_free(&tu);
     dev_free(&tv);
     dev_free(&tr);
@@ -354,44 +375,62 @@ extern "C" int mf_load_coo(mf_ctx *ctx, const int32_t *u, const int32_t *v, cons
     CK(cudaSetDevice(ctx->device));
     cudaStream_t st = ctx->stream();
     if (nnz != ctx->cap_n) {  // (re)allocate; buffers are reused by repeated loads of the same size
-        for (void **p : {(void **)&ctx->u, (void **)&ctx->v, (void **)&ctx->r, (void **)&ctx->perm,
-                         (void **)&ctx->stg_u, (void **)&ctx->stg_v, (void **)&ctx->stg_r})
+        for (void **p : {(void **)&ctx->u, (void **)&ctx->v, (void **)&ctx->r, (void **)&ctx->perm})
             if (*p) cudaFree(*p), *p = nullptr;
         ctx->cap_n = 0;
         ctx->perm_n = -1;
+        RC(ctx->gather_q());
+        ctx->drop_layouts();  // free cached schedule copies of R before the new arrays
         RC(dev_alloc(ctx, &ctx->u, nnz, "alloc u"));
         RC(dev_alloc(ctx, &ctx->v, nnz, "alloc v"));
         RC(dev_alloc(ctx, &ctx->r, nnz, "alloc r"));
         ctx->cap_n = nnz;
-    }
-    if (ctx->shuffle) {
-        RC(dev_alloc(ctx, &ctx->perm, nnz, "alloc perm"));
-        RC(dev_alloc(ctx, &ctx->stg_u, nnz, "alloc staging u"));
-        RC(dev_alloc(ctx, &ctx->stg_v, nnz, "alloc staging v"));
-        RC(dev_alloc(ctx, &ctx->stg_r, nnz, "alloc staging r"));
     }
     RC(ctx->gather_q());
     ctx->drop_layouts();
     ctx->pf_hogwild.reset(), ctx->pf_wave_cta.reset(), ctx->last_pf_pick = 0;  // a new workload re-runs the trials
     ctx->seg_valid = false;
     ctx->N = 0;
-    const cudaMemcpyKind kind = is_device_ptr(u) ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
-    // shuffle: stage the caller's order, then one fused gather + validate + rebase kernel writes the
-    // A-8 order; no shuffle: copy in place and run the same kernel as validate + rebase.
-    int32_t *su = ctx->shuffle ? ctx->stg_u : ctx->u, *sv = ctx->shuffle ? ctx->stg_v : ctx->v;
-    float *sr = ctx->shuffle ? ctx->stg_r : ctx->r;
-    CK(cudaMemcpyAsync(su, u, sizeof(int32_t) * nnz, kind, st));
-    CK(cudaMemcpyAsync(sv, v, sizeof(int32_t) * nnz, kind, st));
-    CK(cudaMemcpyAsync(sr, r, sizeof(float) * nnz, kind, st));
+    // Footprint (peak bytes per sample besides the caller's data): the A-8 permutation is computed
+    // first (64-bit keys double-buffered + indices: 24 B transient, 4 B kept for mf_get_order and
+    // repeated loads), then host inputs pass through a transient 12-B staging copy (device inputs are
+    // gathered straight from the caller's buffers): at most 12 (R) + 4 + 24 = 40 B per sample, i.e.
+    // 123 GB for the 3.07B-sample Hugewiki shape next to its 12.8-GB fp16 P.
     if (ctx->shuffle && !(ctx->perm_n == nnz && ctx->perm_seed == ctx->seed_shuffle)) {
         // the A-8 permutation depends only on (nnz, seed): computed once and cached
+        RC(dev_alloc(ctx, &ctx->perm, nnz, "alloc perm"));
         CK(launch_shuffle_perm(nnz, ctx->seed_shuffle, ctx->perm, st));
         ctx->perm_n = nnz;
         ctx->perm_seed = ctx->seed_shuffle;
     }
+    const bool dev_in = is_device_ptr(u) && is_device_ptr(v) && is_device_ptr(r);
+    const cudaMemcpyKind kind = dev_in ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+    // shuffle: one fused gather + validate + rebase kernel writes the A-8 order from the caller's device
+    // buffers or a transient staging copy of the host ones; no shuffle: copy in place and run the same
+    // kernel as validate + rebase.
+    const int32_t *su = u, *sv = v;
+    const float *sr = r;
+    int32_t *tmp_u = nullptr, *tmp_v = nullptr;
+    float *tmp_r = nullptr;
+    if (!ctx->shuffle) {
+        CK(cudaMemcpyAsync(ctx->u, u, sizeof(int32_t) * nnz, kind, st));
+        CK(cudaMemcpyAsync(ctx->v, v, sizeof(int32_t) * nnz, kind, st));
+        CK(cudaMemcpyAsync(ctx->r, r, sizeof(float) * nnz, kind, st));
+        su = ctx->u, sv = ctx->v, sr = ctx->r;
+    } else if (!dev_in) {
+        CK(cudaMallocAsync((void **)&tmp_u, sizeof(int32_t) * nnz, st));
+        CK(cudaMallocAsync((void **)&tmp_v, sizeof(int32_t) * nnz, st));
+        CK(cudaMallocAsync((void **)&tmp_r, sizeof(float) * nnz, st));
+        CK(cudaMemcpyAsync(tmp_u, u, sizeof(int32_t) * nnz, kind, st));
+        CK(cudaMemcpyAsync(tmp_v, v, sizeof(int32_t) * nnz, kind, st));
+        CK(cudaMemcpyAsync(tmp_r, r, sizeof(float) * nnz, kind, st));
+        su = tmp_u, sv = tmp_v, sr = tmp_r;
+    }
     CK(cudaMemsetAsync(ctx->scratch, 0, sizeof(DevScratch), st));
     CK(launch_gather_validate(su, sv, sr, ctx->shuffle ? ctx->perm : nullptr, nnz, ctx->p_begin, ctx->p_end, ctx->n,
                               ctx->u, ctx->v, ctx->r, ctx->scratch, st));
+    for (void *p : {(void *)tmp_u, (void *)tmp_v, (void *)tmp_r})
+        if (p) CK(cudaFreeAsync(p, st));
     CK(cudaMemcpyAsync(ctx->h_scratch, ctx->scratch, sizeof(DevScratch), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     if (ctx->h_scratch->bad)
@@ -413,17 +452,23 @@ int mf_ctx::reshuffle() {
     mf_ctx *ctx = this;
     cudaStream_t st = stream();
     uint32_t *p2 = nullptr, *p3 = nullptr;
+    int32_t *nu = nullptr, *nv = nullptr;
+    float *nr = nullptr;
     CK(cudaMallocAsync((void **)&p2, sizeof(uint32_t) * N, st));
     CK(cudaMallocAsync((void **)&p3, sizeof(uint32_t) * N, st));
     CK(launch_shuffle_perm(N, seed_shuffle ^ ((uint64_t)(uint32_t)epoch << 48), p2, st));
-    CK(launch_gather(u, v, r, p2, N, stg_u, stg_v, stg_r, st));
     CK(launch_compose(perm, p2, p3, N, st));
     CK(cudaMemcpyAsync(perm, p3, sizeof(uint32_t) * N, cudaMemcpyDeviceToDevice, st));
-    CK(cudaFreeAsync(p2, st));
     CK(cudaFreeAsync(p3, st));
-    std::swap(u, stg_u);
-    std::swap(v, stg_v);
-    std::swap(r, stg_r);
+    // gather into transient arrays, then back into the resident ones (no second resident copy of R)
+    CK(cudaMallocAsync((void **)&nu, sizeof(int32_t) * N, st));
+    CK(cudaMallocAsync((void **)&nv, sizeof(int32_t) * N, st));
+    CK(cudaMallocAsync((void **)&nr, sizeof(float) * N, st));
+    CK(launch_gather(u, v, r, p2, N, nu, nv, nr, st));
+    CK(cudaMemcpyAsync(u, nu, sizeof(int32_t) * N, cudaMemcpyDeviceToDevice, st));
+    CK(cudaMemcpyAsync(v, nv, sizeof(int32_t) * N, cudaMemcpyDeviceToDevice, st));
+    CK(cudaMemcpyAsync(r, nr, sizeof(float) * N, cudaMemcpyDeviceToDevice, st));
+    for (void *p : {(void *)p2, (void *)nu, (void *)nv, (void *)nr}) CK(cudaFreeAsync(p, st));
     perm_n = -1;  // perm no longer equals the load-time permutation
     RC(gather_q());
     drop_layouts();
@@ -568,6 +613,7 @@ static int epoch_local(mf_ctx *ctx, int schedule, mf_epoch_stats *stats) {
         if (ctx->reshuffle_due) RC(ctx->reshuffle());
         ctx->reshuffle_due = true;
     }
+    RC(ctx->drop_other_layouts(schedule));
     if (schedule == MF_SCHED_DETERMINISTIC) RC(ctx->build_waves());
     if (schedule == MF_SCHED_WAVEFRONT) RC(ctx->build_wavefront());
     if (schedule == MF_SCHED_PARTITIONED) return ctx->epoch_partitioned(stats);

@@ -86,8 +86,6 @@ struct mf_ctx {
     int64_t perm_n = -1;       // perm is the A-8 permutation of perm_n samples under perm_seed (cached)
     bool reshuffle_due = false;  // MF_OPT_SHUFFLE = 2: permute again before the next epoch
     uint64_t perm_seed = 0;
-    int32_t *stg_u = nullptr, *stg_v = nullptr;  // staging copy of the caller's order (shuffle on)
-    float *stg_r = nullptr;
     int64_t N = 0, cap_n = 0;
     int shuffled = 0;
 
@@ -164,6 +162,7 @@ struct mf_ctx {
     int copy_out(const void *X, int64_t count, float *dst);
     int copy_in(void *X, int64_t count, const float *src);
     void drop_layouts();
+    int drop_other_layouts(int schedule);
     void release();
 
     // mf_wavefront.cu

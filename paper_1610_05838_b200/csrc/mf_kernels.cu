@@ -56,7 +56,6 @@ static cudaError_t dispatch_shape(const ShapeId &s, F &&f) {
 }
 
 ShapeId select_shape(int k, int storage, int variant) {
-    const int bytes = storage == kF32 ? 4 : 2;
     if (storage == kF32) {
         if (k == 128) {
             if (variant == 1) return {storage, 16, 2, 16, 1};
@@ -169,14 +168,20 @@ __global__ void __launch_bounds__(kBlock) k_hogwild(UpdateArgs a) {
     int64_t next_chunk = (nwarps + warp_id) * (int64_t)f;
     if (base >= N) return;
     int64_t end = min(base + len0, N);
+    // L2 eviction priorities: the triples are read once per epoch and would otherwise push P rows out
+    // of L2 (1.2 GB of R per epoch streams past a 123-MB P on the Netflix shape), so they are marked
+    // evict_first; optionally the factor rows evict_last (MF_OPT_VARIANT bits 28..29)
+    const uint64_t pol_r = a.cache_policy == 1 ? policy_evict_normal() : policy_evict_first();
+    const uint64_t pol_p = a.cache_policy == 2 ? policy_evict_last() : policy_evict_normal();
+    const uint64_t pol_q = a.cache_policy >= 2 ? policy_evict_last() : policy_evict_normal();
     int32_t tu, tv;
     float tr;
     {
         const int64_t i = base + lane;
         const bool ok = i < end;
-        tu = ok ? __ldg(a.u + i) : 0;
-        tv = ok ? __ldg(a.v + i) : 0;
-        tr = ok ? __ldg(a.r + i) : 0.f;
+        tu = ok ? ld_stream_s32(a.u + i, pol_r) : 0;
+        tv = ok ? ld_stream_s32(a.v + i, pol_r) : 0;
+        tr = ok ? ld_stream_f32(a.r + i, pol_r) : 0.f;
     }
     for (;;) {
         int64_t nbase = base + 32, nend = end;
@@ -191,15 +196,15 @@ __global__ void __launch_bounds__(kBlock) k_hogwild(UpdateArgs a) {
         {
             const int64_t i = nbase + lane;
             const bool ok = more && i < nend;
-            nu = ok ? __ldg(a.u + i) : 0;
-            nv = ok ? __ldg(a.v + i) : 0;
-            nr = ok ? __ldg(a.r + i) : 0.f;
+            nu = ok ? ld_stream_s32(a.u + i, pol_r) : 0;
+            nv = ok ? ld_stream_s32(a.v + i, pol_r) : 0;
+            nr = ok ? ld_stream_f32(a.r + i, pol_r) : 0.f;
         }
         {
             const int cnt = (int)(end - base < 32 ? end - base : 32);
             if (a.count_updates) done += (lane == 0) ? cnt : 0;
-#pragma unroll 1
             const int steps = (cnt + gper - 1) / gper < ntile ? (cnt + gper - 1) / gper : ntile;
+#pragma unroll 1
             for (int j0 = 0; j0 < steps; j0 += D) {
                 int32_t su[D], sv[D];
                 float sr[D];
@@ -244,8 +249,8 @@ __global__ void __launch_bounds__(kBlock) k_hogwild(UpdateArgs a) {
                 }
 #pragma unroll
                 for (int d = 0; d < D; d++) {
-                    load_row<SH>(a.P, su[d], k, sub, val[d], pr[d]);
-                    load_row<SH>(a.Q, sv[d], k, sub, val[d], qr[d]);
+                    load_row_pol<SH>(a.P, su[d], k, sub, val[d], pr[d], pol_p);
+                    load_row_pol<SH>(a.Q, sv[d], k, sub, val[d], qr[d], pol_q);
                 }
 #pragma unroll
                 for (int d = 0; d < D; d++) {
@@ -261,8 +266,8 @@ __global__ void __launch_bounds__(kBlock) k_hogwild(UpdateArgs a) {
                     sgd_step<SH>(pf[d], qf[d], err, a.eta, a.lam);
                     narrow_row<SH>(pf[d], pr[d]);
                     narrow_row<SH>(qf[d], qr[d]);
-                    store_row<SH>(a.P, su[d], k, sub, val[d], pr[d]);
-                    store_row<SH>(a.Q, sv[d], k, sub, val[d], qr[d]);
+                    store_row_pol<SH>(a.P, su[d], k, sub, val[d], pr[d], pol_p);
+                    store_row_pol<SH>(a.Q, sv[d], k, sub, val[d], qr[d], pol_q);
                 }
             }
         }
@@ -337,6 +342,7 @@ cudaError_t launch_hogwild(const ShapeId &sh, const UpdateArgs &a_in, int worker
         const int pf = (variant >> 16) & 0xF;  // bits 16..19: L2 row-prefetch distance in steps (0, 15 = off)
         a.prefetch = pf == 15 ? 0 : pf;
         a.prefetch_kind = (variant >> 20) & 0x3;  // bits 20..21: 1 = P rows only, 2 = per-lane prefetch
+        a.cache_policy = (variant >> 28) & 0x3;   // bits 28..29: L2 eviction priorities (UpdateArgs)
     }
     return dispatch_shape(sh, [&](auto tag) -> cudaError_t {
         using SH = decltype(tag);

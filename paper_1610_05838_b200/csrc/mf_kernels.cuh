@@ -39,6 +39,9 @@ struct UpdateArgs {
     const unsigned long long *abort_if;  // optional: the kernel does nothing if *abort_if != 0
     int prefetch;       // batch-Hogwild!: L2-prefetch the rows of the rating this many steps ahead (0 = off)
     int prefetch_kind;  // bit 0: P rows only; bit 1: per-lane prefetch.global.L2 instead of one bulk prefetch
+    int cache_policy;   // L2 eviction priorities (MF_OPT_VARIANT bits 28..29, resolved): 0 = R evict_first,
+                        // 1 = none (plain loads), 2 = R evict_first + P/Q rows evict_last, 3 = R evict_first +
+                        // Q rows evict_last
 };
 
 // Kernel-shape choice for (k, storage); filled by select_shape().

@@ -219,6 +219,12 @@ int mf_ctx::build_partition() {
     if (G > n || G > p_rows() * (is_distributed() ? world : 1))
         return fail(MF_EINVAL, "partitioned: G = %d exceeds the matrix dimensions", G);
     const int local = is_distributed() ? 1 : G;
+    // A previous layout may still hold the only current copy of Q in its segment buffers (an option
+    // that changes the layout was set between partitioned epochs): bring it home before freeing them.
+    if (seg_valid && !full_valid) {
+        const int rc = gather_q();
+        if (rc != MF_OK) return rc;
+    }
     if (comm_stream) cudaStreamSynchronize(comm_stream);  // no hand-over may still target old buffers
     recv_pending = false;
     // free a previous layout's buffers (keep the NCCL comm)

@@ -47,6 +47,17 @@ struct Vec<16> {
         __stcg(reinterpret_cast<uint4 *>(p), make_uint4(w[0], w[1], w[2], w[3]));
     }
 };
+// the same 16-B accesses with an L2 eviction-priority policy (createpolicy), still .cg (L2-coherent)
+__device__ __forceinline__ void ld16_pol(const void *p, uint32_t (&w)[4], uint64_t pol) {
+    asm volatile("ld.global.cg.L2::cache_hint.v4.u32 {%0, %1, %2, %3}, [%4], %5;"
+                 : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3])
+                 : "l"(p), "l"(pol));
+}
+__device__ __forceinline__ void st16_pol(void *p, const uint32_t (&w)[4], uint64_t pol) {
+    asm volatile("st.global.cg.L2::cache_hint.v4.u32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(p), "r"(w[0]), "r"(w[1]),
+                 "r"(w[2]), "r"(w[3]), "l"(pol)
+                 : "memory");
+}
 template <>
 struct Vec<8> {
     static constexpr int NW = 2;
@@ -198,6 +209,70 @@ __device__ __forceinline__ void load_row(const void *base, int64_t row, int k, i
             for (int i = 0; i < SH::NW; i++) out.w[j][i] = 0u;
         }
     }
+}
+
+// load_row / store_row with an L2 policy (16-B full-row shapes; other shapes ignore the policy)
+template <class SH>
+__device__ __forceinline__ void load_row_pol(const void *base, int64_t row, int k, int sub, bool valid,
+                                             RowRaw<SH> &out, uint64_t pol) {
+    if constexpr (SH::VB == 16 && SH::FULL) {
+        const char *rp = reinterpret_cast<const char *>(base) + row * (int64_t)k * SH::BYTES;
+#pragma unroll
+        for (int j = 0; j < SH::V; j++) {
+            if (valid) {
+                ld16_pol(rp + vec_elem<SH>(j, sub) * SH::BYTES, out.w[j], pol);
+            } else {
+#pragma unroll
+                for (int i = 0; i < SH::NW; i++) out.w[j][i] = 0u;
+            }
+        }
+    } else {
+        load_row<SH>(base, row, k, sub, valid, out);
+    }
+}
+
+template <class SH>
+__device__ __forceinline__ void store_row(void *base, int64_t row, int k, int sub, bool valid, const RowRaw<SH> &in);
+
+template <class SH>
+__device__ __forceinline__ void store_row_pol(void *base, int64_t row, int k, int sub, bool valid,
+                                              const RowRaw<SH> &in, uint64_t pol) {
+    if constexpr (SH::VB == 16 && SH::FULL) {
+        char *rp = reinterpret_cast<char *>(base) + row * (int64_t)k * SH::BYTES;
+#pragma unroll
+        for (int j = 0; j < SH::V; j++)
+            if (valid) st16_pol(rp + vec_elem<SH>(j, sub) * SH::BYTES, in.w[j], pol);
+    } else {
+        store_row<SH>(base, row, k, sub, valid, in);
+    }
+}
+
+// L2 eviction-priority policies (fraction 1.0: every access of the instruction gets the priority)
+__device__ __forceinline__ uint64_t policy_evict_first() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_last() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_normal() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+// streamed read-only words (the COO triples): non-coherent path, no L1 allocation, L2 policy
+__device__ __forceinline__ int32_t ld_stream_s32(const int32_t *p, uint64_t pol) {
+    int32_t x;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.b32 %0, [%1], %2;" : "=r"(x) : "l"(p), "l"(pol));
+    return x;
+}
+__device__ __forceinline__ float ld_stream_f32(const float *p, uint64_t pol) {
+    float x;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(x) : "l"(p), "l"(pol));
+    return x;
 }
 
 template <class SH>

@@ -307,6 +307,42 @@ def test_p8_bf16_exhaustive_roundtrip_and_rne():
     assert math.isnan(L.orc_bf16_to_f32(L.orc_f32_to_bf16(float("nan"))))
 
 
+@pytest.mark.skipif(not oracle.host_has_f16c(), reason="host CPU has no F16C")
+def test_f16c_golden_build_is_bitwise_the_plain_build():
+    """The golden-writing build (-mf16c: hardware vcvtps2ph / vcvtph2ps for the _Float16 casts) gives
+    the plain build's bits: every binary16 pattern widened, sampled fp32 patterns (ties, subnormal
+    and overflow ranges) narrowed, and whole fp16 / bf16 epochs on C1 plus the test RMSE."""
+    A, B = oracle.load(False), oracle.load(True)
+    for h in range(65536):
+        x, y = A.orc_f16_to_f32(h), B.orc_f16_to_f32(h)
+        assert (x == y) or (math.isnan(x) and math.isnan(y)), h
+    rng = np.random.default_rng(3)
+    bits = np.concatenate([rng.integers(0, 2 ** 32, 60000, dtype=np.uint64).astype(np.uint32),
+                           (np.arange(0x33000000, 0x47800000, 0x1001, dtype=np.uint32))])
+    xs = bits.view(np.float32)
+    for x in xs[np.isfinite(xs)]:
+        assert A.orc_f32_to_f16(float(x)) == B.orc_f32_to_f16(float(x)), float(x)
+    cfg = datagen.CONFIGS["C1"]
+    (u, v, r), (tu, tv, tr) = datagen.make(cfg)
+    order = oracle.shuffle_perm(cfg.seed_shuffle, len(u))
+    c = oracle._c
+    u, v, r, tu, tv, tr, order = (c(u, np.int32), c(v, np.int32), c(r, np.float32), c(tu, np.int32),
+                                  c(tv, np.int32), c(tr, np.float32), c(order, np.int64))
+    for st in (F16, BF16):
+        fac = []
+        for L in (A, B):
+            P, Q = oracle.init(cfg.seed_init, cfg.m, cfg.k, 0, st), oracle.init(cfg.seed_init, cfg.n, cfg.k, 1, st)
+            for t in range(3):
+                assert L.orc_epoch(cfg.k, st, P.ctypes.data, Q.ctypes.data, u.ctypes.data, v.ctypes.data,
+                                   r.ctypes.data, order.ctypes.data, len(u), oracle.eta(cfg.alpha, cfg.beta, t),
+                                   cfg.lam) == 0
+            fac.append((P, Q, L.orc_rmse(cfg.k, st, P.ctypes.data, Q.ctypes.data, tu.ctypes.data, tv.ctypes.data,
+                                         tr.ctypes.data, len(tu))))
+        np.testing.assert_array_equal(fac[0][0], fac[1][0])
+        np.testing.assert_array_equal(fac[0][1], fac[1][1])
+        assert fac[0][2] == fac[1][2]
+
+
 # ------------------------------------------------------- init / shuffle -----
 def test_splitmix64_published_vectors():
     """SplitMix64 (Steele, Lea, Flood 2014) from state 1234567: Vigna's reference sequence."""
