@@ -1,5 +1,6 @@
 """Benchmark: SGD updates/s of the batch-Hogwild! epoch (PAPER.md:207 metric) on the Netflix-shaped
-synthetic workload (BASELINE.json configs[1]), k = 128, on one B200 (or G B200s, partitioned).
+synthetic workload (BASELINE.json configs[1]), k = 128, on one B200; with --gpus N > 1 the partitioned
+path on the Hugewiki-shaped workload split over the N GPUs (BASELINE.json configs[3], strong scaling).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
                     [--storage f16|f32|bf16] [--config C2] [--schedule hogwild|wavefront_cta|...]
@@ -11,7 +12,10 @@ the test-RMSE evaluation, both in libmf.so's kernels.  Prints ONE
 from pinned HOST buffers (batch-Hogwild!: mf_epoch_host streams R from host memory every step, H2D
 overlapped with the update kernel; other schedules: mf_load_coo H2D + validation + A-8 shuffle,
 mf_epoch), then mf_rmse with the test set from host memory and the result D2H.
-N > 1 (torchrun): the partitioned path with NCCL Q rotation, one process per GPU, max-over-ranks time.
+N > 1 (torchrun): the partitioned path with NCCL Q rotation, one process per GPU, max-over-ranks time
+(defaults: --config C4 --scaling strong --storage f16).  N = 1 also runs, in `other_runs`, the other
+storage, the CTA wavefront and deterministic schedules on the same workload, and the Hugewiki shape on
+this one GPU (batch-Hogwild!, CTA wavefront and the 1-partition partitioned path; --no-c4 skips it).
 `--impl reference` times the CPU oracle (the only reference this paper-only task has) on a bounded
 sample of the same workload.
 """
@@ -43,6 +47,74 @@ def peaks():
         return float(p["hbm_gbs"]), "measured"
     except Exception:
         return HBM_FALLBACK_GBS, "fallback"
+
+
+def l2_peaks(row_bytes):
+    """Measured L2 ceilings (scripts/l2_ceiling.cu on a B200, profiles/r02_l2_ceiling.jsonl): the best
+    random-row read-modify-write bandwidth for rows of `row_bytes` resident in L2 (the update kernels'
+    own L2 access shape) and the best contiguous read+write bandwidth; (None, None) if absent."""
+    rows, stream = None, None
+    try:
+        with open(os.path.join(ROOT, "profiles", "r02_l2_ceiling.jsonl")) as f:
+            for line in f:
+                d = json.loads(line)
+                if d.get("pattern") == "rows_rw" and d.get("row_bytes") == row_bytes:
+                    rows = max(rows or 0.0, d["GBps"])
+                elif d.get("pattern") == "stream_rw":
+                    stream = max(stream or 0.0, d["GBps"])
+    except Exception:
+        pass
+    return rows, stream
+
+
+def cpu_info():
+    model = "unknown"
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return model, os.cpu_count()
+
+
+SHAPE_NAME = {"C1": "planted rank-8 parity config", "C2": "Netflix-shaped", "C3": "Yahoo!Music-shaped",
+              "C4": "Hugewiki-shaped"}
+
+
+def roofline(cfg, storage, N, k_s, traffic, schedule):
+    """Roofline object of the update kernel.  Its algorithmic bytes B_alg = 12 + 4kb per update (SURVEY
+    §8(d)) all pass through L2 (triple, p_u and q_v read, both rows written; the CTA wavefront keeps q_v on
+    chip, so 12 + 2kb reach L2), so the primary bound is the L2's measured ceiling for random-row
+    read-modify-write; `hbm` relates the DRAM bytes (ncu, per launch, when captured for this config) or,
+    failing that, the compulsory 12 + 2kb (R stream + P rows; Q is L2-resident at every configured shape)
+    to the measured HBM copy peak."""
+    b = 4 if storage == "f32" else 2
+    hbm, hbm_kind = peaks()
+    on_chip_q = schedule == "wavefront_cta"
+    B = b_alg(cfg.k, storage)
+    B_l2 = 12 + 2 * cfg.k * b if on_chip_q else B
+    l2_rows, l2_stream = l2_peaks(cfg.k * b)
+    b_hbm = 12 + 2 * cfg.k * b
+    roof = {"bound": "l2" if l2_rows else "hbm", "achieved": B_l2 * N / k_s / 1e9,
+            "peak": l2_rows if l2_rows else hbm, "unit": "GB/s", "traffic": traffic,
+            "peak_kind": ("measured L2 random-row RMW ceiling, %d-B rows (scripts/l2_ceiling.cu, "
+                          "profiles/r02_l2_ceiling.jsonl)" % (cfg.k * b)) if l2_rows else hbm_kind,
+            "bytes_per_update_alg": B, "bytes_per_update_l2": B_l2, "updates_per_launch": N,
+            "kernel_ms": k_s * 1e3}
+    roof["frac"] = roof["achieved"] / roof["peak"]
+    if l2_stream:
+        roof["l2_stream_rw_peak"] = l2_stream
+    dram = traffic / N if traffic else b_hbm
+    roof["hbm"] = {"achieved": dram * N / k_s / 1e9, "peak": hbm, "peak_kind": hbm_kind, "unit": "GB/s",
+                   "frac": dram * N / k_s / 1e9 / hbm, "bytes_per_update": dram,
+                   "basis": "ncu dram__bytes_read+write of one launch" if traffic else
+                            "compulsory 12 + 2kb (R + P rows; Q L2-resident)",
+                   "frac_compulsory": b_hbm * N / k_s / 1e9 / hbm,
+                   "frac_alg_bytes": B * N / k_s / 1e9 / hbm}
+    return roof
 
 
 def b_alg(k, storage):
@@ -102,12 +174,14 @@ class Clocks:
                 "reasons": sorted(reasons), "samples": len(self.rows)}
 
 
-def load_traffic(storage, cfgname):
-    """ncu dram bytes per launch of the update kernel, from the committed profile summary (or None)."""
+def load_traffic(storage, cfgname, schedule="hogwild"):
+    """ncu dram bytes per launch of the update kernel for this (config, storage, schedule), from the
+    committed profile summary profiles/ncu_summary.json (or None)."""
+    key = f"{cfgname}/{storage}" if schedule == "hogwild" else f"{cfgname}-wfcta/{storage}"
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as f:
             d = json.load(f)
-        return d["kernels"][f"{cfgname}/{storage}"]["dram_bytes_per_launch"]
+        return d["kernels"][key]["dram_bytes_per_launch"]
     except Exception:
         return None
 
@@ -175,7 +249,8 @@ def run_reference(a, cfg):
            "impl": "reference",
            "config": workload_config(cfg, G, a.storage, a.schedule if G == 1 else "partitioned", a.scaling),
            "arm": {"what": "serial C++ oracle (oracle/mf_oracle.cpp), 1 core", "sample_per_step": sample},
-           "cpu_baseline": {"value": val, "unit": "updates/s", "cores": 1, "kind": "oracle", "sample": desc},
+           "cpu_baseline": {"value": val, "unit": "updates/s", "cores": 1, "kind": "oracle", "sample": desc,
+                            "cpu_model": cpu_info()[0], "host_cpus": cpu_info()[1]},
            "e2e": {"value": val, "unit": "updates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out), flush=True)
 
@@ -201,8 +276,8 @@ def workload_config(cfg, G, storage, schedule, scaling="weak"):
     """The `config` object, identical for both arms of the same run."""
     b = 4 if storage == "f32" else 2
     if G == 1:
-        return {"workload": f"{cfg.name}: Netflix-shaped (PAPER.md Table 2) m={cfg.m} n={cfg.n} "
-                            f"N={cfg.n_train} k={cfg.k}, planted rank-8 synthetic ratings",
+        return {"workload": f"{cfg.name}: {SHAPE_NAME.get(cfg.name, cfg.name)} (PAPER.md Table 2) m={cfg.m} "
+                            f"n={cfg.n} N={cfg.n_train} k={cfg.k}, planted rank-8 synthetic ratings",
                 "schedule": schedule, "storage": storage, "alpha": cfg.alpha, "beta": cfg.beta, "lambda": cfg.lam,
                 "l2": "inputs larger than L2 (R %.2f GB, P %.0f MB); no flush" % (12 * cfg.n_train / 1e9,
                                                                                   cfg.m * cfg.k * b / 1e6),
@@ -210,9 +285,10 @@ def workload_config(cfg, G, storage, schedule, scaling="weak"):
     m_glob, n_tr, _ = partition_shape(cfg, G, scaling)
     what = ("one %s-shaped row segment per GPU (weak scaling)" % cfg.name if scaling == "weak" else
             "%s split into %d row segments (strong scaling)" % (cfg.name, G))
-    return {"workload": f"{cfg.name} partitioned over {G} GPUs: m={m_glob} n={cfg.n} N={n_tr * G} k={cfg.k}, "
-                        f"{what}; one global planted rank-8 model",
-            "schedule": "partitioned (S passes x G rounds of G x G Latin-square blocks, NCCL Q rotation)",
+    return {"workload": f"{cfg.name} ({SHAPE_NAME.get(cfg.name, cfg.name)}) partitioned over {G} GPUs: m={m_glob} "
+                        f"n={cfg.n} N={n_tr * G} k={cfg.k}, {what}; one global planted rank-8 model",
+            "schedule": "partitioned (S passes x G rounds; unit grid of 2G half-segment Q units, each family "
+                        "rotating by its own Latin square over NCCL send/recv, overlapped with the other's updates)",
             "storage": storage, "parallelism": f"P row segments x rotating Q segments over {G} GPUs",
             "alpha": cfg.alpha, "beta": cfg.beta, "lambda": cfg.lam, "l2": "inputs larger than L2; no flush",
             "step": "one epoch (mf_epoch partitioned) + test RMSE (mf_rmse, collective)"}
@@ -230,20 +306,32 @@ def cpu_baseline(cfg, storage, u, v, r, budget_s=12.0):
         m.epoch(u[done:done + n], v[done:done + n], r[done:done + n], eta, cfg.lam)
         t_all += time.perf_counter() - t0
         done += n
-    return {"value": done / t_all, "unit": "updates/s", "cores": 1, "kind": "oracle",
+    model, nproc = cpu_info()
+    return {"value": done / t_all, "unit": "updates/s", "cores": 1, "kind": "oracle", "cpu_model": model,
+            "host_cpus": nproc,
             "sample": f"first {done} samples of {cfg.name} in stored order, full-size P/Q, {storage} storage, "
-                      f"{t_all:.1f} s"}
+                      f"{t_all:.1f} s on 1 of {nproc} host CPUs ({model})"}
 
 
 # ---------------------------------------------------------------------- ours
+def resolve_defaults(a, world):
+    """N = 1: BASELINE.json configs[1] (Netflix shape, batch-Hogwild!, fp16 storage).  N > 1 (or
+    --partitioned): configs[3], the Hugewiki shape split over the N GPUs (strong scaling), fp16 storage."""
+    multi = world > 1 or a.partitioned
+    a.config = a.config or ("C4" if multi else "C2")
+    a.scaling = a.scaling or ("strong" if multi else "weak")
+    a.storage = a.storage or "f16"
+    return a
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--storage", default="f16", choices=["f16", "f32", "bf16"])
-    ap.add_argument("--config", default="C2")
+    ap.add_argument("--storage", default=None, choices=["f16", "f32", "bf16"])
+    ap.add_argument("--config", default=None, help="default C2 (one GPU), C4 (N > 1)")
     ap.add_argument("--schedule", default="hogwild",
                     choices=["hogwild", "wavefront", "wavefront_cta", "deterministic"])
     ap.add_argument("--workers", type=int, default=0)
@@ -254,10 +342,13 @@ def main():
     ap.add_argument("--partitioned", action="store_true",
                     help="run the multi-GPU (NCCL, partitioned) path even at one rank")
     ap.add_argument("--ref-sample", type=int, default=1_000_000)
-    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
-                    help="N > 1: weak = one --config-shaped row segment per GPU; strong = --config split over N")
+    ap.add_argument("--scaling", default=None, choices=["weak", "strong"],
+                    help="N > 1: strong (default) = --config split over N; weak = one --config-shaped row segment "
+                         "per GPU")
+    ap.add_argument("--no-c4", action="store_true", help="N = 1: skip the Hugewiki-shaped runs in other_runs")
     a = ap.parse_args()
     a.warmup = max(a.warmup, 3)
+    resolve_defaults(a, int(os.environ.get("WORLD_SIZE", "1")))
     cfg = datagen.CONFIGS[a.config]
 
     if a.impl == "reference":
@@ -322,24 +413,12 @@ def main():
     rmses = [head["rmse"]]
 
     # roofline of the dominant kernel (the update kernel): algorithmic bytes / its event-timed duration
-    peak, peak_kind = peaks()
     k_s = head["kernel_s"]
-    B = b_alg(cfg.k, a.storage)
-    achieved = B * N / k_s / 1e9
-    traffic = load_traffic(a.storage, cfg.name)
-    roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-            "traffic": traffic, "peak_kind": peak_kind, "kernel": "k_hogwild" if a.schedule == "hogwild" else
-            "k_" + a.schedule, "kernel_ms": k_s * 1e3, "kernel_share_of_step": k_s * 1e3 / ms,
-            "bytes_per_update_alg": B, "updates_per_launch": N,
-            "note": "frac > 1 is possible: Q (n*k*b = %.1f MB) stays L2-resident, so HBM carries ~12+2kb B/update"
-                    % (cfg.n * cfg.k * (4 if a.storage == "f32" else 2) / 1e6)}
-    # the same kernel against the bytes DRAM must move when Q is L2-resident (R + P read + P write), and
-    # against the DRAM bytes ncu measured for one launch (profiles/ncu_summary.json)
-    b_hbm = 12 + 2 * cfg.k * (4 if a.storage == "f32" else 2)
-    roof["frac_hbm_compulsory"] = b_hbm * N / k_s / 1e9 / peak
-    if traffic:
-        roof["frac_dram_measured_bytes"] = traffic / k_s / 1e9 / peak
-        roof["dram_bytes_per_update_measured"] = traffic / N
+    traffic = load_traffic(a.storage, cfg.name, a.schedule)
+    roof = roofline(cfg, a.storage, N, k_s, traffic, a.schedule)
+    roof.update({"kernel": "k_hogwild" if a.schedule == "hogwild" else "k_" + a.schedule,
+                 "kernel_share_of_step": k_s * 1e3 / ms})
+    peak = roof["hbm"]["peak"]
     ceil = (load_pattern_ceiling(cfg, a.storage, p_only=(a.schedule == "wavefront_cta"))
             if a.schedule in ("hogwild", "wavefront_cta") else None)
     if ceil:
@@ -357,14 +436,21 @@ def main():
                                     (f"deterministic/{a.storage}", a.storage, "deterministic", {})):
             res = measure(st_, sch, max(3, a.steps // 5), 3, **opts)
             res["alg_GBps"] = b_alg(cfg.k, st_) * N / res["kernel_s"] / 1e9
-            res["frac_alg"] = res["alg_GBps"] / peak
+            rf = roofline(cfg, st_, N, res["kernel_s"], load_traffic(st_, cfg.name, key.split("/")[0]),
+                          key.split("/")[0])
+            res["roofline_frac"] = rf["frac"]
+            res["roofline_bound"] = rf["bound"]
+            res["hbm_frac"] = rf["hbm"]["frac"]
             # against the memory-pattern ceiling of the kernel's own global traffic (p+q rows for
             # batch-Hogwild!, p rows only for the CTA wavefront whose Q group is on chip)
             ceil = load_pattern_ceiling(cfg, st_, p_only=(sch == "wavefront")) if sch != "deterministic" else None
             res["frac_of_pattern_ceiling"] = (N / res["kernel_s"]) / ceil if ceil else None
             others[key] = {k_: res[k_] for k_ in ("value", "ms", "kernel_s", "rmse", "workers", "alg_GBps",
-                                                  "frac_alg", "epochs_done", "variant",
-                                                  "frac_of_pattern_ceiling")}
+                                                  "roofline_bound", "roofline_frac", "hbm_frac", "epochs_done",
+                                                  "variant", "frac_of_pattern_ceiling")}
+
+    if not a.no_variants and not a.no_c4 and a.config != "C4":
+        others.update(c4_leg(mf, stream, local, a.storage))
 
     # end to end through the public API from pinned host buffers
     hu, hv, hr = (torch.from_numpy(x).pin_memory() for x in (u, v, r))
@@ -424,6 +510,44 @@ def main():
         "other_runs": others,
     }
     print(json.dumps(out), flush=True)
+
+
+def c4_leg(mf, stream, local, storage, epochs=5):
+    """BASELINE.json configs[3], the Hugewiki shape (N = 3,069,817,980, m = 50M, n = 39,781, k = 128) on
+    THIS one GPU: batch-Hogwild!, the CTA wavefront and the partitioned schedule with one partition (the
+    multi-GPU code path's kernels and per-round launches, loopback transport).  The R triples (36.8 GB) and
+    P (12.8 GB fp16) are resident; HBM binds here (P is 100x the L2).  Synthetic draws are i.i.d., so the
+    stored order is already random (A-8, MF_OPT_SHUFFLE = 0).  Epochs 0-2 of the auto-tuned schedules are
+    their prefetch trials; the kernel time reported is the mean of the later epochs."""
+    import gc
+    cfg = datagen.CONFIGS["C4"]
+    t0 = time.perf_counter()
+    (u, v, r), (tu, tv, tr) = datagen.make(cfg)
+    gen_s = time.perf_counter() - t0
+    N = len(u)
+    out = {}
+    for key, sched, opts in (("C4:hogwild", "hogwild", {}), ("C4:wavefront_cta", "wavefront", {"wave_cta": 1}),
+                             ("C4:partitioned_1", "partitioned", {"partitions": 1})):
+        g = mf.MF(cfg.m, cfg.n, cfg.k, cfg.alpha, cfg.lam, cfg.seed_init, storage=storage, beta=cfg.beta,
+                  seed_shuffle=cfg.seed_shuffle, device=local, stream=stream.cuda_stream, shuffle=0, **opts)
+        g.load(u, v, r)
+        ks = []
+        for _ in range(epochs):
+            ks.append(g.epoch(sched).kernel_seconds)
+        rm = g.rmse(tu, tv, tr)
+        g.close()
+        k_s = statistics.mean(ks[3:]) if sched != "partitioned" else statistics.mean(ks[1:])
+        sname = "wavefront_cta" if opts.get("wave_cta") else "hogwild"
+        rf = roofline(cfg, storage, N, k_s, load_traffic(storage, "C4", sname), sname)
+        out[key + "/" + storage] = {"value": N / k_s, "kernel_s": k_s, "rmse_after_%d_epochs" % epochs: rm,
+                                    "roofline_bound": rf["bound"], "roofline_frac": rf["frac"],
+                                    "hbm": rf["hbm"], "N": N}
+    out["C4:note"] = ("kernel-timed (CUDA events inside libmf), inputs resident; host generation %.0f s; "
+                      "partitioned_1 = MF_SCHED_PARTITIONED with one loopback partition: %d passes x 1 round of "
+                      "two concurrent half-segment launches per epoch" % (gen_s, 4))
+    del u, v, r
+    gc.collect()
+    return out
 
 
 def run_partitioned(a, cfg, rank, world, local):
@@ -502,9 +626,6 @@ def run_partitioned(a, cfg, rank, world, local):
     n_tot = float(n_tot)
     value = n_tot / (ms * 1e-3)
     k_s = statistics.mean(kern)
-    peak, peak_kind = peaks()
-    B = b_alg(cfg.k, a.storage)
-    achieved = B * N_loc / k_s / 1e9
     g.close()
 
     hu, hv, hr = (torch.from_numpy(x).pin_memory() for x in (u, v, r))
@@ -537,9 +658,8 @@ def run_partitioned(a, cfg, rank, world, local):
                     "in_flight_per_q_column": st.workers / max(1, cfg.n // G),
                     "note": "accuracy falls with in-flight ratings per Q-segment column (DESIGN.md 5.5)"},
             "test_rmse": rm,
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                         "traffic": None, "peak_kind": peak_kind, "kernel": "k_hogwild (rank 0, all rounds)",
-                         "kernel_ms": k_s * 1e3, "bytes_per_update_alg": B},
+            "roofline": dict(roofline(cfg, a.storage, N_loc, k_s, None, "hogwild"),
+                             kernel="k_hogwild (rank 0, all launches of the epoch)"),
             "cpu_baseline": None,
             "e2e": {"value": n_tot / (float(e2e_ms) * 1e-3), "unit": "updates/s",
                     "h2d_bytes_per_step": 12 * N_loc * G + 12 * len(tu) * G, "d2h_bytes_per_step": 8 * G,

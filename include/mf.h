@@ -97,10 +97,13 @@ typedef enum {
                                  per SM with the column group's Q rows staged in shared memory, lock-free inside the block;
                                  2 = as 1 with two 512-thread CTA workers per SM */
     MF_OPT_STREAM_CHUNK = 18, /* mf_epoch_host: samples per streamed chunk (default 2^23) */
-    MF_OPT_PART_SPLIT = 19    /* partitioned: 0 = one launch per block, its workers spread over the whole Q segment, the
-                                 hand-over after it (default); 1 = each block as two half-segment sub-blocks, the lower
-                                 half's hand-over overlapping the upper half's updates -- twice the ratings in flight per
-                                 Q column, so further from serial SGD */
+    MF_OPT_PART_SPLIT = 19    /* partitioned: 2 = unit grid (default): 2G column units (segment halves), each family of
+                                 halves rotating by its own Latin square (a randomized G x 2G Latin rectangle per pass,
+                                 P:525-535), the two units of a partition updated concurrently on two streams with half
+                                 of its workers each, every unit's hand-over overlapping the other unit's updates
+                                 (P:307-314); 0 = one launch per whole block, hand-over after it; 1 = each block as two
+                                 half-segment sub-blocks in sequence with all workers each -- twice the ratings in flight
+                                 per Q column, so further from serial SGD */
 } mf_option;
 
 typedef struct {
@@ -179,10 +182,16 @@ int mf_attach_nccl(mf_ctx *ctx, const void *id128, int rank, int world);
  * square, so the blocks of one round share no row or column segment. */
 int mf_segment(int64_t extent, int32_t parts, int32_t index, int64_t *begin, int64_t *end);
 int mf_round_segment(uint64_t seed, int32_t pass, int32_t G, int32_t round, int32_t rank, int32_t *col_segment);
+/* Unit grid (MF_OPT_PART_SPLIT = 2): the segment c whose half `half` (0 lower rows [0, len/2), 1 upper) partition
+ * `rank` updates in `round` of `pass`; half 0 equals mf_round_segment.  Host-only.  MF_EINVAL on out-of-range input. */
+int mf_round_unit(uint64_t seed, int32_t pass, int32_t G, int32_t round, int32_t rank, int32_t half, int32_t *col_segment);
 /* Peers of partition `rank` for the Q exchange after round `round` of pass `pass` (the last round hands
  * over to round 0 of pass+1): it sends its segment to *send_to and receives from *recv_from. */
 int mf_round_peers(uint64_t seed, int32_t pass, int32_t G, int32_t round, int32_t rank, int32_t *send_to,
                    int32_t *recv_from);
+/* The same for the unit of family `half` under the unit grid (half 0 equals mf_round_peers). */
+int mf_unit_peers(uint64_t seed, int32_t pass, int32_t G, int32_t round, int32_t rank, int32_t half, int32_t *send_to,
+                  int32_t *recv_from);
 /* The paper's Hogwild! feasibility rule (§5.5.1): with s concurrent workers on an i x j
  * block grid of an m x n matrix, convergence was observed only for s < min(floor(m/i), floor(n/j)) /
  * safety (safety = 20 in the paper: Hugewiki, min(m, n) = 40k, s = 768 converges at j = 2, fails at

@@ -319,7 +319,7 @@ extern "C" int mf_set_option(mf_ctx *ctx, int key, double value) {
             ctx->wf_valid = false;
             return MF_OK;
         case MF_OPT_PART_SPLIT:
-            if (iv < 0 || iv > 1) return ctx->fail(MF_EINVAL, "part split must be 0 or 1");
+            if (iv < 0 || iv > 2) return ctx->fail(MF_EINVAL, "part split must be 0, 1 or 2");
             ctx->part_split = (int)iv;
             ctx->part_valid = false;
             return MF_OK;

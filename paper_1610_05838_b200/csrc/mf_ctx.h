@@ -32,7 +32,9 @@ struct mf_ctx {
     int count_updates = 0;
     int partitions = 0;
     int subepochs = 0;  // passes per epoch of the partitioned schedule (MF_OPT_SUBEPOCHS; 0 = 4)
-    int part_split = 0; // partitioned: 1 = blocks as two half-segment sub-blocks, pipelined hand-over (MF_OPT_PART_SPLIT)
+    int part_split = 2; // partitioned (MF_OPT_PART_SPLIT): 0 = whole blocks; 1 = two half-segment sub-blocks in
+                        // sequence, pipelined hand-over; 2 = unit grid (2G half-segment units, two concurrent
+                        // families with their own Latin squares, each hand-over overlapping the other's compute)
     int wave_cta = 0;   // wavefront worker = CTA with shared-memory Q group (MF_OPT_WAVE_CTA)
     int variant = 0;
     int trace = 0;
@@ -111,6 +113,7 @@ struct mf_ctx {
     int part_G = 0;                  // partitions = world size (NCCL) or logical partitions (loopback)
     int part_local = 0;              // partitions hosted by this context (1 with NCCL, G in loopback)
     int part_S = 1;                  // passes per epoch in the current layout
+    int part_mode = 0;               // MF_OPT_PART_SPLIT the current layout was built with
     int32_t *bu = nullptr, *bv = nullptr;  // samples bucketed by (local partition, column segment); v segment-local
     float *br = nullptr;
     std::vector<int64_t> h_blk_off;  // (part_local * G + 1) block offsets
@@ -125,6 +128,13 @@ struct mf_ctx {
     cudaEvent_t ev_half[2] = {}, ev_recv[2] = {};  // pipelined half-segment exchange
     bool recv_pending = false;  // q_cur halves are still arriving on comm_stream (wait on ev_recv)
     void *gather_tmp = nullptr;
+    // unit grid (MF_OPT_PART_SPLIT = 2): column unit (c, h) = half h (0 lower, 1 upper) of segment c; family h
+    // rotates by its own Latin square per pass; family 1 computes on stream2 concurrently with family 0
+    std::vector<void *> u_cur[2], u_next[2];  // per family, per hosted partition: the unit it holds / receive buffer
+    std::vector<int32_t> held_u[2];           // held_u[h][g] = segment whose half h partition g holds
+    int64_t unit_rows_max = 0;
+    cudaStream_t stream2 = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
 
     // streamed epochs from caller memory (mf_stream.cu)
     static constexpr int kStreamBufs = 3;
@@ -177,6 +187,11 @@ struct mf_ctx {
     int build_partition();
     int exchange_segments(const std::vector<int32_t> &want);
     int exchange_half(const std::vector<int32_t> &want, int h);
+    int epoch_units(mf_epoch_stats *stats);
+    int exchange_unit(const std::vector<int32_t> &want, int h, cudaStream_t hs);
+    int scatter_units(const std::vector<int32_t> (&want)[2]);
+    int gather_units();
+    void unit_rows(int c, int h, int64_t *row0, int64_t *rows) const;  // global first row and row count of unit (c, h)
     int rmse_partitioned(int64_t nnz, double *out);
     int gather_q();
     void release_partition();

@@ -152,13 +152,14 @@ __global__ void __launch_bounds__(kBlock) k_hogwild(UpdateArgs a) {
     const int64_t nwarps = (a.active_groups + G - 1) / G;
     const int64_t tail_zone = nwarps * (int64_t)f;
     const int64_t dyn0 = 2 * nwarps * (int64_t)f;
+    unsigned long long *const ctr = a.chunk_ctr ? a.chunk_ctr : &a.scratch->chunk;
     auto claim = [&](int64_t *len) -> int64_t {
         unsigned long long c = 0;
         int want = f;
         if (lane == 0) {
-            const unsigned long long seen = *(volatile unsigned long long *)&a.scratch->chunk;
+            const unsigned long long seen = *(volatile unsigned long long *)ctr;
             if (dyn0 + (int64_t)seen + tail_zone >= N) want = 32;
-            c = atomicAdd(&a.scratch->chunk, (unsigned long long)want);
+            c = atomicAdd(ctr, (unsigned long long)want);
         }
         *len = __shfl_sync(0xffffffffu, want, 0);
         return dyn0 + (int64_t)__shfl_sync(0xffffffffu, c, 0);
@@ -328,7 +329,7 @@ static cudaError_t hogwild_launch(const UpdateArgs &a, int workers, cudaStream_t
     args.active_groups = groups;
     args.batch_f = batch_f;
     // every launch claims chunks from 0 (the partitioned path launches once per block)
-    cudaError_t e = cudaMemsetAsync(&a.scratch->chunk, 0, sizeof(unsigned long long), st);
+    cudaError_t e = cudaMemsetAsync(a.chunk_ctr ? a.chunk_ctr : &a.scratch->chunk, 0, sizeof(unsigned long long), st);
     if (e != cudaSuccess) return e;
     k_hogwild<SH, D><<<blocks, kBlock, 0, st>>>(args);
     return cudaGetLastError();

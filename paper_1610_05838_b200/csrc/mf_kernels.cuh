@@ -18,6 +18,7 @@ struct DevScratch {
     unsigned bar_gen;             // grid barrier generation
     int pad;
     unsigned long long bad;       // validation: out-of-range / non-finite count
+    unsigned long long chunk2;    // second claim counter (a concurrent launch on another stream)
 };
 
 struct UpdateArgs {
@@ -33,6 +34,7 @@ struct UpdateArgs {
     int batch_f;        // samples per chunk (multiple of 32)
     int count_updates;
     DevScratch *scratch;
+    unsigned long long *chunk_ctr;  // batch-Hogwild! claim counter (nullptr: &scratch->chunk)
     const int64_t *wave_off;  // deterministic: wave offsets (nwaves + 1)
     int64_t nwaves;
     int64_t active_groups;  // batch-Hogwild!: groups beyond this idle (exact worker count)

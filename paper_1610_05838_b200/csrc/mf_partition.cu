@@ -14,6 +14,18 @@
 //
 // Inside a block the update is batch-Hogwild! (workers = max(1, N_local / 10^4), A-10),
 // or exactly serial with MF_OPT_WORKERS = 1 (used for parity).
+//
+// Unit grid (MF_OPT_PART_SPLIT = 2, the default): the column dimension is cut finer than the workers,
+// C = 2G column units (the lower and upper half of every segment), as the paper asks of a grid that
+// must keep convergence (§5.5.2) and as its overlap of transfer and compute needs (P:307-314,
+// §4.2).  Family h (all lower halves, or all upper halves) rotates by its own randomized Latin square
+// per pass, so over a pass every partition visits all 2G units (a randomized G x 2G Latin rectangle:
+// in a round no two partitions share a unit, and the pair of units a partition holds changes from
+// round to round and pass to pass).  A partition updates its two units concurrently, family 0 on the
+// context stream and family 1 on a second stream, with half of the partition's workers each -- the
+// same ratings in flight per Q column as one launch over a whole segment -- and each unit is handed on
+// (comm stream) as soon as its own sub-block is done, while the other family is still computing; the
+// next round of a family waits only for its own unit to arrive.
 #include <cuda_runtime.h>
 #include <nccl.h>
 
@@ -39,6 +51,10 @@ void round_perm(std::vector<int32_t> &pi, uint64_t seed, int32_t epoch, int G) {
     permutation(pi, G, host_mix(seed ^ 0xB10CB10Cull ^ ((uint64_t)(uint32_t)epoch << 32)));
 }
 int32_t sigma(const std::vector<int32_t> &pi, int G, int g, int r) { return pi[(g + r) % G]; }
+// unit grid: family h's Latin square of pass p (family 0's is the whole-segment square of round_perm)
+void unit_perm(std::vector<int32_t> &pi, uint64_t seed, int32_t pass, int G, int h) {
+    round_perm(pi, h ? seed ^ 0x5EC0DF4A11F00D5Eull : seed, pass, G);
+}
 
 // segment index of x in [0, extent) split into `parts` (boundaries floor(i*extent/parts))
 __device__ __forceinline__ int seg_of(int64_t x, int64_t extent, int parts) {
@@ -65,15 +81,17 @@ __global__ void k_part_keys(const int32_t *u, const int32_t *v, int64_t n, int64
     }
 }
 
-// gather into block order; v becomes local to its column segment
+// gather into block order; v becomes local to its column segment (unit grid: to its half-segment unit)
 __global__ void k_part_gather(const int32_t *u, const int32_t *v, const float *r, const uint32_t *idx,
-                              const uint32_t *keys, int64_t n, int64_t n_cols, int G, int32_t *bu, int32_t *bv,
-                              float *br) {
+                              const uint32_t *keys, int64_t n, int64_t n_cols, int G, int unit, int32_t *bu,
+                              int32_t *bv, float *br) {
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
         const uint32_t j = idx[i];
         const int cs = (int)((keys[i] >> 1) % (uint32_t)G);
+        const int64_t qb = ((int64_t)cs * n_cols) / G, qe = ((int64_t)(cs + 1) * n_cols) / G;
+        const int64_t base = qb + ((unit && (keys[i] & 1u)) ? (qe - qb) / 2 : 0);
         bu[i] = u[j];
-        bv[i] = v[j] - (int32_t)(((int64_t)cs * n_cols) / G);
+        bv[i] = v[j] - (int32_t)base;
         br[i] = r[j];
     }
 }
@@ -119,6 +137,16 @@ extern "C" int mf_feasibility(int64_t m, int64_t n, int32_t i, int32_t j, int64_
     return s * safety < mn ? 1 : 0;
 }
 
+extern "C" int mf_round_unit(uint64_t seed, int32_t pass, int32_t G, int32_t round, int32_t rank, int32_t half,
+                             int32_t *col_segment) {
+    if (G <= 0 || round < 0 || round >= G || rank < 0 || rank >= G || pass < 0 || half < 0 || half > 1 || !col_segment)
+        return MF_EINVAL;
+    std::vector<int32_t> pi;
+    unit_perm(pi, seed, pass, G, half);
+    *col_segment = sigma(pi, G, rank, round);
+    return MF_OK;
+}
+
 extern "C" int mf_round_segment(uint64_t seed, int32_t epoch, int32_t G, int32_t round, int32_t rank,
                                 int32_t *col_segment) {
     if (G <= 0 || round < 0 || round >= G || rank < 0 || rank >= G || epoch < 0 || !col_segment) return MF_EINVAL;
@@ -130,25 +158,40 @@ extern "C" int mf_round_segment(uint64_t seed, int32_t epoch, int32_t G, int32_t
 
 // peers of partition `rank` for the exchange that follows round `round` of `epoch` (the last round
 // hands over to round 0 of epoch + 1): it sends its segment to *send_to, receives from *recv_from.
-extern "C" int mf_round_peers(uint64_t seed, int32_t epoch, int32_t G, int32_t round, int32_t rank,
-                              int32_t *send_to, int32_t *recv_from) {
-    if (G <= 0 || round < 0 || round >= G || rank < 0 || rank >= G || epoch < 0 || !send_to || !recv_from)
-        return MF_EINVAL;
+static int family_peers(uint64_t seed, int32_t pass, int32_t G, int32_t round, int32_t rank, int h, int32_t *send_to,
+                        int32_t *recv_from) {
     std::vector<int32_t> pi, pn;
-    round_perm(pi, seed, epoch, G);
+    unit_perm(pi, seed, pass, G, h);
     if (round + 1 < G) pn = pi;
-    else round_perm(pn, seed, epoch + 1, G);
+    else unit_perm(pn, seed, pass + 1, G, h);
     const int nr = (round + 1) % G;
     std::vector<int32_t> held(G), want(G);
     for (int g = 0; g < G; g++) {
         held[g] = sigma(pi, G, g, round);
         want[g] = sigma(pn, G, g, nr);
     }
-    for (int h = 0; h < G; h++) {
-        if (want[h] == held[rank]) *send_to = h;
-        if (held[h] == want[rank]) *recv_from = h;
+    for (int x = 0; x < G; x++) {
+        if (want[x] == held[rank]) *send_to = x;
+        if (held[x] == want[rank]) *recv_from = x;
     }
     return MF_OK;
+}
+
+// peers of partition `rank` for the exchange that follows round `round` of pass `pass` (the last round
+// hands over to round 0 of pass + 1): it sends its segment to *send_to, receives from *recv_from.
+extern "C" int mf_round_peers(uint64_t seed, int32_t epoch, int32_t G, int32_t round, int32_t rank,
+                              int32_t *send_to, int32_t *recv_from) {
+    if (G <= 0 || round < 0 || round >= G || rank < 0 || rank >= G || epoch < 0 || !send_to || !recv_from)
+        return MF_EINVAL;
+    return family_peers(seed, epoch, G, round, rank, 0, send_to, recv_from);
+}
+
+extern "C" int mf_unit_peers(uint64_t seed, int32_t pass, int32_t G, int32_t round, int32_t rank, int32_t half,
+                             int32_t *send_to, int32_t *recv_from) {
+    if (G <= 0 || round < 0 || round >= G || rank < 0 || rank >= G || pass < 0 || half < 0 || half > 1 || !send_to ||
+        !recv_from)
+        return MF_EINVAL;
+    return family_peers(seed, pass, G, round, rank, half, send_to, recv_from);
 }
 
 // ------------------------------------------------------------------ NCCL ----
@@ -197,6 +240,12 @@ void mf_ctx::release_partition() {
             if (p) cudaFree(p);
     q_cur.clear();
     q_next.clear();
+    for (int h = 0; h < 2; h++) {
+        for (auto *vec : {&u_cur[h], &u_next[h]})
+            for (void *p : *vec)
+                if (p) cudaFree(p);
+        u_cur[h].clear(), u_next[h].clear(), held_u[h].clear();
+    }
     held.clear();
     h_blk_off.clear();
     seg_valid = false;
@@ -206,6 +255,10 @@ void mf_ctx::release_partition() {
         if (*ev) cudaEventDestroy(*ev), *ev = nullptr;
     if (comm_stream) cudaStreamDestroy(comm_stream);
     comm_stream = nullptr;
+    if (stream2) cudaStreamDestroy(stream2);
+    stream2 = nullptr;
+    for (auto *ev : {&ev_fork, &ev_join})
+        if (*ev) cudaEventDestroy(*ev), *ev = nullptr;
     if (nccl) {
         if (nccl->comm) ncclCommDestroy(nccl->comm);
         delete nccl;
@@ -232,11 +285,16 @@ int mf_ctx::build_partition() {
         if (p) cudaFree(p);
     bu = bv = nullptr;
     br = nullptr;
-    for (auto *vec : {&q_cur, &q_next})
+    for (auto *vec : {&q_cur, &q_next, &u_cur[0], &u_next[0], &u_cur[1], &u_next[1]})
         for (void *p : *vec)
             if (p) cudaFree(p);
-    q_cur.assign(local, nullptr);
-    q_next.assign(local, nullptr);
+    const int mode = part_split;
+    q_cur.assign(mode == 2 ? 0 : local, nullptr);
+    q_next.assign(mode == 2 ? 0 : local, nullptr);
+    for (int h = 0; h < 2; h++) {
+        u_cur[h].assign(mode == 2 ? local : 0, nullptr);
+        u_next[h].assign(mode == 2 ? local : 0, nullptr);
+    }
     seg_valid = false;
 
     cudaStream_t st = stream();
@@ -262,14 +320,14 @@ int mf_ctx::build_partition() {
     CK(cudaMallocAsync((void **)&doff, sizeof(int64_t) * (nb + 1), st));
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((N + 255) / 256, 148 * 16));
     // loopback: rows are global, split into G segments; NCCL: u is already local to this rank's segment
-    k_part_keys<<<grid, 256, 0, st>>>(u, v, N, m, n, G, is_distributed() ? 0 : 1, S, part_split, k0, i0);
+    k_part_keys<<<grid, 256, 0, st>>>(u, v, N, m, n, G, is_distributed() ? 0 : 1, S, mode != 0, k0, i0);
     CK(cudaGetLastError());
     int bits = 1;
     while (bits < 32 && (1ull << bits) < (uint64_t)nb) bits++;
     CK(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, k0, k1, i0, i1, N, 0, bits, st));
     CK(cudaMallocAsync(&tmp, tmp_bytes, st));
     CK(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, k0, k1, i0, i1, N, 0, bits, st));  // stable
-    k_part_gather<<<grid, 256, 0, st>>>(u, v, r, i1, k1, N, n, G, bu, bv, br);
+    k_part_gather<<<grid, 256, 0, st>>>(u, v, r, i1, k1, N, n, G, mode == 2, bu, bv, br);
     CK(cudaGetLastError());
     k_offsets<<<grid, 256, 0, st>>>(k1, N, nb, doff);
     CK(cudaGetLastError());
@@ -280,18 +338,31 @@ int mf_ctx::build_partition() {
 
     seg_rows_max = 0;
     for (int c = 0; c < G; c++) seg_rows_max = std::max(seg_rows_max, seg_begin(n, G, c + 1) - seg_begin(n, G, c));
+    unit_rows_max = (seg_rows_max + 1) / 2;
     const size_t bytes = (size_t)seg_rows_max * k * storage_bytes();
+    const size_t ubytes = (size_t)std::max<int64_t>(1, unit_rows_max) * k * storage_bytes();
     for (int g = 0; g < local; g++) {
-        CK(cudaMalloc(&q_cur[g], bytes));
-        CK(cudaMalloc(&q_next[g], bytes));
+        if (mode == 2) {
+            for (int h = 0; h < 2; h++) {
+                CK(cudaMalloc(&u_cur[h][g], ubytes));
+                CK(cudaMalloc(&u_next[h][g], ubytes));
+            }
+        } else {
+            CK(cudaMalloc(&q_cur[g], bytes));
+            CK(cudaMalloc(&q_next[g], bytes));
+        }
     }
     if (!comm_stream) CK(cudaStreamCreateWithFlags(&comm_stream, cudaStreamNonBlocking));
-    for (auto *ev : {&ev_half[0], &ev_half[1], &ev_recv[0], &ev_recv[1]})
+    if (!stream2) CK(cudaStreamCreateWithFlags(&stream2, cudaStreamNonBlocking));
+    for (auto *ev : {&ev_half[0], &ev_half[1], &ev_recv[0], &ev_recv[1], &ev_fork, &ev_join})
         if (!*ev) CK(cudaEventCreateWithFlags(ev, cudaEventDisableTiming));
     part_G = G;
     part_local = local;
     part_S = S;
+    part_mode = mode;
     held.assign(G, -1);
+    held_u[0].assign(G, -1);
+    held_u[1].assign(G, -1);
     part_valid = true;
     return MF_OK;
 }
@@ -347,6 +418,7 @@ static int scatter_segments(mf_ctx *ctx, const std::vector<int32_t> &want) {
 int mf_ctx::gather_q() {
     if (full_valid) return MF_OK;
     if (!seg_valid) return fail(MF_ESTATE, "no valid copy of Q");
+    if (part_mode == 2) return gather_units();
     const int G = part_G;
     const size_t rb = (size_t)k * storage_bytes();
     const size_t bytes = (size_t)seg_rows_max * rb;
@@ -380,6 +452,7 @@ int mf_ctx::epoch_partitioned(mf_epoch_stats *stats) {
     if (!is_distributed() && partitions < 1) return fail(MF_EINVAL, "set MF_OPT_PARTITIONS or attach NCCL");
     int rc = build_partition();
     if (rc != MF_OK) return rc;
+    if (part_mode == 2) return epoch_units(stats);
     const int G = part_G;
     cudaStream_t st = stream();
     const int S = part_S, L = part_local;
@@ -427,8 +500,8 @@ int mf_ctx::epoch_partitioned(mf_epoch_stats *stats) {
                 for (int g = 0; g < G; g++) next[g] = sigma(pn, G, g, 0);
             }
             for (int h = 0; h < 2; h++) {
-                if (recv_pending && part_split) CK(cudaStreamWaitEvent(st, ev_recv[h], 0));
-                if (recv_pending && !part_split && h == 0) {  // one launch over the whole segment: both halves
+                if (recv_pending && part_mode) CK(cudaStreamWaitEvent(st, ev_recv[h], 0));
+                if (recv_pending && !part_mode && h == 0) {  // one launch over the whole segment: both halves
                     CK(cudaStreamWaitEvent(st, ev_recv[0], 0));
                     CK(cudaStreamWaitEvent(st, ev_recv[1], 0));
                 }
@@ -505,6 +578,192 @@ int mf_ctx::exchange_half(const std::vector<int32_t> &want, int h) {
     }
     CK(cudaEventRecord(ev_recv[h], cs));
     return MF_OK;
+}
+
+// ------------------------------------------------------------- unit grid ----
+void mf_ctx::unit_rows(int c, int h, int64_t *row0, int64_t *rows) const {
+    const int64_t b = seg_begin(n, part_G, c), len = seg_begin(n, part_G, c + 1) - b, hm = len / 2;
+    *row0 = b + (h ? hm : 0);
+    *rows = h ? len - hm : hm;
+}
+
+// full Q -> unit buffers (partition g takes unit (want[h][g], h) of both families)
+int mf_ctx::scatter_units(const std::vector<int32_t> (&want)[2]) {
+    const size_t rb = (size_t)k * storage_bytes();
+    for (int h = 0; h < 2; h++) {
+        for (int li = 0; li < part_local; li++) {
+            const int g = is_distributed() ? rank : li;
+            int64_t r0, rows;
+            unit_rows(want[h][g], h, &r0, &rows);
+            if (rows) CK(cudaMemcpyAsync(u_cur[h][li], (char *)Q + r0 * rb, rows * rb, cudaMemcpyDeviceToDevice, stream()));
+        }
+        held_u[h] = want[h];
+    }
+    seg_valid = true;
+    return MF_OK;
+}
+
+// unit buffers -> full Q (collective with NCCL: one all-gather per family)
+int mf_ctx::gather_units() {
+    const int G = part_G;
+    const size_t rb = (size_t)k * storage_bytes();
+    const size_t ubytes = (size_t)std::max<int64_t>(1, unit_rows_max) * rb;
+    cudaStream_t st = stream();
+    if (recv_pending) {  // the last round's hand-overs are still on the comm stream
+        CK(cudaStreamWaitEvent(st, ev_recv[0], 0));
+        CK(cudaStreamWaitEvent(st, ev_recv[1], 0));
+        recv_pending = false;
+    }
+    if (is_distributed()) {
+        if (!gather_tmp) CK(cudaMalloc(&gather_tmp, 2 * ubytes * G));
+        for (int h = 0; h < 2; h++) {
+            char *dst = (char *)gather_tmp + (size_t)h * G * ubytes;
+            NK(ncclAllGather(u_cur[h][0], dst, ubytes, ncclUint8, nccl->comm, st));
+            for (int x = 0; x < G; x++) {
+                int64_t r0, rows;
+                unit_rows(held_u[h][x], h, &r0, &rows);
+                if (rows) CK(cudaMemcpyAsync((char *)Q + r0 * rb, dst + x * ubytes, rows * rb, cudaMemcpyDeviceToDevice, st));
+            }
+        }
+    } else {
+        for (int h = 0; h < 2; h++)
+            for (int g = 0; g < G; g++) {
+                int64_t r0, rows;
+                unit_rows(held_u[h][g], h, &r0, &rows);
+                if (rows) CK(cudaMemcpyAsync((char *)Q + r0 * rb, u_cur[h][g], rows * rb, cudaMemcpyDeviceToDevice, st));
+            }
+    }
+    CK(cudaStreamSynchronize(st));
+    full_valid = true;
+    return MF_OK;
+}
+
+// Family h's units move toward `want` on the comm stream once the compute stream hs has finished the
+// family's sub-blocks of this round; the receive lands in u_next[h] (the caller swaps the buffers).  A
+// unit that stays (dst == self) is copied locally so that u_next is complete.
+int mf_ctx::exchange_unit(const std::vector<int32_t> &want, int h, cudaStream_t hs) {
+    const int G = part_G;
+    const size_t rb = (size_t)k * storage_bytes();
+    cudaStream_t cs = comm_stream;
+    CK(cudaEventRecord(ev_half[h], hs));
+    CK(cudaStreamWaitEvent(cs, ev_half[h], 0));
+    const std::vector<int32_t> &have = held_u[h];
+    std::vector<int> dst(G), src(G);
+    for (int g = 0; g < G; g++)
+        for (int x = 0; x < G; x++) {
+            if (want[x] == have[g]) dst[g] = x;
+            if (have[x] == want[g]) src[g] = x;
+        }
+    for (int li = 0; li < part_local; li++) {
+        const int g = is_distributed() ? rank : li;
+        int64_t s0, sr, r0, rr;
+        unit_rows(have[g], h, &s0, &sr);
+        unit_rows(want[g], h, &r0, &rr);
+        if (is_distributed()) {
+            if (dst[g] == g) {
+                if (sr) CK(cudaMemcpyAsync(u_next[h][0], u_cur[h][0], sr * rb, cudaMemcpyDeviceToDevice, cs));
+            } else {
+                NK(ncclGroupStart());
+                if (sr) NK(ncclSend(u_cur[h][0], sr * rb, ncclUint8, dst[g], nccl->comm, cs));
+                if (rr) NK(ncclRecv(u_next[h][0], rr * rb, ncclUint8, src[g], nccl->comm, cs));
+                NK(ncclGroupEnd());
+            }
+        } else if (sr) {  // loopback: partition g's unit lands in the receive buffer of partition dst[g]
+            CK(cudaMemcpyAsync(u_next[h][dst[g]], u_cur[h][li], sr * rb, cudaMemcpyDeviceToDevice, cs));
+        }
+    }
+    CK(cudaEventRecord(ev_recv[h], cs));
+    return MF_OK;
+}
+
+int mf_ctx::epoch_units(mf_epoch_stats *stats) {
+    const int G = part_G;
+    cudaStream_t st = stream();
+    const int S = part_S, L = part_local;
+    const float eta = eta_at(epoch);
+    const ShapeId sh = select_shape(k, storage, variant & 0xF);
+    auto blk = [&](int s, int li, int c, int h) { return ((((size_t)s * L + li) * G + c) << 1) | (size_t)h; };
+    std::vector<int64_t> n_local(L, 0);  // samples of each hosted partition per epoch (worker clamp, A-10)
+    for (int s = 0; s < S; s++)
+        for (int li = 0; li < L; li++) n_local[li] += h_blk_off[blk(s, li, G - 1, 1) + 1] - h_blk_off[blk(s, li, 0, 0)];
+    // MF_OPT_WORKERS = 1 is the exact mode: one rating at a time per partition, so the two families run
+    // one after the other on the context stream (family 0's sub-blocks, then family 1's, every round)
+    const bool serial = workers == 1;
+    int launches = 0, used_max = 0;
+    CK(cudaEventRecord(events[0], st));
+    CK(cudaMemsetAsync(scratch, 0, sizeof(DevScratch), st));
+    CK(cudaEventRecord(events[1], st));
+    std::vector<int32_t> pi[2], want[2], next[2];
+    for (int h = 0; h < 2; h++) {
+        want[h].assign(G, 0), next[h].assign(G, 0);
+        unit_perm(pi[h], seed_shuffle, epoch * S, G, h);
+        for (int g = 0; g < G; g++) want[h][g] = sigma(pi[h], G, g, 0);
+    }
+    int rc = MF_OK;
+    if (!seg_valid) {
+        rc = scatter_units(want);
+        recv_pending = false;
+    } else {
+        for (int h = 0; h < 2 && rc == MF_OK; h++) {
+            if (held_u[h] == want[h]) continue;  // normally in place: the previous epoch's last round handed it over
+            if (recv_pending) CK(cudaStreamWaitEvent(st, ev_recv[h], 0));
+            rc = exchange_unit(want[h], h, st);
+            for (int li = 0; li < L; li++) std::swap(u_cur[h][li], u_next[h][li]);
+            held_u[h] = want[h];
+            CK(cudaStreamWaitEvent(st, ev_recv[h], 0));
+        }
+    }
+    if (rc != MF_OK) return rc;
+    full_valid = false;
+    CK(cudaEventRecord(ev_fork, st));
+    CK(cudaStreamWaitEvent(stream2, ev_fork, 0));
+    for (int s = 0; s < S; s++) {
+        for (int h = 0; h < 2; h++) unit_perm(pi[h], seed_shuffle, epoch * S + s, G, h);
+        for (int r = 0; r < G; r++) {
+            int used_round = 0;
+            for (int h = 0; h < 2; h++) {
+                for (int g = 0; g < G; g++) want[h][g] = sigma(pi[h], G, g, r);
+                if (r + 1 < G) {
+                    for (int g = 0; g < G; g++) next[h][g] = sigma(pi[h], G, g, r + 1);
+                } else {  // hand over to round 0 of the next pass (of this or the next epoch)
+                    std::vector<int32_t> pn;
+                    unit_perm(pn, seed_shuffle, epoch * S + s + 1, G, h);
+                    for (int g = 0; g < G; g++) next[h][g] = sigma(pn, G, g, 0);
+                }
+                cudaStream_t hs = (serial || h == 0) ? st : stream2;
+                if (recv_pending) CK(cudaStreamWaitEvent(hs, ev_recv[h], 0));
+                for (int li = 0; li < L; li++) {
+                    const int g = is_distributed() ? rank : li;
+                    const size_t b = blk(s, li, want[h][g], h);
+                    const int64_t lo = h_blk_off[b], hi = h_blk_off[b + 1];
+                    if (hi <= lo) continue;
+                    UpdateArgs a = update_args(eta);
+                    a.u = bu + lo;
+                    a.v = bv + lo;
+                    a.r = br + lo;
+                    a.n = hi - lo;
+                    a.Q = u_cur[h][li];
+                    a.chunk_ctr = h ? &scratch->chunk2 : &scratch->chunk;
+                    const int64_t wp = workers > 0 ? workers : std::max<int64_t>(1, std::min<int64_t>(n_local[li] / 10000, 1 << 30));
+                    const int w = serial ? 1 : (int)std::max<int64_t>(1, wp / 2);  // half of the partition's workers per family
+                    int used = 0;
+                    CK(launch_hogwild(sh, a, w, variant, hs, &used));
+                    used_round += used;
+                    launches++;
+                }
+                rc = exchange_unit(next[h], h, hs);
+                if (rc != MF_OK) return rc;
+                for (int li = 0; li < L; li++) std::swap(u_cur[h][li], u_next[h][li]);
+                held_u[h] = next[h];
+            }
+            used_max = std::max(used_max, serial ? 1 : used_round / std::max(1, L));
+            recv_pending = true;
+        }
+    }
+    CK(cudaEventRecord(ev_join, stream2));
+    CK(cudaStreamWaitEvent(st, ev_join, 0));
+    CK(cudaEventRecord(events[2], st));
+    return finish_epoch(MF_SCHED_PARTITIONED, eta, launches, used_max, stats);
 }
 
 // Collective status agreement: each rank contributes its local status; every rank

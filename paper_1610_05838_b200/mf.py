@@ -54,6 +54,10 @@ _sig = {
     "mf_round_segment": ([c.c_uint64, c.c_int32, c.c_int32, c.c_int32, c.c_int32, c.POINTER(c.c_int32)], c.c_int),
     "mf_round_peers": ([c.c_uint64, c.c_int32, c.c_int32, c.c_int32, c.c_int32, c.POINTER(c.c_int32),
                         c.POINTER(c.c_int32)], c.c_int),
+    "mf_round_unit": ([c.c_uint64, c.c_int32, c.c_int32, c.c_int32, c.c_int32, c.c_int32, c.POINTER(c.c_int32)],
+                      c.c_int),
+    "mf_unit_peers": ([c.c_uint64, c.c_int32, c.c_int32, c.c_int32, c.c_int32, c.c_int32, c.POINTER(c.c_int32),
+                       c.POINTER(c.c_int32)], c.c_int),
     "mf_wavefront_trace": ([_P, _P, c.c_int64, c.POINTER(c.c_int64)], c.c_int),
     "mf_feasibility": ([c.c_int64, c.c_int64, c.c_int32, c.c_int32, c.c_int64, c.c_int32, c.POINTER(c.c_int64)],
                        c.c_int),
@@ -194,6 +198,18 @@ def mf_round_segment(seed, epoch, G, rnd, rank):
 def mf_round_peers(seed, epoch, G, rnd, rank):
     s, r = c.c_int32(), c.c_int32()
     _check(None, _lib.mf_round_peers(seed, epoch, G, rnd, rank, c.byref(s), c.byref(r)))
+    return s.value, r.value
+
+
+def mf_round_unit(seed, pas, G, rnd, rank, half):
+    out = c.c_int32()
+    _check(None, _lib.mf_round_unit(seed, pas, G, rnd, rank, half, c.byref(out)))
+    return out.value
+
+
+def mf_unit_peers(seed, pas, G, rnd, rank, half):
+    s, r = c.c_int32(), c.c_int32()
+    _check(None, _lib.mf_unit_peers(seed, pas, G, rnd, rank, half, c.byref(s), c.byref(r)))
     return s.value, r.value
 
 

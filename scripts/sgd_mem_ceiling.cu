@@ -10,7 +10,8 @@
 // allows for that shape.  Swept over groups in flight per SM and rows in flight per group.
 //
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o /tmp/sgd_mem_ceiling scripts/sgd_mem_ceiling.cu
-//   /tmp/sgd_mem_ceiling m n N row_bytes [p_only]
+//   /tmp/sgd_mem_ceiling m n N row_bytes [p_only] [warps_per_sm D]   (the last two: one configuration only,
+//   for an ncu capture of the pattern's saturated unit)
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -158,6 +159,13 @@ int main(int argc, char **argv) {
     printf("{\"m\": %lld, \"n\": %lld, \"N\": %lld, \"row_bytes\": %d, \"sms\": %d}\n", (long long)m, (long long)n,
            (long long)N, row_bytes, sms);
     const bool p_only = argc > 5 && atoi(argv[5]) != 0;
+    if (argc > 7 && row_bytes == 256 && !p_only) {  // one configuration (L16 x V1, p+q rows)
+        const int wps = atoi(argv[6]), D = atoi(argv[7]);
+        const double u1 = D == 2 ? run<16, 1, 2, true>(u, v, r, N, P, Q, wps, sms, ctr)
+                                 : run<16, 1, 1, true>(u, v, r, N, P, Q, wps, sms, ctr);
+        printf("{\"shape\": \"L16xV1\", \"warps_per_sm\": %d, \"D\": %d, \"updates_per_s\": %.4g}\n", wps, D, u1);
+        return 0;
+    }
     if (row_bytes == 256 && !p_only) {
         sweep<16, 1>("L16xV1", u, v, r, N, P, Q, sms, ctr, row_bytes);
         sweep<8, 2>("L8xV2", u, v, r, N, P, Q, sms, ctr, row_bytes);

@@ -211,7 +211,8 @@ def c4r10():
 
 
 @pytest.mark.parametrize("schedule,G,split", [
-    ("hogwild", 1, 0), ("partitioned", 2, 0), ("partitioned", 4, 0), ("partitioned", 8, 0),
+    ("hogwild", 1, 0), ("partitioned", 2, 2), ("partitioned", 4, 2), ("partitioned", 8, 2),
+    ("partitioned", 2, 0), ("partitioned", 4, 0), ("partitioned", 8, 0),
     pytest.param("partitioned", 4, 1, marks=pytest.mark.xfail(
         strict=False, reason="the pipelined half-segment form (MF_OPT_PART_SPLIT = 1) puts a launch's 7,674 "
                              "in-flight ratings on half of a 9,945-column Q segment: +0.69% after 10 epochs "

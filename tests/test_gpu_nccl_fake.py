@@ -4,7 +4,7 @@ Real NCCL refuses two ranks on one device, and this environment gives one GPU pe
 run with tests/fake_nccl (LD_PRELOAD), a host-staged stand-in for the NCCL calls libmf makes
 (grouped send/recv, all-gather, all-reduce) that keeps their pairing and stream-ordering semantics.
 Everything else is the production path: mf_attach_nccl, local-row layout, the hand-over on the comm
-stream (whole blocks, and the pipelined half-segment form), collective mf_rmse / mf_get_factors.  With one worker per block the
+stream (whole blocks, the pipelined half-segment form and the unit grid), collective mf_rmse / mf_get_factors.  With one worker per block the
 run must equal the serial oracle over the (epoch, pass, round, rank, half) order reconstructed from
 the ranks' stored orders and libmf's round schedule.
 """
@@ -31,7 +31,7 @@ def fake_nccl(tmp_path_factory):
     return str(out)
 
 
-@pytest.mark.parametrize("G,split", [(2, 0), (3, 0), (2, 1), (3, 1)])
+@pytest.mark.parametrize("G,split", [(2, 0), (3, 0), (2, 1), (3, 1), (2, 2), (3, 2)])
 def test_multirank_partitioned_matches_oracle_block_sweep(fake_nccl, tmp_path, G, split):
     from paper_1610_05838_b200 import mf
     cfg = datagen.CONFIGS["C1"]
@@ -64,14 +64,22 @@ def test_multirank_partitioned_matches_oracle_block_sweep(fake_nccl, tmp_path, G
         order = []
         for s in range(S):
             for rnd in range(G):
-                for g in range(G):
-                    o = res[g]["order"]  # this rank's stored order, as indices into the global arrays
-                    pos = np.arange(len(o))
-                    c = mf.mf_round_segment(cfg.seed_shuffle, e * S + s, G, rnd, g)
-                    mid = cs[c][0] + (cs[c][1] - cs[c][0]) // 2
-                    for lo, hi in (((cs[c][0], mid), (mid, cs[c][1])) if split else ((cs[c][0], cs[c][1]),)):
-                        sel = ((pos * S) // len(o) == s) & (v[o] >= lo) & (v[o] < hi)
-                        order.append(o[sel])
+                for h in ((0, 1) if split == 2 else (None,)):  # unit grid: family 0's sub-blocks, then family 1's
+                    for g in range(G):
+                        o = res[g]["order"]  # this rank's stored order, as indices into the global arrays
+                        pos = np.arange(len(o))
+                        if split == 2:
+                            c = mf.mf_round_unit(cfg.seed_shuffle, e * S + s, G, rnd, g, h)
+                        else:
+                            c = mf.mf_round_segment(cfg.seed_shuffle, e * S + s, G, rnd, g)
+                        mid = cs[c][0] + (cs[c][1] - cs[c][0]) // 2
+                        if split == 2:
+                            ranges = ((cs[c][0], mid),) if h == 0 else ((mid, cs[c][1]),)
+                        else:
+                            ranges = ((cs[c][0], mid), (mid, cs[c][1])) if split else ((cs[c][0], cs[c][1]),)
+                        for lo, hi in ranges:
+                            sel = ((pos * S) // len(o) == s) & (v[o] >= lo) & (v[o] < hi)
+                            order.append(o[sel])
         order = np.concatenate(order)
         assert len(order) == len(u) and len(np.unique(order)) == len(u)
         ref.epoch(u, v, r, oracle.eta(cfg.alpha, cfg.beta, e), cfg.lam, order)

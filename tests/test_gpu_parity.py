@@ -213,77 +213,81 @@ def test_c1_hogwild_rmse_within_half_percent(mfmod, c1, storage):
     assert abs(got - trace[-1]) <= 0.005 * trace[-1], (got, trace[-1])
 
 
-def test_netflix_slice_hogwild_many_workers(mfmod):
-    """C2-1pct, 10 epochs, explicit large worker count (c/n ~ 5): RMSE within 0.5% of serial."""
-    cfg = datagen.CONFIGS["C2-1pct"]
-    (u, v, r), test = datagen.make(cfg)
-    order = oracle.shuffle_perm(cfg.seed_shuffle, len(u))
-    E = 10
-    _, trace = oracle.train(cfg.m, cfg.n, cfg.k, oracle.F32, cfg.seed_init, u, v, r, cfg.alpha, cfg.beta, cfg.lam,
-                            E, order=order, test=test)
-    with _gpu(mfmod, cfg, count_updates=1) as g:
-        g.load(u, v, r)
-        for _ in range(E):
-            st = g.epoch("hogwild")
-            assert st.updates == len(u)
-        got = g.rmse(*test)
-    assert abs(got - trace[-1]) <= 0.005 * trace[-1], (got, trace[-1])
+# Single-run gates against oracle goldens on the 10% Netflix slice (C2-10pct: 48,019 x 1,777, 9.9M ratings,
+# the full shape's degrees; tests/golden/C2-10pct*_trace.json, scripts/make_golden.py, oracle/ only).  Every
+# run is gated on its own (no aggregation over repeats).  The gate epoch per storage is where the oracle's
+# own trace moves less than 0.5% per epoch (reading T5): fp32 epoch 10 (0.1811 -> 0.1811); fp16
+# epoch 6 (0.1816), before the fp16 trajectory leaves the fp32 plateau (epochs 7-20 descend 1-4% per
+# epoch, so a lag of a fraction of an epoch alone would exceed 0.5% there); bf16 epoch 20 (0.1062 ->
+# 0.1061, after its descent).
+GATE_EPOCH = {0: 10, 1: 6, 2: 20}
+STNAME = {0: "f32", 1: "f16", 2: "bf16"}
+
+
+def _c2_10pct_gold(storage, k=128):
+    import json
+    import os
+    name = "C2-10pct" if k == 128 else f"C2-10pct-k{k}"
+    path = os.path.join(os.path.dirname(__file__), "golden", f"{name}_{STNAME[storage]}_trace.json")
+    if not os.path.exists(path):
+        pytest.skip(f"{path} not generated yet")
+    return json.load(open(path))["rmse"]
 
 
 @functools.lru_cache(maxsize=None)
-def _c2_1pct_oracle_trace(storage, epochs):
-    cfg = datagen.CONFIGS["C2-1pct"]
-    (u, v, r), test = datagen.make(cfg)
-    order = oracle.shuffle_perm(cfg.seed_shuffle, len(u))
-    return oracle.train(cfg.m, cfg.n, cfg.k, ORC[storage], cfg.seed_init, u, v, r, cfg.alpha, cfg.beta, cfg.lam,
-                        epochs, order=order, test=test)[1]
+def _c2_10pct_data(k=128):
+    cfg = datagen.CONFIGS["C2-10pct"]
+    if k != cfg.k:
+        cfg = cfg.scaled(k=k)
+    return cfg, datagen.make(cfg)
 
 
-@pytest.mark.parametrize("storage,pf", [(0, 15), (0, 1), (1, 1), (1, 2), (2, 1)])
-def test_netflix_slice_hogwild_l2_prefetch(mfmod, storage, pf):
-    """The L2 row prefetch of batch-Hogwild! (MF_OPT_VARIANT bits 16..19) only moves cache lines: every
-    setting processes each sample exactly once and lands within 0.5% of the serial oracle (C2-1pct,
-    k = 128 full-row shape, 10 epochs as in the test above; median of 3 runs, see _hogwild_median)."""
-    cfg = datagen.CONFIGS["C2-1pct"]
-    (u, v, r), test = datagen.make(cfg)
-    E = 10
-    trace = _c2_1pct_oracle_trace(storage, E)
-    got = _hogwild_median(mfmod, cfg, storage, (u, v, r), test, E, variant=pf << 16,
-                          check=lambda g: (int(g.get(mfmod.MF_OPT_VARIANT)) >> 16) & 0xF == pf)
-    assert abs(got - trace[-1]) <= 0.005 * trace[-1], (got, trace[-1])
-
-
-def _hogwild_median(mfmod, cfg, storage, train, test, E, reps=3, check=None, **opts):
-    """Median test RMSE of `reps` independent batch-Hogwild! runs (E epochs each, every one exactly once
-    per epoch).  Lock-free runs differ from run to run: on the 1% Netflix slice (178 columns) fp16
-    repeats spread -0.39..+0.29% around the serial oracle (scripts/hogwild_repeatability.py), so a
-    single run can touch a 0.5% gate that the schedule meets; the median of three does not."""
+def _hogwild_run(mfmod, cfg, storage, train, test, E, check=None, **opts):
+    """Test RMSE after E batch-Hogwild! epochs of ONE run (exactly once per epoch checked)."""
     u, v, r = train
-    vals = []
-    for _ in range(reps):
-        with _gpu(mfmod, cfg, storage, count_updates=1, **opts) as g:
-            g.load(u, v, r)
-            for _ in range(E):
-                assert g.epoch("hogwild").updates == len(u)
-            vals.append(g.rmse(*test))
-            if check is not None:
-                assert check(g)
-    return float(np.median(vals))
+    with _gpu(mfmod, cfg, storage, count_updates=1, **opts) as g:
+        g.load(u, v, r)
+        for _ in range(E):
+            assert g.epoch("hogwild").updates == len(u)
+        if check is not None:
+            assert check(g)
+        return g.rmse(*test)
+
+
+def test_netflix_slice_hogwild_many_workers(mfmod):
+    """C2-10pct, fp32, 10 epochs with an explicit worker count of 9,472 -- the full residency the full-size
+    Netflix shape runs at, on a tenth of its columns (c/n = 5.3 ratings in flight per column, 10x the
+    full shape's 0.53): test RMSE within 0.5% of the serial oracle's (single run)."""
+    cfg, (train, test) = _c2_10pct_data()
+    gold = _c2_10pct_gold(0)
+    E = GATE_EPOCH[0]
+    got = _hogwild_run(mfmod, cfg, 0, train, test, E, workers=9472,
+                       check=lambda g: int(g.get(mfmod.MF_OPT_WORKERS)) == 9472)
+    assert abs(got - gold[E - 1]) <= 0.005 * gold[E - 1], (got, gold[E - 1])
+
+
+@pytest.mark.parametrize("storage,pf", [(0, 15), (0, 1), (1, 15), (1, 1), (1, 2), (2, 15), (2, 1)])
+def test_netflix_slice_hogwild_l2_prefetch(mfmod, storage, pf):
+    """The L2 row prefetch of batch-Hogwild! (MF_OPT_VARIANT bits 16..19; 15 = off) only moves cache lines:
+    every setting processes each sample exactly once and one run lands within 0.5% of the serial oracle's
+    test RMSE at the storage's gate epoch (C2-10pct, k = 128 full-row shape)."""
+    cfg, (train, test) = _c2_10pct_data()
+    gold = _c2_10pct_gold(storage)
+    E = GATE_EPOCH[storage]
+    got = _hogwild_run(mfmod, cfg, storage, train, test, E, variant=pf << 16,
+                       check=lambda g: (int(g.get(mfmod.MF_OPT_VARIANT)) >> 16) & 0xF == pf)
+    assert abs(got - gold[E - 1]) <= 0.005 * gold[E - 1], (got, gold[E - 1])
 
 
 @pytest.mark.parametrize("k,storage", [(32, 0), (32, 1), (64, 0), (64, 1)])
 def test_netflix_slice_hogwild_small_k(mfmod, k, storage):
     """The k = 32 / 64 batch-Hogwild! shapes (16 lanes per rating, 4- / 8-byte vectors): exactly once per
-    epoch, test RMSE within 0.5% of the storage-matched serial oracle after 10 epochs (C2-1pct; median
-    of 3 runs)."""
-    cfg = datagen.CONFIGS["C2-1pct"].scaled(k=k)
-    (u, v, r), test = datagen.make(cfg)
-    order = oracle.shuffle_perm(cfg.seed_shuffle, len(u))
-    E = 10
-    _, trace = oracle.train(cfg.m, cfg.n, cfg.k, ORC[storage], cfg.seed_init, u, v, r, cfg.alpha, cfg.beta,
-                            cfg.lam, E, order=order, test=test)
-    got = _hogwild_median(mfmod, cfg, storage, (u, v, r), test, E)
-    assert abs(got - trace[-1]) <= 0.005 * trace[-1], (got, trace[-1])
+    epoch, one run within 0.5% of the storage-matched serial oracle at the gate epoch (C2-10pct)."""
+    cfg, (train, test) = _c2_10pct_data(k)
+    gold = _c2_10pct_gold(storage, k)
+    E = GATE_EPOCH[storage]
+    got = _hogwild_run(mfmod, cfg, storage, train, test, E)
+    assert abs(got - gold[E - 1]) <= 0.005 * gold[E - 1], (got, gold[E - 1])
 
 
 def test_hogwild_prefetch_auto_resolves(mfmod):

@@ -22,25 +22,38 @@ def mf():
 def _block_sweep_order(mf, perm, u, v, m, n, G, seed, e, S=4, split=0):
     """Caller indices in processing order: pass s (stored positions [s N/S, (s+1) N/S)) -> round ->
     partition -> block samples in stored order (split = 1: the lower half of the block's columns, then
-    the upper half); pass s of epoch e uses Latin square e*S + s."""
+    the upper half); pass s of epoch e uses Latin square e*S + s.  split = 2 (unit grid): pass -> round
+    -> family h -> partition g -> the samples of unit (sigma_h(g, round), h), the half h of that segment
+    (with one worker the two families of a round run one after the other, family 0 first)."""
     us, vs = u[perm], v[perm]
     N = len(perm)
     pas = (np.arange(N) * S) // N
     rs = [mf.mf_segment(m, G, g) for g in range(G)]
     cs = [mf.mf_segment(n, G, c) for c in range(G)]
     out = []
+
+    def half(c, h):
+        mid = cs[c][0] + (cs[c][1] - cs[c][0]) // 2
+        return (cs[c][0], mid) if h == 0 else (mid, cs[c][1])
+
     for s in range(S):
         for rnd in range(G):
+            if split == 2:
+                for h in (0, 1):
+                    for g in range(G):
+                        lo, hi = half(mf.mf_round_unit(seed, e * S + s, G, rnd, g, h), h)
+                        sel = (pas == s) & (us >= rs[g][0]) & (us < rs[g][1]) & (vs >= lo) & (vs < hi)
+                        out.append(perm[np.nonzero(sel)[0]])
+                continue
             for g in range(G):
                 c = mf.mf_round_segment(seed, e * S + s, G, rnd, g)
-                mid = cs[c][0] + (cs[c][1] - cs[c][0]) // 2  # lower half first, then upper half
-                for lo, hi in (((cs[c][0], mid), (mid, cs[c][1])) if split else ((cs[c][0], cs[c][1]),)):
+                for lo, hi in ((half(c, 0), half(c, 1)) if split else ((cs[c][0], cs[c][1]),)):
                     sel = (pas == s) & (us >= rs[g][0]) & (us < rs[g][1]) & (vs >= lo) & (vs < hi)
                     out.append(perm[np.nonzero(sel)[0]])
     return np.concatenate(out)
 
 
-@pytest.mark.parametrize("split", [0, 1])
+@pytest.mark.parametrize("split", [0, 1, 2])
 @pytest.mark.parametrize("G", [1, 2, 3, 4])
 @pytest.mark.parametrize("storage", [0, 1])
 def test_loopback_serial_blocks_match_oracle_block_sweep(mf, G, storage, split):
