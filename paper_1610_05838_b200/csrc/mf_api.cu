@@ -314,7 +314,7 @@ extern "C" int mf_set_option(mf_ctx *ctx, int key, double value) {
             ctx->part_valid = false;
             return MF_OK;
         case MF_OPT_WAVE_CTA:
-            if (iv < 0 || iv > 2) return ctx->fail(MF_EINVAL, "wave cta must be 0, 1 or 2");
+            if (iv < 0 || iv > 3) return ctx->fail(MF_EINVAL, "wave cta must be 0, 1, 2 or 3");
             ctx->wave_cta = (int)iv;
             ctx->wf_valid = false;
             return MF_OK;
@@ -636,7 +636,7 @@ static int epoch_local(mf_ctx *ctx, int schedule, mf_epoch_stats *stats) {
     ctx->variant_eff = ctx->variant;
     if (((ctx->variant >> 16) & 0xF) == 0) {
         if (schedule == MF_SCHED_HOGWILD) tune = &ctx->pf_hogwild, pf_on = 1;
-        else if (schedule == MF_SCHED_WAVEFRONT && ctx->wave_cta)
+        else if (schedule == MF_SCHED_WAVEFRONT && ctx->wave_cta && ctx->wave_cta != 3)
             tune = &ctx->pf_wave_cta, pf_on = ctx->storage == kF32 ? 1 : 2;
         if (tune) ctx->variant_eff |= tune->next(pf_on, &pf_slot) << 16;
     }
@@ -653,6 +653,9 @@ static int epoch_local(mf_ctx *ctx, int schedule, mf_epoch_stats *stats) {
         // MF_OPT_VARIANT bits 24..25: 0 = 1024-thread CTAs, 2 samples per group and step; 1 = one
         // sample; 2 = 256-thread CTAs and the fenced barrier (r01 form)
         const int wsel = (ctx->variant >> 24) & 0x3;
+        // bits 22..23: grid barrier of the 1024-thread forms, 0 = arrival counter polled to its target,
+        // 1 = generation flag bumped by the last arriver (r01c)
+        a.barrier = ((ctx->variant >> 22) & 0x3) == 1 ? 1 : 0;
         CK(launch_waves(sh, a, st, &l, wsel == 2 ? 0 : wsel == 1 ? 1 : 2));
         used = 0;
     } else {  // wavefront

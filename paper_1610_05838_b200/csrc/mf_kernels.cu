@@ -405,6 +405,22 @@ __device__ __forceinline__ void grid_barrier_ra(DevScratch *s, unsigned nblocks)
     __syncthreads();
 }
 
+// Monotonic-counter barrier (one CTA per SM): every CTA adds 1 with a release reduction (no return
+// value to wait for) and polls the counter with acquire loads until it reaches target = (wave + 1) x
+// CTAs; the counter is zeroed with the epoch's scratch.  One memory round trip fewer than the
+// generation-flag form (the last arriver's atomic, its flag store, the waiters' poll).
+__device__ __forceinline__ void grid_barrier_count(DevScratch *s, unsigned target) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(&s->bar_count) : "memory");
+        unsigned cur;
+        do {
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(cur) : "l"(&s->bar_count) : "memory");
+        } while ((int)(cur - target) < 0);
+    }
+    __syncthreads();
+}
+
 // D samples of the same wave per group and step (a wave's samples are pairwise independent, so any
 // number may be in flight -- unlike batch-Hogwild! there is no staleness to bound); the per-rating
 // arithmetic (lane_dot, then the butterfly) is the same for every D, so results do not depend on it.
@@ -417,6 +433,23 @@ __global__ void __launch_bounds__(BLOCK) k_waves(UpdateArgs a) {
     const int64_t gid = ((int64_t)blockIdx.x * BLOCK + threadIdx.x) / L;
     int bad = 0;
     unsigned long long done = 0;
+    // The triples of a group's first step in the next wave are read-only and independent of the wave's
+    // updates: they are loaded before the barrier, so after it only the row loads stand between the
+    // barrier and the first update (one memory latency per wave instead of two).
+    int32_t nu[D], nv[D];
+    float nr[D];
+    auto fetch_first = [&](int64_t wv) {
+        const int64_t lo = a.wave_off[wv], hi = a.wave_off[wv + 1];
+#pragma unroll
+        for (int d = 0; d < D; d++) {
+            const int64_t s = lo + (gid - (lane / L)) + d * groups + lane / L;
+            const bool ok = s < hi;
+            nu[d] = ok ? __ldg(a.u + s) : 0;
+            nv[d] = ok ? __ldg(a.v + s) : 0;
+            nr[d] = ok ? __ldg(a.r + s) : 0.f;
+        }
+    };
+    if (a.nwaves > 0) fetch_first(0);
     for (int64_t w = 0; w < a.nwaves; w++) {
         const int64_t lo = a.wave_off[w], hi = a.wave_off[w + 1];
         // warp-uniform trip count so the full-warp shuffles stay converged
@@ -430,9 +463,13 @@ __global__ void __launch_bounds__(BLOCK) k_waves(UpdateArgs a) {
             for (int d = 0; d < D; d++) {
                 const int64_t s = s0 + d * groups + lane / L;
                 val[d] = s < hi;
-                su[d] = val[d] ? __ldg(a.u + s) : 0;
-                sv[d] = val[d] ? __ldg(a.v + s) : 0;
-                sr[d] = val[d] ? __ldg(a.r + s) : 0.f;
+                if (s0 == warp_first) {
+                    su[d] = nu[d], sv[d] = nv[d], sr[d] = nr[d];
+                } else {
+                    su[d] = val[d] ? __ldg(a.u + s) : 0;
+                    sv[d] = val[d] ? __ldg(a.v + s) : 0;
+                    sr[d] = val[d] ? __ldg(a.r + s) : 0.f;
+                }
                 load_row<SH>(a.P, su[d], k, sub, val[d], pr[d]);
                 load_row<SH>(a.Q, sv[d], k, sub, val[d], qr[d]);
             }
@@ -459,7 +496,9 @@ __global__ void __launch_bounds__(BLOCK) k_waves(UpdateArgs a) {
                 if (val[d] && sub == 0) done++;
             }
         }
+        if (w + 1 < a.nwaves) fetch_first(w + 1);
         if (BLOCK == kBlock) grid_barrier(a.scratch, gridDim.x);
+        else if (a.barrier == 0) grid_barrier_count(a.scratch, (unsigned)(w + 1) * gridDim.x);
         else grid_barrier_ra(a.scratch, gridDim.x);
     }
     if (bad) a.scratch->diverged = 1;

@@ -44,6 +44,8 @@ struct UpdateArgs {
     int cache_policy;   // L2 eviction priorities (MF_OPT_VARIANT bits 28..29, resolved): 0 = R evict_first,
                         // 1 = none (plain loads), 2 = R evict_first + P/Q rows evict_last, 3 = R evict_first +
                         // Q rows evict_last
+    int barrier;        // deterministic waves, 1024-thread CTAs: 0 = arrival counter polled to (w+1) x CTAs
+                        // (one release reduction + acquire polls), 1 = last arriver bumps a generation flag
 };
 
 // Kernel-shape choice for (k, storage); filled by select_shape().

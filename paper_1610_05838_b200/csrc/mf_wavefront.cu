@@ -45,6 +45,37 @@ __global__ void k_block_keys(const int32_t *u, const int32_t *v, int64_t n, int6
     }
 }
 
+// q-stationary layout (MF_OPT_WAVE_CTA = 3): key = band * n + v, so a block (band, column group) is a
+// contiguous key range and inside it the samples of one Q row (a "run") are contiguous, each run in
+// shuffled order (the sort is stable)
+__global__ void k_run_keys(const int32_t *u, const int32_t *v, int64_t n, int64_t rows, int64_t cols, int s,
+                           uint32_t *keys, uint32_t *idx) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        keys[i] = (uint32_t)((int64_t)seg_index(u[i], rows, s) * cols + v[i]);
+        idx[i] = (uint32_t)i;
+    }
+}
+
+// block offsets of the q-stationary layout: off[b] = first sorted position with key >= band * n +
+// first column of group g (b = band * c + g), off[s * c] = n; one binary search per block
+__global__ void k_run_block_offsets(const uint32_t *sorted_keys, int64_t n, int s, int c, int64_t cols, int64_t *off) {
+    const int64_t nb = (int64_t)s * c;
+    for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b <= nb; b += (int64_t)gridDim.x * blockDim.x) {
+        if (b == nb) {
+            off[b] = n;
+            continue;
+        }
+        const uint32_t key = (uint32_t)((b / c) * cols + seg_begin(cols, c, (int)(b % c)));
+        int64_t lo = 0, hi = n;
+        while (lo < hi) {
+            const int64_t mid = (lo + hi) >> 1;
+            if (sorted_keys[mid] < key) lo = mid + 1;
+            else hi = mid;
+        }
+        off[b] = lo;
+    }
+}
+
 // offsets[b] = first sorted position with key >= b, for b in [0, nb]
 __global__ void k_block_offsets(const uint32_t *sorted_keys, int64_t n, int64_t nb, int64_t *off) {
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i <= n; i += (int64_t)gridDim.x * blockDim.x) {
@@ -71,6 +102,21 @@ struct WfArgs {
     int64_t n_cols;       // column groups are balanced segments [floor(g n / c), floor((g+1) n / c))
 };
 
+// Column lock acquire: test-and-test-and-set.  Waiters poll with plain relaxed loads (served by the L2
+// slice, no read-modify-write) and try the compare-and-swap only when the lock reads free, with a short
+// growing back-off, so ~1,000 waiting warps do not flood the L2 atomic units the running workers' row
+// traffic goes through.
+__device__ __forceinline__ void lock_acquire(int32_t *lock) {
+    unsigned ns = 32;
+    for (;;) {
+        int32_t cur;
+        asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(cur) : "l"(lock) : "memory");
+        if (cur == 0 && atomicCAS(lock, 0, 1) == 0) break;
+        __nanosleep(ns);
+        if (ns < 256) ns <<= 1;
+    }
+}
+
 __device__ __forceinline__ int64_t globaltimer() {
     int64_t t;
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -80,6 +126,7 @@ __device__ __forceinline__ int64_t globaltimer() {
 template <class SH, int D>
 __global__ void __launch_bounds__(kBlock) k_wavefront(WfArgs a) {
     static_assert(SH::L == 32, "wavefront worker is a full warp");
+    static_assert(D >= 1 && D <= 16, "in-block pipeline depth");
     const int lane = threadIdx.x & 31;
     const int w = (blockIdx.x * kBlock + threadIdx.x) >> 5;
     if (w >= a.s) return;
@@ -90,16 +137,33 @@ __global__ void __launch_bounds__(kBlock) k_wavefront(WfArgs a) {
     for (int j = 0; j < c; j++) {
         const int col = a.latin ? a.seq[(a.seq[c + w] + j) % c] : a.seq[(int64_t)w * c + j];
         int32_t *lock = a.locks + col;
-        if (lane == 0)
-            while (atomicCAS(lock, 0, 1) != 0) __nanosleep(64);
+        const int64_t blk = (int64_t)w * c + col;
+        const int64_t lo = a.off[blk], hi = a.off[blk + 1];
+        // The block's triples are this worker's alone: fetch the first two 32-sample tiles (lane i holds
+        // sample tb + i) before taking the lock, so only the Q rows wait for it.
+        int64_t tb = lo;
+        int32_t cu = 0, cv = 0, nu = 0, nv = 0;
+        float cr = 0.f, nr = 0.f;
+        {
+            const int64_t i0 = lo + lane, i1 = lo + 32 + lane;
+            if (i0 < hi) cu = __ldg(a.u + i0), cv = __ldg(a.v + i0), cr = __ldg(a.r + i0);
+            if (i1 < hi) nu = __ldg(a.u + i1), nv = __ldg(a.v + i1), nr = __ldg(a.r + i1);
+        }
+        if (lane == 0) lock_acquire(lock);
         __syncwarp();
         __threadfence();  // acquire: the previous holder's stores are visible (loads are .cg)
         const int64_t t0 = a.trace ? globaltimer() : 0;
-        const int64_t blk = (int64_t)w * c + col;
-        const int64_t lo = a.off[blk], hi = a.off[blk + 1];
         done += (uint64_t)(hi - lo);
 
-        // ring of D prefetched samples, history of the D last written rows
+        // sample j's triple from the two tiles held in registers (j warp-uniform, tb <= j < tb + 64)
+        auto triple = [&](int64_t jj, int32_t &uu, int32_t &vv, float &rr) {
+            const int o = (int)(jj - tb);
+            const bool in_cur = o < 32;
+            uu = __shfl_sync(0xffffffffu, in_cur ? cu : nu, o & 31);
+            vv = __shfl_sync(0xffffffffu, in_cur ? cv : nv, o & 31);
+            rr = __shfl_sync(0xffffffffu, in_cur ? cr : nr, o & 31);
+        };
+        // ring of D prefetched samples (rows loaded D samples ahead), history of the D last written rows
         int32_t ru[D], rv[D];
         float rr[D];
         RowRaw<SH> rp[D], rq[D];
@@ -109,11 +173,10 @@ __global__ void __launch_bounds__(kBlock) k_wavefront(WfArgs a) {
         for (int d = 0; d < D; d++) {
             hu[d] = -1;
             hv[d] = -1;
-            const int64_t i = lo + d;
-            const bool ok = i < hi;
-            ru[d] = ok ? __ldg(a.u + i) : 0;
-            rv[d] = ok ? __ldg(a.v + i) : 0;
-            rr[d] = ok ? __ldg(a.r + i) : 0.f;
+            const bool ok = lo + d < hi;
+            ru[d] = rv[d] = 0;
+            rr[d] = 0.f;
+            if (ok) triple(lo + d, ru[d], rv[d], rr[d]);
             load_row<SH>(a.P, ru[d], k, lane, ok, rp[d]);
             load_row<SH>(a.Q, rv[d], k, lane, ok, rq[d]);
         }
@@ -144,12 +207,19 @@ __global__ void __launch_bounds__(kBlock) k_wavefront(WfArgs a) {
                     hv[d] = rv[d];
                     hp[d] = pr;
                     hq[d] = qr;
-                    // refill this slot with sample i + D
+                    // refill this slot with sample i + D (its triple is in the register tiles)
                     const int64_t nx = i + D;
+                    if (nx - tb >= 32) {  // warp-uniform: the current tile is used up, slide by 32
+                        tb += 32;
+                        cu = nu, cv = nv, cr = nr;
+                        const int64_t i1 = tb + 32 + lane;
+                        nu = 0, nv = 0, nr = 0.f;
+                        if (i1 < hi) nu = __ldg(a.u + i1), nv = __ldg(a.v + i1), nr = __ldg(a.r + i1);
+                    }
                     const bool ok = nx < hi;
-                    ru[d] = ok ? __ldg(a.u + nx) : 0;
-                    rv[d] = ok ? __ldg(a.v + nx) : 0;
-                    rr[d] = ok ? __ldg(a.r + nx) : 0.f;
+                    ru[d] = rv[d] = 0;
+                    rr[d] = 0.f;
+                    if (ok) triple(nx, ru[d], rv[d], rr[d]);
                     load_row<SH>(a.P, ru[d], k, lane, ok, rp[d]);
                     load_row<SH>(a.Q, rv[d], k, lane, ok, rq[d]);
                 }
@@ -463,6 +533,156 @@ cudaError_t dispatch_cta_shape(const ShapeId &s, F &&f) {
     return cudaErrorInvalidValue;
 }
 
+// ------------------------------------------------- q-stationary CTA workers --
+// MF_OPT_WAVE_CTA = 3: worker = one 1024-thread CTA per SM holding column group c (the column lock as in
+// the other forms).  The block's samples are sorted by Q row (stable, so each row's samples keep the
+// shuffled order): the block is a set of runs, one per Q row.  The CTA's warps claim runs; a warp keeps
+// its run's q_v in registers for the whole run (q_v is touched by no other warp or CTA while the column
+// lock is held) and streams the run's p_u rows, D of them in flight, with register forwarding when a
+// p_u repeats inside the ring (a duplicate rating).  So no two concurrent updates ever share a Q row
+// -- the in-block Hogwild! races of the staged form (128 ratings in flight on a ~120-row group on the
+// Netflix shape) are gone -- and only p_u (read + write) and the triples cross L2 per rating; q_v
+// crosses once per run.  Each sample's update is exactly the paper's from the snapshot
+// (p_u, q_v); q_v is rounded to storage after every update, as the serial oracle does.  Runs of
+// different warps race only on P rows they share (a user with two items of the group).
+template <class SH, int D, int THREADS>
+__global__ void __launch_bounds__(THREADS, 1) k_wavefront_q(WfArgs a) {
+    static_assert(SH::L == 32, "a run is processed by one full warp");
+    extern __shared__ int32_t run_start[];  // nrows + 1 entries for the current block
+    __shared__ int s_col, s_next;
+    const int lane = threadIdx.x & 31;
+    const int w = blockIdx.x;
+    if (w >= a.s) return;  // CTA-uniform
+    const int k = SH::FULL ? SH::KMAX : a.k;
+    const int c = a.c;
+    const int nthreads = blockDim.x;
+    const int active_warps = a.min_per_group > 0 ? a.min_per_group : THREADS / 32;  // warps claiming runs
+    float chk = 0.f;
+    unsigned long long done = 0;
+    for (int j = 0; j < c; j++) {
+        if (threadIdx.x == 0) {
+            const int col = a.latin ? a.seq[(a.seq[c + w] + j) % c] : a.seq[(int64_t)w * c + j];
+            lock_acquire(a.locks + col);
+            __threadfence();  // acquire
+            s_col = col;
+            s_next = 0;
+        }
+        __syncthreads();
+        const int col = s_col;
+        const int64_t q0 = seg_begin(a.n_cols, c, col);
+        const int nrows = (int)(seg_begin(a.n_cols, c, col + 1) - q0);
+        const int64_t blk = (int64_t)w * c + col;
+        const int64_t lo = a.off[blk], hi = a.off[blk + 1];
+        const int64_t t0 = a.trace ? globaltimer() : 0;
+        // run table: run_start[r] = first block position whose Q row is >= q0 + r, r in [0, nrows]
+        for (int64_t i = lo + threadIdx.x; i < hi; i += nthreads) {
+            const int vl = (int)(__ldg(a.v + i) - q0);
+            const int prev = i > lo ? (int)(__ldg(a.v + i - 1) - q0) : -1;
+            for (int rr = prev + 1; rr <= vl; rr++) run_start[rr] = (int)(i - lo);
+        }
+        {
+            const int last = hi > lo ? (int)(__ldg(a.v + hi - 1) - q0) : -1;
+            for (int rr = last + 1 + (int)threadIdx.x; rr <= nrows; rr += nthreads) run_start[rr] = (int)(hi - lo);
+        }
+        __syncthreads();
+        if ((int)(threadIdx.x >> 5) < active_warps) {
+            for (;;) {
+                int r = 0;
+                if (lane == 0) r = atomicAdd(&s_next, 1);
+                r = __shfl_sync(0xffffffffu, r, 0);
+                if (r >= nrows) break;  // warp-uniform
+                const int64_t rb = lo + run_start[r], re = lo + run_start[r + 1];
+                if (rb == re) continue;
+                const int64_t vrow = q0 + r;
+                done += (uint64_t)(re - rb);
+                RowRaw<SH> qraw;
+                load_row<SH>(a.Q, vrow, k, lane, true, qraw);
+                // triples of the run from two 32-sample register tiles (lane i: sample tb + i)
+                int64_t tb = rb;
+                int32_t cu = 0, nu = 0;
+                float cr = 0.f, nr = 0.f;
+                {
+                    const int64_t i0 = rb + lane, i1 = rb + 32 + lane;
+                    if (i0 < re) cu = __ldg(a.u + i0), cr = __ldg(a.r + i0);
+                    if (i1 < re) nu = __ldg(a.u + i1), nr = __ldg(a.r + i1);
+                }
+                auto triple = [&](int64_t jj, int32_t &uu, float &rr_) {
+                    const int o = (int)(jj - tb);
+                    const bool in_cur = o < 32;
+                    uu = __shfl_sync(0xffffffffu, in_cur ? cu : nu, o & 31);
+                    rr_ = __shfl_sync(0xffffffffu, in_cur ? cr : nr, o & 31);
+                };
+                int32_t ru[D], hu[D];
+                float rr[D];
+                RowRaw<SH> rp[D];
+#pragma unroll
+                for (int d = 0; d < D; d++) {
+                    hu[d] = -1;
+                    const bool ok = rb + d < re;
+                    ru[d] = 0;
+                    rr[d] = 0.f;
+                    if (ok) triple(rb + d, ru[d], rr[d]);
+                    load_row<SH>(a.P, ru[d], k, lane, ok, rp[d]);
+                }
+                float q[SH::E];
+                widen_row<SH>(qraw, q);
+                for (int64_t base = rb; base < re; base += D) {
+#pragma unroll
+                    for (int d = 0; d < D; d++) {
+                        const int64_t i = base + d;
+                        if (i < re) {  // warp-uniform
+                            RowRaw<SH> pr = rp[d];
+                            // p_u written by one of the D - 1 samples since this load was issued (a
+                            // duplicate rating inside the ring, rare): read it again -- the same lanes
+                            // stored it, so program order makes the new value visible
+                            bool hit = false;
+#pragma unroll
+                            for (int t = 1; t < D; t++) hit |= hu[(d + t) % D] == ru[d];
+                            if (hit) load_row<SH>(a.P, ru[d], k, lane, true, pr);
+                            float p[SH::E];
+                            widen_row<SH>(pr, p);
+                            const float err = rr[d] - group_dot<SH>(p, q);
+                            chk = fmaf(err, 0.f, chk);
+                            sgd_step<SH>(p, q, err, a.eta, a.lam);
+                            narrow_row<SH>(p, pr);
+                            narrow_row<SH>(q, qraw);
+                            widen_row<SH>(qraw, q);  // q_v as stored after this update (serial semantics)
+                            store_row<SH>(a.P, ru[d], k, lane, true, pr);
+                            hu[d] = ru[d];
+                            const int64_t nx = i + D;
+                            if (nx - tb >= 32) {  // warp-uniform: slide the triple tiles
+                                tb += 32;
+                                cu = nu, cr = nr;
+                                const int64_t i1 = tb + 32 + lane;
+                                nu = 0, nr = 0.f;
+                                if (i1 < re) nu = __ldg(a.u + i1), nr = __ldg(a.r + i1);
+                            }
+                            const bool ok = nx < re;
+                            ru[d] = 0;
+                            rr[d] = 0.f;
+                            if (ok) triple(nx, ru[d], rr[d]);
+                            load_row<SH>(a.P, ru[d], k, lane, ok, rp[d]);
+                        }
+                    }
+                }
+                store_row<SH>(a.Q, vrow, k, lane, true, qraw);
+            }
+        }
+        if (a.trace && threadIdx.x == 0) {
+            int64_t *tr = a.trace + 4 * blk;
+            tr[0] = w;
+            tr[1] = blk;
+            tr[2] = t0;
+            tr[3] = globaltimer();
+        }
+        __threadfence();  // release: every thread's P and Q stores of this block before the unlock
+        __syncthreads();
+        if (threadIdx.x == 0) atomicExch(a.locks + col, 0);
+    }
+    if (chk != chk) a.scratch->diverged = 1;
+    if (a.count_updates && lane == 0 && done) atomicAdd(&a.scratch->updates, done);
+}
+
 ShapeId warp_shape(int k, int storage) {
     if (storage == kF32) {
         if (k == 128) return {storage, 32, 1, 16, 1};
@@ -511,14 +731,23 @@ void mf_ctx::release_wavefront() {
     wf_valid = false;
 }
 
-// Auto sizing: ~8 workers per SM, c = 2s column blocks, but
-// keep >= ~100 samples per block and s <= m, c <= n.
+// Auto sizing: up to 8 warp workers per SM, c = 2s column blocks (Latin-rectangle lock
+// utilisation ~95% at c/s = 2), blocks of >= ~32 samples, s <= m, c <= n.
 int mf_ctx::build_wavefront() {
     if (wf_valid) return MF_OK;
     release_wavefront();
     const int64_t rows = p_rows();
     int s = wave_rows, c = wave_cols;
-    if (wave_cta) {
+    if (wave_cta == 3) {
+        // q-stationary CTA workers: one per SM, c = s column groups (as many as the run table of a group,
+        // 4 B per Q row in shared memory, allows: <= 48K rows per group)
+        if (s <= 0) s = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)num_sms, rows));
+        if (c <= 0) {
+            int64_t cc = std::min<int64_t>((int64_t)s, n);
+            while (cc < n && (n + cc - 1) / cc > 48 * 1024) cc++;
+            c = (int)cc;
+        }
+    } else if (wave_cta) {
         // one CTA worker per SM; c = s column groups (the largest blocks: per-block lock, copy-in and
         // tail cost is amortised best -- Netflix shape, f16: c = s 11.8 G/s, 2s 10.0, 4s 7.7, 8s 6.2),
         // more if the largest group does not fit in shared memory (200 KB of the 227 KB per CTA)
@@ -532,7 +761,10 @@ int mf_ctx::build_wavefront() {
         }
     }
     if (s <= 0) {
-        const double by_blocks = std::sqrt((double)N / 200.0);
+        // warp workers: up to 8 per SM (1,184 on a B200), each with 4 samples of its block in flight, but
+        // blocks of >= ~32 samples (one register tile of triples) so the per-block lock hand-over (~1-2 us)
+        // stays small against the block's updates: s = sqrt(N / 64) with c = 2s
+        const double by_blocks = std::sqrt((double)N / 64.0);
         s = (int)std::max<double>(1.0, std::min<double>({(double)num_sms * 8, by_blocks, (double)rows}));
     }
     if (c <= 0) c = (int)std::min<int64_t>(2 * (int64_t)s, n);
@@ -554,14 +786,19 @@ int mf_ctx::build_wavefront() {
     CK(cudaMallocAsync((void **)&i0, sizeof(uint32_t) * N, st));
     CK(cudaMallocAsync((void **)&i1, sizeof(uint32_t) * N, st));
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((N + 255) / 256, 148 * 16));
-    k_block_keys<<<grid, 256, 0, st>>>(u, v, N, rows, n, s, c, k0, i0);
+    const bool runs = wave_cta == 3;
+    const uint64_t key_range = runs ? (uint64_t)s * (uint64_t)n : (uint64_t)nb;
+    if (key_range >= (1ull << 32)) return fail(MF_EINVAL, "wavefront: s * n too large for the run layout");
+    if (runs) k_run_keys<<<grid, 256, 0, st>>>(u, v, N, rows, n, s, k0, i0);
+    else k_block_keys<<<grid, 256, 0, st>>>(u, v, N, rows, n, s, c, k0, i0);
     CK(cudaGetLastError());
     int bits = 1;
-    while (bits < 32 && (1ull << bits) < (uint64_t)nb) bits++;
+    while (bits < 32 && (1ull << bits) < key_range) bits++;
     CK(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, k0, k1, i0, i1, N, 0, bits, st));
     CK(cudaMallocAsync(&tmp, tmp_bytes, st));
     CK(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, k0, k1, i0, i1, N, 0, bits, st));  // stable
-    k_block_offsets<<<grid, 256, 0, st>>>(k1, N, nb, wf_off);
+    if (runs) k_run_block_offsets<<<grid, 256, 0, st>>>(k1, N, s, c, n, wf_off);
+    else k_block_offsets<<<grid, 256, 0, st>>>(k1, N, nb, wf_off);
     CK(cudaGetLastError());
     CK(launch_gather(u, v, r, i1, N, fu, fv, fr, st));
     CK(cudaFreeAsync(tmp, st));
@@ -630,7 +867,34 @@ int mf_ctx::run_wavefront(const ShapeId &, const UpdateArgs &ua, int *launches, 
     a.eta = ua.eta;
     a.lam = ua.lam;
     a.n_cols = n;
-    if (wave_cta) {
+    if (wave_cta == 3) {
+        const size_t smem = (size_t)((n + c - 1) / c + 1) * sizeof(int32_t);  // run table
+        // MF_OPT_VARIANT bits 26..27: warps claiming runs, 0 -> all, 1 -> 1 (one run at a time: the block
+        // is processed serially in run order), 2 -> 8, 3 -> 16; bits 4..7: p rows in flight per warp,
+        // 0 -> 4 (1024-thread CTA, 128 rows in flight per SM, 64 registers), 8 -> 8 (512-thread CTA,
+        // the same 128 in flight, 128 registers), 2 -> 2 (1024 threads)
+        {
+            const int sel = (variant_eff >> 26) & 0x3;
+            a.min_per_group = sel == 0 ? 0 : sel == 1 ? 1 : sel == 2 ? 8 : 16;
+        }
+        const int dsel = (variant_eff >> 4) & 0xF;
+        const int depth = dsel == 2 || dsel == 8 ? dsel : 4;
+        const ShapeId sh = warp_shape(k, storage);
+        CK(dispatch_warp_shape(sh, [&](auto tag) -> cudaError_t {
+            using SH = decltype(tag);
+            auto launch = [&](auto kern, int threads) -> cudaError_t {
+                cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+                if (e != cudaSuccess) return e;
+                kern<<<s, threads, smem, st>>>(a);
+                return cudaGetLastError();
+            };
+            if constexpr (SH::FULL) {
+                if (depth == 8) return launch(k_wavefront_q<SH, 8, 512>, 512);
+                if (depth == 4) return launch(k_wavefront_q<SH, 4, 1024>, 1024);
+            }
+            return launch(k_wavefront_q<SH, 2, 1024>, 1024);
+        }));
+    } else if (wave_cta) {
         const int64_t row_bytes = (int64_t)k * storage_bytes();
         const int64_t max_rows = (n + c - 1) / c;  // balanced column groups
         const size_t smem = (size_t)(max_rows * row_bytes);
@@ -685,10 +949,18 @@ int mf_ctx::run_wavefront(const ShapeId &, const UpdateArgs &ua, int *launches, 
     } else {
         const ShapeId sh = warp_shape(k, storage);
         const int blocks = (s * 32 + kBlock - 1) / kBlock;
-        const int depth = ((variant_eff >> 4) & 0xF) == 4 ? 4 : 2;  // samples of a block in flight per warp
+        // samples of a block in flight per warp (MF_OPT_VARIANT bits 4..7: 2, 4 or 8; 0 = 4 for the full-row
+        // shapes).  The triples come from two 32-sample register tiles fetched before the lock, so the
+        // only latency on a sample's path is its row loads, issued `depth` samples ahead.
+        const int dsel = (variant_eff >> 4) & 0xF;
+        const int depth = dsel == 2 || dsel == 8 ? dsel : 4;
         CK(dispatch_warp_shape(sh, [&](auto tag) -> cudaError_t {
             using SH = decltype(tag);
             if constexpr (SH::FULL) {
+                if (depth == 8) {
+                    k_wavefront<SH, 8><<<blocks, kBlock, 0, st>>>(a);
+                    return cudaGetLastError();
+                }
                 if (depth == 4) {
                     k_wavefront<SH, 4><<<blocks, kBlock, 0, st>>>(a);
                     return cudaGetLastError();

@@ -2,6 +2,12 @@
 # pattern's ceiling under ncu, and per-config DRAM traffic of the update kernels (C2, C3, C4)
 set -x
 mkdir -p gpurun_out
+timeout 900 python -m pytest tests/test_gpu_wavefront.py -x -q -p no:cacheprovider > gpurun_out/r02d_pytest_wavefront.log 2>&1
+tail -3 gpurun_out/r02d_pytest_wavefront.log
+for c in "C2 f16,f32" "C3 f16"; do set -- $c
+  timeout 600 python scripts/probe.py --cfg $1 --epochs 3 --storage $2 --variants 32,64,128 --sched wavefront > gpurun_out/r02d_warp_wavefront_$1.log 2>&1
+done
+cat gpurun_out/r02d_warp_wavefront_*.log
 NV="nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo"
 $NV -o /tmp/l2c scripts/l2_ceiling.cu && $NV -o /tmp/smc scripts/sgd_mem_ceiling.cu
 timeout 300 /tmp/l2c > gpurun_out/r02d_l2_ceiling.jsonl 2>&1

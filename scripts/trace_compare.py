@@ -27,7 +27,9 @@ def main():
     a = ap.parse_args()
     cfg = datagen.CONFIGS[a.cfg]
     (u, v, r), test = datagen.make(cfg)
-    for sch in a.scheds.split(","):
+    for spec in a.scheds.split(","):
+        # schedule[@option=value@...]: extra MF options, e.g. wavefront_cta@variant=134217728
+        sch, *extra = spec.split("@")
         opts = {"wave_cta": 1} if sch.startswith("wavefront_cta") else {}
         name = "wavefront" if sch.startswith("wavefront_cta") else sch
         if sch.startswith("wavefront_cta:"):  # wavefront_cta:c -- c column groups
@@ -41,14 +43,17 @@ def main():
                 opts["workers"] = int(f[3])
             if len(f) > 4:  # partitioned:G:S:workers:split
                 opts["part_split"] = int(f[4])
+        for kv in extra:
+            opts[kv.split("=")[0]] = int(kv.split("=")[1])
         with mf.MF(cfg.m, cfg.n, cfg.k, cfg.alpha, cfg.lam, cfg.seed_init, storage=a.storage, beta=cfg.beta,
                    seed_shuffle=cfg.seed_shuffle, **opts) as g:
             g.load(u, v, r)
-            tr = []
+            tr, ks = [], []
             for _ in range(a.epochs):
-                g.epoch(name)
+                ks.append(g.epoch(name).kernel_seconds)
                 tr.append(g.rmse(*test))
-        print(json.dumps({"cfg": cfg.name, "storage": a.storage, "schedule": sch, "rmse": tr}), flush=True)
+        print(json.dumps({"cfg": cfg.name, "storage": a.storage, "schedule": spec, "rmse": tr,
+                          "kernel_s": ks}), flush=True)
 
 
 if __name__ == "__main__":

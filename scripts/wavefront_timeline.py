@@ -24,11 +24,12 @@ def main():
     ap.add_argument("--storage", default="f16")
     ap.add_argument("--epochs", type=int, default=4)
     ap.add_argument("--variant", type=int, default=0)
+    ap.add_argument("--wave-cta", type=int, default=1, help="0 = warp workers, 1 = staged CTA, 3 = q-stationary CTA")
     a = ap.parse_args()
     cfg = datagen.CONFIGS[a.cfg]
     (u, v, r), test = datagen.make(cfg)
     with mf.MF(cfg.m, cfg.n, cfg.k, cfg.alpha, cfg.lam, cfg.seed_init, storage=a.storage, beta=cfg.beta, shuffle=0,
-               wave_cta=1, trace=1, variant=a.variant) as g:
+               wave_cta=a.wave_cta, trace=1, variant=a.variant) as g:
         g.load(u, v, r)
         for e in range(a.epochs):
             st = g.epoch("wavefront")

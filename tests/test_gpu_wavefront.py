@@ -115,6 +115,120 @@ def test_wavefront_single_worker_is_serial_block_order(mfmod):
     assert np.linalg.norm(Q - ref.Q) / np.linalg.norm(ref.Q) <= 1e-5
 
 
+def _trace_order(mfmod, rec, perm, u, v, m, n, s, c, by_row=False):
+    """Serial order of a wavefront epoch reconstructed from its audit trace: blocks by start time, each
+    block's samples in stored (shuffled) order.  Blocks of one column never overlap in time and blocks
+    of one band run on one worker in sequence, so sorting by start time orders every pair of blocks that
+    share a row or a column as the GPU ran them; blocks that overlap in time share neither."""
+    band = np.searchsorted([mfmod.mf_segment(m, s, w)[1] for w in range(s)], u[perm], side="right")
+    grp = np.searchsorted([mfmod.mf_segment(n, c, g)[1] for g in range(c)], v[perm], side="right")
+    key = band.astype(np.int64) * c + grp
+    if by_row:  # q-stationary layout: inside a block the samples are sorted by Q row (stable)
+        order_pos = np.lexsort((np.arange(len(perm)), v[perm], key))
+        by_blk = {}
+        for pos in order_pos:
+            by_blk.setdefault(int(key[pos]), []).append(pos)
+        return np.concatenate([perm[np.asarray(by_blk.get(int(b), []), dtype=np.int64)]
+                               for b in rec[np.argsort(rec[:, 2]), 1]])
+    by_blk = {}
+    for pos in np.argsort(key, kind="stable"):
+        by_blk.setdefault(int(key[pos]), []).append(pos)
+    order = [perm[np.asarray(by_blk.get(int(b), []), dtype=np.int64)] for b in rec[np.argsort(rec[:, 2]), 1]]
+    return np.concatenate(order)
+
+
+@pytest.mark.parametrize("storage", [0, 1])
+@pytest.mark.parametrize("s,c,depth", [(8, 16, 2), (8, 16, 4), (8, 16, 8), (0, 0, 0), (24, 30, 4)])
+def test_wavefront_equals_serial_sweep_in_trace_order(mfmod, storage, s, c, depth):
+    """The paper-literal wavefront (warp workers, serial blocks, column locks) with D samples of a block in
+    flight and register forwarding is exactly serial SGD over the blocks in the order the audit trace
+    shows: its factors after 2 epochs equal the oracle's over that order (fp32 1e-5, fp16 2e-3)."""
+    cfg = datagen.CONFIGS["C1"]
+    (u, v, r), _ = datagen.make(cfg)
+    st = {0: oracle.F32, 1: oracle.F16}[storage]
+    ref = oracle.Model(cfg.m, cfg.n, cfg.k, st, seed=cfg.seed_init)
+    with mfmod.MF(cfg.m, cfg.n, cfg.k, cfg.alpha, cfg.lam, cfg.seed_init, storage=storage, beta=cfg.beta,
+                  wave_rows=s, wave_cols=c, trace=1, count_updates=1, seed_shuffle=cfg.seed_shuffle,
+                  variant=depth << 4) as g:
+        g.load(u, v, r)
+        perm = g.order()
+        for e in range(2):
+            stt = g.epoch("wavefront")
+            assert stt.updates == len(u)
+            ss = stt.workers
+            cc = c or int(g.get(mfmod.MF_OPT_WAVE_COLS)) or 2 * ss
+            rec = mfmod.mf_wavefront_trace(g.h, ss * cc + 10)
+            assert _audit(rec, ss, cc) == 0
+            ref.epoch(u, v, r, oracle.eta(cfg.alpha, cfg.beta, e), cfg.lam,
+                      _trace_order(mfmod, rec, perm, u, v, cfg.m, cfg.n, ss, cc))
+        P, Q = g.factors()
+    Pr, Qr = ref.factors_f32()
+    tol = {0: 1e-5, 1: 2e-3}[storage]
+    assert np.linalg.norm(P - Pr) / np.linalg.norm(Pr) <= tol
+    assert np.linalg.norm(Q - Qr) / np.linalg.norm(Qr) <= tol
+
+
+# ------------------------------------------------- q-stationary CTA workers --
+@pytest.mark.parametrize("storage", [0, 1])
+@pytest.mark.parametrize("s,c", [(1, 1), (4, 6), (0, 0)])
+def test_wavefront_q_one_warp_equals_serial_sweep_in_trace_order(mfmod, storage, s, c):
+    """MF_OPT_WAVE_CTA = 3 with one warp claiming runs per CTA (MF_OPT_VARIANT bits 26..27 = 1): every
+    block is processed serially run by run (its samples sorted by Q row, stable, so each row keeps the
+    shuffled order), q_v held in registers and rounded to storage after every update, p_u rows D = 4
+    deep.  The factors after 2 epochs equal the oracle's over the blocks in audit-trace order
+    (fp32 1e-5, fp16 2e-3); s = c = 1 is serial SGD over the stored order sorted by item."""
+    cfg = datagen.CONFIGS["C1"]
+    (u, v, r), _ = datagen.make(cfg)
+    st = {0: oracle.F32, 1: oracle.F16}[storage]
+    ref = oracle.Model(cfg.m, cfg.n, cfg.k, st, seed=cfg.seed_init)
+    with mfmod.MF(cfg.m, cfg.n, cfg.k, cfg.alpha, cfg.lam, cfg.seed_init, storage=storage, beta=cfg.beta,
+                  wave_rows=s, wave_cols=c, wave_cta=3, trace=1, count_updates=1, seed_shuffle=cfg.seed_shuffle,
+                  variant=1 << 26) as g:
+        g.load(u, v, r)
+        perm = g.order()
+        for e in range(2):
+            stt = g.epoch("wavefront")
+            assert stt.updates == len(u)
+            ss = stt.workers
+            cc = c or int(g.get(mfmod.MF_OPT_WAVE_COLS))
+            rec = mfmod.mf_wavefront_trace(g.h, ss * cc + 10)
+            assert _audit(rec, ss, cc) == 0
+            ref.epoch(u, v, r, oracle.eta(cfg.alpha, cfg.beta, e), cfg.lam,
+                      _trace_order(mfmod, rec, perm, u, v, cfg.m, cfg.n, ss, cc, by_row=True))
+        P, Q = g.factors()
+    Pr, Qr = ref.factors_f32()
+    tol = {0: 1e-5, 1: 2e-3}[storage]
+    assert np.linalg.norm(P - Pr) / np.linalg.norm(Pr) <= tol
+    assert np.linalg.norm(Q - Qr) / np.linalg.norm(Qr) <= tol
+
+
+@pytest.mark.parametrize("storage", [0, 1])
+@pytest.mark.parametrize("depth", [0, 2, 8])
+def test_wavefront_q_exactly_once_conflict_free_and_rmse(mfmod, storage, depth):
+    """All warps claiming runs (default), each p_u ring depth: every sample once per epoch, no column
+    conflict in the audit, and one run's test RMSE within 0.5% of the serial oracle's on the 10% Netflix
+    slice at the storage's gate epoch (reading T5; oracle goldens tests/golden/C2-10pct_*)."""
+    import json
+    import os
+    cfg = datagen.CONFIGS["C2-10pct"]
+    stname = {0: "f32", 1: "f16"}[storage]
+    path = os.path.join(os.path.dirname(__file__), "golden", f"C2-10pct_{stname}_trace.json")
+    gold = json.load(open(path))["rmse"]
+    E = {0: 10, 1: 6}[storage]
+    (u, v, r), test = datagen.make(cfg)
+    with mfmod.MF(cfg.m, cfg.n, cfg.k, cfg.alpha, cfg.lam, cfg.seed_init, storage=storage, beta=cfg.beta,
+                  wave_cta=3, trace=1, count_updates=1, seed_shuffle=cfg.seed_shuffle, variant=depth << 4) as g:
+        g.load(u, v, r)
+        for e in range(E):
+            stt = g.epoch("wavefront")
+            assert stt.updates == len(u)
+            if e == 0:
+                ss, cc = stt.workers, int(g.get(mfmod.MF_OPT_WAVE_COLS))
+                assert _audit(mfmod.mf_wavefront_trace(g.h, ss * cc + 10), ss, cc) == 0
+        got = g.rmse(*test)
+    assert abs(got - gold[E - 1]) <= 0.005 * gold[E - 1], (got, gold[E - 1])
+
+
 # ------------------------------------------------------- CTA workers (smem Q) --
 def test_wavefront_cta_exactly_once_conflict_free_and_rmse(mfmod):
     """MF_OPT_WAVE_CTA=1: one CTA per SM, the column group's Q rows in shared memory."""
