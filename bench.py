@@ -85,12 +85,14 @@ SHAPE_NAME = {"C1": "planted rank-8 parity config", "C2": "Netflix-shaped", "C3"
 
 
 def roofline(cfg, storage, N, k_s, traffic, schedule):
-    """Roofline object of the update kernel.  Its algorithmic bytes B_alg = 12 + 4kb per update (SURVEY
-    §8(d)) all pass through L2 (triple, p_u and q_v read, both rows written; the CTA wavefront keeps q_v on
-    chip, so 12 + 2kb reach L2), so the primary bound is the L2's measured ceiling for random-row
-    read-modify-write; `hbm` relates the DRAM bytes (ncu, per launch, when captured for this config) or,
-    failing that, the compulsory 12 + 2kb (R stream + P rows; Q is L2-resident at every configured shape)
-    to the measured HBM copy peak."""
+    """Roofline object of the update kernel, against the resource that binds it.
+
+    L2: the algorithmic bytes B_alg = 12 + 4kb per update all pass through L2 (triple,
+    p_u and q_v read, both rows written; the CTA wavefront keeps q_v on chip, so 12 + 2kb reach L2),
+    against the L2's measured ceiling for random-row read-modify-write.  HBM: the DRAM bytes of one
+    launch (ncu, when captured for this config) or, failing that, the compulsory 12 + 2kb (R stream + P
+    rows; Q is L2-resident at every configured shape), against the measured HBM copy peak.  `bound` is
+    the one of the two the kernel is closer to (the larger fraction); both are reported."""
     b = 4 if storage == "f32" else 2
     hbm, hbm_kind = peaks()
     on_chip_q = schedule == "wavefront_cta"
@@ -98,22 +100,24 @@ def roofline(cfg, storage, N, k_s, traffic, schedule):
     B_l2 = 12 + 2 * cfg.k * b if on_chip_q else B
     l2_rows, l2_stream = l2_peaks(cfg.k * b)
     b_hbm = 12 + 2 * cfg.k * b
-    roof = {"bound": "l2" if l2_rows else "hbm", "achieved": B_l2 * N / k_s / 1e9,
-            "peak": l2_rows if l2_rows else hbm, "unit": "GB/s", "traffic": traffic,
-            "peak_kind": ("measured L2 random-row RMW ceiling, %d-B rows (scripts/l2_ceiling.cu, "
-                          "profiles/r02_l2_ceiling.jsonl)" % (cfg.k * b)) if l2_rows else hbm_kind,
-            "bytes_per_update_alg": B, "bytes_per_update_l2": B_l2, "updates_per_launch": N,
-            "kernel_ms": k_s * 1e3}
-    roof["frac"] = roof["achieved"] / roof["peak"]
-    if l2_stream:
-        roof["l2_stream_rw_peak"] = l2_stream
     dram = traffic / N if traffic else b_hbm
-    roof["hbm"] = {"achieved": dram * N / k_s / 1e9, "peak": hbm, "peak_kind": hbm_kind, "unit": "GB/s",
-                   "frac": dram * N / k_s / 1e9 / hbm, "bytes_per_update": dram,
-                   "basis": "ncu dram__bytes_read+write of one launch" if traffic else
-                            "compulsory 12 + 2kb (R + P rows; Q L2-resident)",
-                   "frac_compulsory": b_hbm * N / k_s / 1e9 / hbm,
-                   "frac_alg_bytes": B * N / k_s / 1e9 / hbm}
+    l2 = None
+    if l2_rows:
+        l2 = {"achieved": B_l2 * N / k_s / 1e9, "peak": l2_rows, "unit": "GB/s",
+              "peak_kind": "measured L2 random-row RMW ceiling, %d-B rows (scripts/l2_ceiling.cu, "
+                           "profiles/r02_l2_ceiling.jsonl)" % (cfg.k * b),
+              "bytes_per_update": B_l2, "stream_rw_peak": l2_stream}
+        l2["frac"] = l2["achieved"] / l2["peak"]
+    hb = {"achieved": dram * N / k_s / 1e9, "peak": hbm, "peak_kind": hbm_kind, "unit": "GB/s",
+          "frac": dram * N / k_s / 1e9 / hbm, "bytes_per_update": dram,
+          "basis": "ncu dram__bytes_read+write of one launch" if traffic else
+                   "compulsory 12 + 2kb (R + P rows; Q L2-resident)",
+          "frac_compulsory": b_hbm * N / k_s / 1e9 / hbm, "frac_alg_bytes": B * N / k_s / 1e9 / hbm}
+    top = l2 if l2 and l2["frac"] >= hb["frac"] else hb
+    roof = {"bound": "l2" if top is l2 else "hbm", "achieved": top["achieved"], "peak": top["peak"],
+            "unit": "GB/s", "frac": top["frac"], "traffic": traffic, "peak_kind": top["peak_kind"],
+            "bytes_per_update_alg": B, "updates_per_launch": N, "kernel_ms": k_s * 1e3,
+            "l2": l2, "hbm": hb}
     return roof
 
 
@@ -441,12 +445,14 @@ def main():
             res["roofline_frac"] = rf["frac"]
             res["roofline_bound"] = rf["bound"]
             res["hbm_frac"] = rf["hbm"]["frac"]
+            res["l2_frac"] = (rf["l2"] or {}).get("frac")
             # against the memory-pattern ceiling of the kernel's own global traffic (p+q rows for
             # batch-Hogwild!, p rows only for the CTA wavefront whose Q group is on chip)
             ceil = load_pattern_ceiling(cfg, st_, p_only=(sch == "wavefront")) if sch != "deterministic" else None
             res["frac_of_pattern_ceiling"] = (N / res["kernel_s"]) / ceil if ceil else None
             others[key] = {k_: res[k_] for k_ in ("value", "ms", "kernel_s", "rmse", "workers", "alg_GBps",
-                                                  "roofline_bound", "roofline_frac", "hbm_frac", "epochs_done",
+                                                  "roofline_bound", "roofline_frac", "hbm_frac", "l2_frac",
+                                                  "epochs_done",
                                                   "variant", "frac_of_pattern_ceiling")}
 
     if not a.no_variants and not a.no_c4 and a.config != "C4":
@@ -541,7 +547,7 @@ def c4_leg(mf, stream, local, storage, epochs=5):
         rf = roofline(cfg, storage, N, k_s, load_traffic(storage, "C4", sname), sname)
         out[key + "/" + storage] = {"value": N / k_s, "kernel_s": k_s, "rmse_after_%d_epochs" % epochs: rm,
                                     "roofline_bound": rf["bound"], "roofline_frac": rf["frac"],
-                                    "hbm": rf["hbm"], "N": N}
+                                    "hbm": rf["hbm"], "l2_frac": (rf["l2"] or {}).get("frac"), "N": N}
     out["C4:note"] = ("kernel-timed (CUDA events inside libmf), inputs resident; host generation %.0f s; "
                       "partitioned_1 = MF_SCHED_PARTITIONED with one loopback partition: %d passes x 1 round of "
                       "two concurrent half-segment launches per epoch" % (gen_s, 4))

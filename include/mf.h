@@ -97,13 +97,16 @@ typedef enum {
                                  per SM with the column group's Q rows staged in shared memory, lock-free inside the block;
                                  2 = as 1 with two 512-thread CTA workers per SM */
     MF_OPT_STREAM_CHUNK = 18, /* mf_epoch_host: samples per streamed chunk (default 2^23) */
-    MF_OPT_PART_SPLIT = 19    /* partitioned: 2 = unit grid (default): 2G column units (segment halves), each family of
+    MF_OPT_PART_SPLIT = 19,   /* partitioned: 2 = unit grid (default): 2G column units (segment halves), each family of
                                  halves rotating by its own Latin square (a randomized G x 2G Latin rectangle per pass,
                                  P:525-535), the two units of a partition updated concurrently on two streams with half
                                  of its workers each, every unit's hand-over overlapping the other unit's updates
                                  (P:307-314); 0 = one launch per whole block, hand-over after it; 1 = each block as two
                                  half-segment sub-blocks in sequence with all workers each -- twice the ratings in flight
                                  per Q column, so further from serial SGD */
+    MF_OPT_R_STAGING = 20     /* batch-Hogwild! rating batches: 1 = registers (three coalesced 32-bit loads per lane per 32-sample
+                                 tile, handed to the groups by shuffles); 2 = staged in shared memory by the TMA engine (bulk
+                                 copies of each chunk's u, v, r, double-buffered per warp; needs 16-B aligned arrays, else 1) */
 } mf_option;
 
 typedef struct {

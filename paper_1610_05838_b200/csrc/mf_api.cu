@@ -323,6 +323,10 @@ extern "C" int mf_set_option(mf_ctx *ctx, int key, double value) {
             ctx->part_split = (int)iv;
             ctx->part_valid = false;
             return MF_OK;
+        case MF_OPT_R_STAGING:
+            if (iv < 1 || iv > 2) return ctx->fail(MF_EINVAL, "R staging must be 1 (registers) or 2 (TMA)");
+            ctx->r_stage = (int)iv;
+            return MF_OK;
         case MF_OPT_STREAM_CHUNK:
             if (iv < 32 || iv > (1ll << 34)) return ctx->fail(MF_EINVAL, "stream chunk must be in [32, 2^34]");
             ctx->stream_chunk = iv;
@@ -358,6 +362,7 @@ extern "C" int mf_get_option(const mf_ctx *ctx, int key, double *value) {
         case MF_OPT_WAVE_CTA: *value = ctx->wave_cta; return MF_OK;
         case MF_OPT_STREAM_CHUNK: *value = (double)ctx->stream_chunk; return MF_OK;
         case MF_OPT_PART_SPLIT: *value = ctx->part_split; return MF_OK;
+        case MF_OPT_R_STAGING: *value = ctx->r_stage; return MF_OK;
         default: return MF_EINVAL;
     }
 }
@@ -558,6 +563,7 @@ UpdateArgs mf_ctx::update_args(float eta) const {
     a.batch_f = batch_f;
     a.count_updates = count_updates;
     a.scratch = scratch;
+    a.r_stage = r_stage;
     return a;
 }
 

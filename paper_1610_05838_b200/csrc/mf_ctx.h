@@ -37,6 +37,7 @@ struct mf_ctx {
                         // families with their own Latin squares, each hand-over overlapping the other's compute)
     int wave_cta = 0;   // wavefront worker = CTA with shared-memory Q group (MF_OPT_WAVE_CTA)
     int variant = 0;
+    int r_stage = 1;    // MF_OPT_R_STAGING: batch-Hogwild! triples 1 = registers, 2 = TMA bulk copies into shared memory
     int trace = 0;
     // L2 prefetch, auto mode (MF_OPT_VARIANT bits 16..19 = 0).  Whether a prefetch pays depends on
     // where the rows live (it hides DRAM latency, and costs L2 request slots where the L2 is the

@@ -172,9 +172,12 @@ __global__ void __launch_bounds__(kBlock) k_hogwild(UpdateArgs a) {
     // L2 eviction priorities: the triples are read once per epoch and would otherwise push P rows out
     // of L2 (1.2 GB of R per epoch streams past a 123-MB P on the Netflix shape), so they are marked
     // evict_first; optionally the factor rows evict_last (MF_OPT_VARIANT bits 28..29)
-    const uint64_t pol_r = a.cache_policy == 1 ? policy_evict_normal() : policy_evict_first();
-    const uint64_t pol_p = a.cache_policy == 2 ? policy_evict_last() : policy_evict_normal();
-    const uint64_t pol_q = a.cache_policy >= 2 ? policy_evict_last() : policy_evict_normal();
+    const int cp = a.cache_policy;
+    const uint64_t pol_r = cp == 1 ? policy_evict_normal() : policy_evict_first();
+    const uint64_t pol_p = cp == 2   ? policy_evict_last()
+                           : cp >= 4 ? policy_evict_last_frac((cp & 1) ? 0.75f : 0.5f)
+                                     : policy_evict_normal();
+    const uint64_t pol_q = cp == 2 || cp == 3 || cp >= 6 ? policy_evict_last() : policy_evict_normal();
     int32_t tu, tv;
     float tr;
     {
@@ -283,7 +286,192 @@ __global__ void __launch_bounds__(kBlock) k_hogwild(UpdateArgs a) {
     if (a.count_updates && lane == 0 && done) atomicAdd(&a.scratch->updates, done);
 }
 
+// ------------------------------------------------- batch-Hogwild!, TMA-staged R
+// The same schedule and update as k_hogwild, with the rating batches staged in shared memory by the
+// TMA engine (north star: "128-bit vectorised, coalesced loads of the COO triples, with TMA or
+// shared-memory staging of rating batches"): when a warp claims chunk c + 1, one lane issues three bulk
+// copies (cp.async.bulk, u / v / r of the chunk, 16-B granules) into the warp's second buffer, completing
+// on an mbarrier, while the warp updates chunk c from the first; a group reads its sample's triple from
+// shared memory.  Chunks are <= kStageF samples; a chunk's last len % 4 triples (not a 16-B granule)
+// are copied by the lanes.  Needs 16-B aligned u / v / r (the main epoch arrays; sub-ranges of the
+// partitioned layout use k_hogwild).
+static constexpr int kStageF = 256;
+static constexpr int kStageSmem = kWarpsPerBlock * 2 * 3 * kStageF * 4;  // dynamic shared memory per CTA (48 KB)
+
+__device__ __forceinline__ void mbar_init1(uint32_t bar) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_wait1(uint32_t bar, uint32_t parity) {
+    uint32_t ok = 0;
+    while (!ok)
+        asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                     : "=r"(ok)
+                     : "r"(bar), "r"(parity)
+                     : "memory");
+}
+
 template <class SH, int D>
+__global__ void __launch_bounds__(kBlock) k_hogwild_tma(UpdateArgs a) {
+    constexpr int L = SH::L, G = SH::G;
+    static_assert(L % D == 0, "D must divide the per-group samples of a 32-sample tile");
+    extern __shared__ __align__(128) int32_t s_dyn[];
+    auto s_tri = reinterpret_cast<int32_t(*)[2][3][kStageF]>(s_dyn);  // [warp][buffer][u, v, r][sample]
+    __shared__ __align__(8) uint64_t s_bar[kWarpsPerBlock][2];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const int grp = lane / L, sub = lane % L;
+    const int k = SH::FULL ? SH::KMAX : a.k;
+    const int64_t N = a.n;
+    const int f = a.batch_f;  // <= kStageF (launcher)
+    const int64_t warp_id = (blockIdx.x * kBlock + threadIdx.x) >> 5;
+    const int64_t gleft = (int64_t)a.active_groups - warp_id * G;
+    if (gleft <= 0) return;  // warp-uniform
+    const int gper = gleft < G ? (int)gleft : G;
+    const int ntile = (32 + gper - 1) / gper;
+    unsigned long long done = 0;
+    int bad = 0;
+    const int ahead = a.prefetch * D;
+    const uint32_t row_bytes = (uint32_t)k * SH::BYTES;
+    const bool pf_on = ahead > 0 && SH::FULL && (row_bytes % 16u) == 0u && (32 % gper) == 0;
+    const bool pf_ponly = a.prefetch_kind & 1;
+    const int64_t nwarps = (a.active_groups + G - 1) / G;
+    const int64_t tail_zone = nwarps * (int64_t)f;
+    const int64_t dyn0 = 2 * nwarps * (int64_t)f;
+    unsigned long long *const ctr = a.chunk_ctr ? a.chunk_ctr : &a.scratch->chunk;
+    auto claim = [&](int64_t *len) -> int64_t {
+        unsigned long long c = 0;
+        int want = f;
+        if (lane == 0) {
+            const unsigned long long seen = *(volatile unsigned long long *)ctr;
+            if (dyn0 + (int64_t)seen + tail_zone >= N) want = 32;
+            c = atomicAdd(ctr, (unsigned long long)want);
+        }
+        *len = __shfl_sync(0xffffffffu, want, 0);
+        return dyn0 + (int64_t)__shfl_sync(0xffffffffu, c, 0);
+    };
+    const int cp = a.cache_policy;
+    const uint64_t pol_p = cp == 2   ? policy_evict_last()
+                           : cp >= 4 ? policy_evict_last_frac((cp & 1) ? 0.75f : 0.5f)
+                                     : policy_evict_normal();
+    const uint64_t pol_q = cp == 2 || cp == 3 || cp >= 6 ? policy_evict_last() : policy_evict_normal();
+    const uint32_t bar0 = (uint32_t)__cvta_generic_to_shared(&s_bar[wib][0]);
+    if (lane == 0) {
+        mbar_init1(bar0);
+        mbar_init1(bar0 + 8);
+    }
+    __syncwarp();
+    // stage chunk [cb, cb + clen) into buffer b: 16-B granules by the TMA engine, the rest by lanes
+    auto stage = [&](int b, int64_t cb, int clen) {
+        const int c4 = clen & ~3;
+        if (lane == 0) {
+            const uint32_t bar = bar0 + 8u * (uint32_t)b;
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // our earlier reads of the buffer
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(12 * c4) : "memory");
+            if (c4) {
+                const int32_t *src[3] = {a.u + cb, a.v + cb, reinterpret_cast<const int32_t *>(a.r) + cb};
+#pragma unroll
+                for (int x = 0; x < 3; x++) {
+                    const uint32_t dst = (uint32_t)__cvta_generic_to_shared(&s_tri[wib][b][x][0]);
+                    asm volatile(
+                        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                            dst),
+                        "l"(src[x]), "r"(4 * c4), "r"(bar)
+                        : "memory");
+                }
+            }
+        }
+        if (lane < clen - c4) {
+            s_tri[wib][b][0][c4 + lane] = __ldg(a.u + cb + c4 + lane);
+            s_tri[wib][b][1][c4 + lane] = __ldg(a.v + cb + c4 + lane);
+            s_tri[wib][b][2][c4 + lane] = __float_as_int(__ldg(a.r + cb + c4 + lane));
+        }
+    };
+    uint32_t phase = 0;  // bit b: parity of buffer b's next completion
+    int64_t base = warp_id * (int64_t)f;
+    if (base >= N) return;
+    int len = (int)min((int64_t)f, N - base);
+    int64_t nbase = (nwarps + warp_id) * (int64_t)f;
+    int64_t nlen64 = f;
+    int b = 0;
+    stage(0, base, len);
+    int nlen = nbase < N ? (int)min(nlen64, N - nbase) : 0;
+    if (nlen) stage(1, nbase, nlen);
+    for (;;) {
+        mbar_wait1(bar0 + 8u * (uint32_t)b, (phase >> b) & 1u);
+        phase ^= 1u << b;
+        __syncwarp();  // the lanes' tail stores of this buffer are visible to the whole warp
+        const int32_t *tu_ = s_tri[wib][b][0], *tv_ = s_tri[wib][b][1];
+        const float *tr_ = reinterpret_cast<const float *>(s_tri[wib][b][2]);
+        if (a.count_updates && lane == 0) done += len;
+        for (int t0 = 0; t0 < len; t0 += 32) {
+            const int cnt = len - t0 < 32 ? len - t0 : 32;
+            const int steps = (cnt + gper - 1) / gper < ntile ? (cnt + gper - 1) / gper : ntile;
+#pragma unroll 1
+            for (int j0 = 0; j0 < steps; j0 += D) {
+                int32_t su[D], sv[D];
+                float sr[D];
+                bool val[D];
+                RowRaw<SH> pr[D], qr[D];
+                float pf[D][SH::E], qf[D][SH::E], dot[D];
+#pragma unroll
+                for (int d = 0; d < D; d++) {
+                    const int s_ = (j0 + d) * gper + grp;
+                    val[d] = grp < gper && s_ < cnt;
+                    su[d] = val[d] ? tu_[t0 + s_] : 0;
+                    sv[d] = val[d] ? tv_[t0 + s_] : 0;
+                    sr[d] = val[d] ? tr_[t0 + s_] : 0.f;
+                }
+                if (pf_on) {  // L2 prefetch of the rows `ahead` steps later inside this chunk
+#pragma unroll
+                    for (int d = 0; d < D; d++) {
+                        const int jt = j0 + ahead + d;
+                        const int idx = jt < steps ? t0 + jt * gper + grp : t0 + 32 + (jt - steps) * gper + grp;
+                        if (grp < gper && idx < len && sub == 0) {
+                            prefetch_row_l2(a.P, tu_[idx], row_bytes);
+                            if (!pf_ponly) prefetch_row_l2(a.Q, tv_[idx], row_bytes);
+                        }
+                    }
+                }
+#pragma unroll
+                for (int d = 0; d < D; d++) {
+                    load_row_pol<SH>(a.P, su[d], k, sub, val[d], pr[d], pol_p);
+                    load_row_pol<SH>(a.Q, sv[d], k, sub, val[d], qr[d], pol_q);
+                }
+#pragma unroll
+                for (int d = 0; d < D; d++) {
+                    widen_row<SH>(pr[d], pf[d]);
+                    widen_row<SH>(qr[d], qf[d]);
+                    dot[d] = lane_dot<SH>(pf[d], qf[d]);
+                }
+                group_allreduce<SH, D>(dot);
+#pragma unroll
+                for (int d = 0; d < D; d++) {
+                    const float err = sr[d] - dot[d];
+                    if (val[d] && !isfinite(err)) bad = 1;
+                    sgd_step<SH>(pf[d], qf[d], err, a.eta, a.lam);
+                    narrow_row<SH>(pf[d], pr[d]);
+                    narrow_row<SH>(qf[d], qr[d]);
+                    store_row_pol<SH>(a.P, su[d], k, sub, val[d], pr[d], pol_p);
+                    store_row_pol<SH>(a.Q, sv[d], k, sub, val[d], qr[d], pol_q);
+                }
+            }
+        }
+        if (!nlen) break;
+        __syncwarp();  // every lane is done reading buffer b before it is refilled
+        // chunk after next: claimed now, staged into the buffer just used
+        int64_t cl_len = 0;
+        const int64_t cbase = claim(&cl_len);
+        const int clen = cbase < N ? (int)min(cl_len, N - cbase) : 0;
+        if (clen) stage(b, cbase, clen);
+        b ^= 1;
+        len = nlen;
+        nlen = clen;
+    }
+    if (bad) a.scratch->diverged = 1;
+    if (a.count_updates && lane == 0 && done) atomicAdd(&a.scratch->updates, done);
+}
+
+template <class SH, int D, bool TMA = false>
 static cudaError_t hogwild_launch(const UpdateArgs &a, int workers, cudaStream_t st, int *used) {
     // occupancy and SM count are queried once per instantiation: the partitioned path launches this
     // kernel hundreds of times per epoch and the host must stay ahead of ~80 us launches
@@ -295,7 +483,12 @@ static cudaError_t hogwild_launch(const UpdateArgs &a, int workers, cudaStream_t
     }();
     static const int per_sm = [] {
         int v = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, k_hogwild<SH, D>, kBlock, 0);
+        if constexpr (TMA) {
+            cudaFuncSetAttribute(k_hogwild_tma<SH, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, kStageSmem);
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, k_hogwild_tma<SH, D>, kBlock, kStageSmem);
+        } else {
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, k_hogwild<SH, D>, kBlock, 0);
+        }
         return v < 1 ? 1 : v;
     }();
     // workers = concurrent ratings = active groups x D
@@ -331,7 +524,8 @@ static cudaError_t hogwild_launch(const UpdateArgs &a, int workers, cudaStream_t
     // every launch claims chunks from 0 (the partitioned path launches once per block)
     cudaError_t e = cudaMemsetAsync(a.chunk_ctr ? a.chunk_ctr : &a.scratch->chunk, 0, sizeof(unsigned long long), st);
     if (e != cudaSuccess) return e;
-    k_hogwild<SH, D><<<blocks, kBlock, 0, st>>>(args);
+    if constexpr (TMA) k_hogwild_tma<SH, D><<<blocks, kBlock, kStageSmem, st>>>(args);
+    else k_hogwild<SH, D><<<blocks, kBlock, 0, st>>>(args);
     return cudaGetLastError();
 }
 
@@ -343,12 +537,22 @@ cudaError_t launch_hogwild(const ShapeId &sh, const UpdateArgs &a_in, int worker
         const int pf = (variant >> 16) & 0xF;  // bits 16..19: L2 row-prefetch distance in steps (0, 15 = off)
         a.prefetch = pf == 15 ? 0 : pf;
         a.prefetch_kind = (variant >> 20) & 0x3;  // bits 20..21: 1 = P rows only, 2 = per-lane prefetch
-        a.cache_policy = (variant >> 28) & 0x3;   // bits 28..29: L2 eviction priorities (UpdateArgs)
+        a.cache_policy = (variant >> 28) & 0x7;   // bits 28..30: L2 eviction priorities (UpdateArgs)
     }
+    // TMA staging of the triples needs 16-B aligned arrays and chunks that fit the warp's buffers
+    const bool tma = a.r_stage == 2 && a.batch_f <= kStageF && !a.abort_if &&
+                     ((reinterpret_cast<uintptr_t>(a.u) | reinterpret_cast<uintptr_t>(a.v) |
+                       reinterpret_cast<uintptr_t>(a.r)) & 15) == 0;
     return dispatch_shape(sh, [&](auto tag) -> cudaError_t {
         using SH = decltype(tag);
         constexpr int L = SH::L;
         if constexpr (SH::FULL) {
+            if (tma && D != 4) {
+                if (workers > 0 && workers < 64) return hogwild_launch<SH, 1, true>(a, workers, st, workers_used);
+                const bool two = D == 2 || D == 3 || (D == 0 && SH::S == kF32 && SH::KMAX >= 128);
+                if (two && L % 2 == 0) return hogwild_launch<SH, (L % 2 == 0 ? 2 : 1), true>(a, workers, st, workers_used);
+                return hogwild_launch<SH, 1, true>(a, workers, st, workers_used);
+            }
             if (workers > 0 && workers < 64) return hogwild_launch<SH, 1>(a, workers, st, workers_used);
             if (D == 4 && L % 4 == 0) return hogwild_launch<SH, (L % 4 == 0 ? 4 : 1)>(a, workers, st, workers_used);
             // D = 0 (auto): two ratings in flight per group for fp32 rows of k >= 128, one otherwise

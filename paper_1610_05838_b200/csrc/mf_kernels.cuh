@@ -41,9 +41,12 @@ struct UpdateArgs {
     const unsigned long long *abort_if;  // optional: the kernel does nothing if *abort_if != 0
     int prefetch;       // batch-Hogwild!: L2-prefetch the rows of the rating this many steps ahead (0 = off)
     int prefetch_kind;  // bit 0: P rows only; bit 1: per-lane prefetch.global.L2 instead of one bulk prefetch
-    int cache_policy;   // L2 eviction priorities (MF_OPT_VARIANT bits 28..29, resolved): 0 = R evict_first,
-                        // 1 = none (plain loads), 2 = R evict_first + P/Q rows evict_last, 3 = R evict_first +
-                        // Q rows evict_last
+    int cache_policy;   // L2 eviction priorities (MF_OPT_VARIANT bits 28..30): 0 = R evict_first, 1 = none (plain
+                        // loads), 2 = R evict_first + P/Q rows evict_last, 3 = R evict_first + Q rows evict_last,
+                        // 4 / 5 = R evict_first + evict_last on 50 / 75% of the P lines, 6 / 7 = as 4 / 5 + Q rows
+                        // evict_last
+    int r_stage;        // batch-Hogwild! triples: 2 = TMA bulk copies of each chunk into shared memory, else
+                        // registers (3 coalesced 32-bit loads per lane per 32-sample tile, shuffled to groups)
     int barrier;        // deterministic waves, 1024-thread CTAs: 0 = arrival counter polled to (w+1) x CTAs
                         // (one release reduction + acquire polls), 1 = last arriver bumps a generation flag
 };

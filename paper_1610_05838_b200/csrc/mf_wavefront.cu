@@ -33,7 +33,6 @@ using namespace mf;
 
 namespace {
 
-constexpr int kBlock = 256;
 
 // row band / column group by balanced segmentation (widths differ by at most one; A-9)
 __global__ void k_block_keys(const int32_t *u, const int32_t *v, int64_t n, int64_t rows, int64_t cols, int s,
@@ -117,6 +116,23 @@ __device__ __forceinline__ void lock_acquire(int32_t *lock) {
     }
 }
 
+// The same acquire by a whole warp in lockstep: lane 0 tests and tries, the outcome is broadcast, every
+// lane loops -- no lane-divergent region, so the shuffles after it compile without convergence fix-ups.
+__device__ __forceinline__ void lock_acquire_warp(int32_t *lock, int lane) {
+    unsigned ns = 32;
+    for (;;) {
+        int got = 0;
+        if (lane == 0) {
+            int32_t cur;
+            asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(cur) : "l"(lock) : "memory");
+            got = cur == 0 && atomicCAS(lock, 0, 1) == 0;
+        }
+        if (__shfl_sync(0xffffffffu, got, 0)) break;
+        __nanosleep(ns);
+        if (ns < 256) ns <<= 1;
+    }
+}
+
 __device__ __forceinline__ int64_t globaltimer() {
     int64_t t;
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -124,11 +140,13 @@ __device__ __forceinline__ int64_t globaltimer() {
 }
 
 template <class SH, int D>
-__global__ void __launch_bounds__(kBlock) k_wavefront(WfArgs a) {
+__global__ void __launch_bounds__(32) k_wavefront(WfArgs a) {
     static_assert(SH::L == 32, "wavefront worker is a full warp");
     static_assert(D >= 1 && D <= 16, "in-block pipeline depth");
     const int lane = threadIdx.x & 31;
-    const int w = (blockIdx.x * kBlock + threadIdx.x) >> 5;
+    // one warp per CTA: the worker index is block-uniform, so no lane-divergent early exit precedes the
+    // shuffles (the compiler then emits them without convergence fix-ups)
+    const int w = blockIdx.x;
     if (w >= a.s) return;
     const int k = SH::FULL ? SH::KMAX : a.k;
     const int c = a.c;
@@ -149,8 +167,7 @@ __global__ void __launch_bounds__(kBlock) k_wavefront(WfArgs a) {
             if (i0 < hi) cu = __ldg(a.u + i0), cv = __ldg(a.v + i0), cr = __ldg(a.r + i0);
             if (i1 < hi) nu = __ldg(a.u + i1), nv = __ldg(a.v + i1), nr = __ldg(a.r + i1);
         }
-        if (lane == 0) lock_acquire(lock);
-        __syncwarp();
+        lock_acquire_warp(lock, lane);
         __threadfence();  // acquire: the previous holder's stores are visible (loads are .cg)
         const int64_t t0 = a.trace ? globaltimer() : 0;
         done += (uint64_t)(hi - lo);
@@ -174,55 +191,63 @@ __global__ void __launch_bounds__(kBlock) k_wavefront(WfArgs a) {
             hu[d] = -1;
             hv[d] = -1;
             const bool ok = lo + d < hi;
-            ru[d] = rv[d] = 0;
-            rr[d] = 0.f;
-            if (ok) triple(lo + d, ru[d], rv[d], rr[d]);
+            int32_t tu_, tv_;
+            float tr_;
+            triple(lo + d, tu_, tv_, tr_);
+            ru[d] = ok ? tu_ : 0;
+            rv[d] = ok ? tv_ : 0;
+            rr[d] = ok ? tr_ : 0.f;
             load_row<SH>(a.P, ru[d], k, lane, ok, rp[d]);
             load_row<SH>(a.Q, rv[d], k, lane, ok, rq[d]);
         }
+        // Branch-free over the D slots: every lane of the warp reaches every shuffle (no collective
+        // fix-up code around the butterflies); a slot past the block's end computes on zero rows and
+        // neither stores nor forwards.
         for (int64_t base = lo; base < hi; base += D) {
 #pragma unroll
             for (int d = 0; d < D; d++) {
                 const int64_t i = base + d;
-                if (i < hi) {  // warp-uniform
-                    RowRaw<SH> pr = rp[d], qr = rq[d];
-                    // forward rows written since this sample's loads were issued (oldest first)
+                const bool val = i < hi;
+                RowRaw<SH> pr = rp[d], qr = rq[d];
+                // forward rows written since this sample's loads were issued (oldest first)
 #pragma unroll
-                    for (int t = 0; t < D; t++) {
-                        const int h = (d + t) % D;
-                        if (hu[h] == ru[d]) pr = hp[h];
-                        if (hv[h] == rv[d]) qr = hq[h];
-                    }
-                    float p[SH::E], q[SH::E];
-                    widen_row<SH>(pr, p);
-                    widen_row<SH>(qr, q);
-                    const float err = rr[d] - group_dot<SH>(p, q);
-                    if (!isfinite(err)) bad = 1;
-                    sgd_step<SH>(p, q, err, a.eta, a.lam);
-                    narrow_row<SH>(p, pr);
-                    narrow_row<SH>(q, qr);
-                    store_row<SH>(a.P, ru[d], k, lane, true, pr);
-                    store_row<SH>(a.Q, rv[d], k, lane, true, qr);
-                    hu[d] = ru[d];
-                    hv[d] = rv[d];
-                    hp[d] = pr;
-                    hq[d] = qr;
-                    // refill this slot with sample i + D (its triple is in the register tiles)
-                    const int64_t nx = i + D;
-                    if (nx - tb >= 32) {  // warp-uniform: the current tile is used up, slide by 32
-                        tb += 32;
-                        cu = nu, cv = nv, cr = nr;
-                        const int64_t i1 = tb + 32 + lane;
-                        nu = 0, nv = 0, nr = 0.f;
-                        if (i1 < hi) nu = __ldg(a.u + i1), nv = __ldg(a.v + i1), nr = __ldg(a.r + i1);
-                    }
-                    const bool ok = nx < hi;
-                    ru[d] = rv[d] = 0;
-                    rr[d] = 0.f;
-                    if (ok) triple(nx, ru[d], rv[d], rr[d]);
-                    load_row<SH>(a.P, ru[d], k, lane, ok, rp[d]);
-                    load_row<SH>(a.Q, rv[d], k, lane, ok, rq[d]);
+                for (int t = 0; t < D; t++) {
+                    const int h = (d + t) % D;
+                    if (hu[h] == ru[d]) pr = hp[h];
+                    if (hv[h] == rv[d]) qr = hq[h];
                 }
+                float p[SH::E], q[SH::E];
+                widen_row<SH>(pr, p);
+                widen_row<SH>(qr, q);
+                const float err = rr[d] - group_dot<SH>(p, q);
+                if (val && !isfinite(err)) bad = 1;
+                sgd_step<SH>(p, q, err, a.eta, a.lam);
+                narrow_row<SH>(p, pr);
+                narrow_row<SH>(q, qr);
+                store_row<SH>(a.P, ru[d], k, lane, val, pr);
+                store_row<SH>(a.Q, rv[d], k, lane, val, qr);
+                hu[d] = val ? ru[d] : -1;
+                hv[d] = val ? rv[d] : -1;
+                hp[d] = pr;
+                hq[d] = qr;
+                // refill this slot with sample i + D (its triple is in the register tiles)
+                const int64_t nx = i + D;
+                if (nx - tb >= 32) {  // warp-uniform: the current tile is used up, slide by 32
+                    tb += 32;
+                    cu = nu, cv = nv, cr = nr;
+                    const int64_t i1 = tb + 32 + lane;
+                    nu = 0, nv = 0, nr = 0.f;
+                    if (i1 < hi) nu = __ldg(a.u + i1), nv = __ldg(a.v + i1), nr = __ldg(a.r + i1);
+                }
+                const bool ok = nx < hi;
+                int32_t tu_, tv_;
+                float tr_;
+                triple(nx, tu_, tv_, tr_);
+                ru[d] = ok ? tu_ : 0;
+                rv[d] = ok ? tv_ : 0;
+                rr[d] = ok ? tr_ : 0.f;
+                load_row<SH>(a.P, ru[d], k, lane, ok, rp[d]);
+                load_row<SH>(a.Q, rv[d], k, lane, ok, rq[d]);
             }
         }
         if (a.trace && lane == 0) {
@@ -585,10 +610,11 @@ __global__ void __launch_bounds__(THREADS, 1) k_wavefront_q(WfArgs a) {
             for (int rr = last + 1 + (int)threadIdx.x; rr <= nrows; rr += nthreads) run_start[rr] = (int)(hi - lo);
         }
         __syncthreads();
-        if ((int)(threadIdx.x >> 5) < active_warps) {
+        {
+            const bool claims = (int)(threadIdx.x >> 5) < active_warps;
             for (;;) {
-                int r = 0;
-                if (lane == 0) r = atomicAdd(&s_next, 1);
+                int r = nrows;
+                if (lane == 0 && claims) r = atomicAdd(&s_next, 1);
                 r = __shfl_sync(0xffffffffu, r, 0);
                 if (r >= nrows) break;  // warp-uniform
                 const int64_t rb = lo + run_start[r], re = lo + run_start[r + 1];
@@ -619,50 +645,58 @@ __global__ void __launch_bounds__(THREADS, 1) k_wavefront_q(WfArgs a) {
                 for (int d = 0; d < D; d++) {
                     hu[d] = -1;
                     const bool ok = rb + d < re;
-                    ru[d] = 0;
-                    rr[d] = 0.f;
-                    if (ok) triple(rb + d, ru[d], rr[d]);
+                    int32_t tu_;
+                    float tr_;
+                    triple(rb + d, tu_, tr_);
+                    ru[d] = ok ? tu_ : 0;
+                    rr[d] = ok ? tr_ : 0.f;
                     load_row<SH>(a.P, ru[d], k, lane, ok, rp[d]);
                 }
                 float q[SH::E];
                 widen_row<SH>(qraw, q);
                 for (int64_t base = rb; base < re; base += D) {
 #pragma unroll
-                    for (int d = 0; d < D; d++) {
+                    for (int d = 0; d < D; d++) {  // branch-free: every lane reaches every shuffle
                         const int64_t i = base + d;
-                        if (i < re) {  // warp-uniform
-                            RowRaw<SH> pr = rp[d];
-                            // p_u written by one of the D - 1 samples since this load was issued (a
-                            // duplicate rating inside the ring, rare): read it again -- the same lanes
-                            // stored it, so program order makes the new value visible
-                            bool hit = false;
+                        const bool val = i < re;
+                        RowRaw<SH> pr = rp[d];
+                        // p_u written by one of the D - 1 samples since this load was issued (a
+                        // duplicate rating inside the ring, rare): read it again -- the same lanes
+                        // stored it, so program order makes the new value visible
+                        bool hit = false;
 #pragma unroll
-                            for (int t = 1; t < D; t++) hit |= hu[(d + t) % D] == ru[d];
-                            if (hit) load_row<SH>(a.P, ru[d], k, lane, true, pr);
-                            float p[SH::E];
-                            widen_row<SH>(pr, p);
-                            const float err = rr[d] - group_dot<SH>(p, q);
+                        for (int t = 1; t < D; t++) hit |= hu[(d + t) % D] == ru[d];
+                        if (val && hit) load_row<SH>(a.P, ru[d], k, lane, true, pr);
+                        float p[SH::E];
+                        widen_row<SH>(pr, p);
+                        const float err = rr[d] - group_dot<SH>(p, q);
+                        if (val) {
                             chk = fmaf(err, 0.f, chk);
-                            sgd_step<SH>(p, q, err, a.eta, a.lam);
+                            float qn[SH::E];
+#pragma unroll
+                            for (int e = 0; e < SH::E; e++) qn[e] = q[e];
+                            sgd_step<SH>(p, qn, err, a.eta, a.lam);
                             narrow_row<SH>(p, pr);
-                            narrow_row<SH>(q, qraw);
+                            narrow_row<SH>(qn, qraw);
                             widen_row<SH>(qraw, q);  // q_v as stored after this update (serial semantics)
                             store_row<SH>(a.P, ru[d], k, lane, true, pr);
-                            hu[d] = ru[d];
-                            const int64_t nx = i + D;
-                            if (nx - tb >= 32) {  // warp-uniform: slide the triple tiles
-                                tb += 32;
-                                cu = nu, cr = nr;
-                                const int64_t i1 = tb + 32 + lane;
-                                nu = 0, nr = 0.f;
-                                if (i1 < re) nu = __ldg(a.u + i1), nr = __ldg(a.r + i1);
-                            }
-                            const bool ok = nx < re;
-                            ru[d] = 0;
-                            rr[d] = 0.f;
-                            if (ok) triple(nx, ru[d], rr[d]);
-                            load_row<SH>(a.P, ru[d], k, lane, ok, rp[d]);
                         }
+                        hu[d] = val ? ru[d] : -1;
+                        const int64_t nx = i + D;
+                        if (nx - tb >= 32) {  // warp-uniform: slide the triple tiles
+                            tb += 32;
+                            cu = nu, cr = nr;
+                            const int64_t i1 = tb + 32 + lane;
+                            nu = 0, nr = 0.f;
+                            if (i1 < re) nu = __ldg(a.u + i1), nr = __ldg(a.r + i1);
+                        }
+                        const bool ok = nx < re;
+                        int32_t tu_;
+                        float tr_;
+                        triple(nx, tu_, tr_);
+                        ru[d] = ok ? tu_ : 0;
+                        rr[d] = ok ? tr_ : 0.f;
+                        load_row<SH>(a.P, ru[d], k, lane, ok, rp[d]);
                     }
                 }
                 store_row<SH>(a.Q, vrow, k, lane, true, qraw);
@@ -948,7 +982,6 @@ int mf_ctx::run_wavefront(const ShapeId &, const UpdateArgs &ua, int *launches, 
         }));
     } else {
         const ShapeId sh = warp_shape(k, storage);
-        const int blocks = (s * 32 + kBlock - 1) / kBlock;
         // samples of a block in flight per warp (MF_OPT_VARIANT bits 4..7: 2, 4 or 8; 0 = 4 for the full-row
         // shapes).  The triples come from two 32-sample register tiles fetched before the lock, so the
         // only latency on a sample's path is its row loads, issued `depth` samples ahead.
@@ -958,15 +991,15 @@ int mf_ctx::run_wavefront(const ShapeId &, const UpdateArgs &ua, int *launches, 
             using SH = decltype(tag);
             if constexpr (SH::FULL) {
                 if (depth == 8) {
-                    k_wavefront<SH, 8><<<blocks, kBlock, 0, st>>>(a);
+                    k_wavefront<SH, 8><<<s, 32, 0, st>>>(a);
                     return cudaGetLastError();
                 }
                 if (depth == 4) {
-                    k_wavefront<SH, 4><<<blocks, kBlock, 0, st>>>(a);
+                    k_wavefront<SH, 4><<<s, 32, 0, st>>>(a);
                     return cudaGetLastError();
                 }
             }
-            k_wavefront<SH, 2><<<blocks, kBlock, 0, st>>>(a);
+            k_wavefront<SH, 2><<<s, 32, 0, st>>>(a);
             return cudaGetLastError();
         }));
     }

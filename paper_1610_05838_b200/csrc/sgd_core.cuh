@@ -258,6 +258,13 @@ __device__ __forceinline__ uint64_t policy_evict_last() {
     asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
     return p;
 }
+// evict_last for a fraction of the lines (chosen by address, so a line keeps its priority), the rest
+// evict_unchanged: pins part of a row array that does not fit L2 as a whole
+__device__ __forceinline__ uint64_t policy_evict_last_frac(float f) {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_last.L2::evict_unchanged.b64 %0, %1;" : "=l"(p) : "f"(f));
+    return p;
+}
 __device__ __forceinline__ uint64_t policy_evict_normal() {
     uint64_t p;
     asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));

@@ -280,6 +280,41 @@ def test_netflix_slice_hogwild_l2_prefetch(mfmod, storage, pf):
     assert abs(got - gold[E - 1]) <= 0.005 * gold[E - 1], (got, gold[E - 1])
 
 
+@pytest.mark.parametrize("storage", [0, 1, 2])
+@pytest.mark.parametrize("pf", [15, 1])
+def test_netflix_slice_hogwild_tma_staged_triples(mfmod, storage, pf):
+    """MF_OPT_R_STAGING = 2: the rating batches reach shared memory by TMA bulk copies (double-buffered per
+    warp) instead of registers; the schedule and the update are those of batch-Hogwild!.  Every sample
+    once per epoch, one run within 0.5% of the serial oracle at the storage's gate epoch (C2-10pct),
+    with and without the L2 row prefetch."""
+    cfg, (train, test) = _c2_10pct_data()
+    gold = _c2_10pct_gold(storage)
+    E = GATE_EPOCH[storage]
+    got = _hogwild_run(mfmod, cfg, storage, train, test, E, r_staging=2, variant=pf << 16,
+                       check=lambda g: int(g.get(mfmod.MF_OPT_R_STAGING)) == 2)
+    assert abs(got - gold[E - 1]) <= 0.005 * gold[E - 1], (got, gold[E - 1])
+
+
+def test_hogwild_tma_staged_triples_ragged_and_tiny(mfmod):
+    """TMA staging with chunk lengths that are not multiples of 4 (the lanes copy the last len % 4
+    triples), N smaller than one chunk, and the worked example: exactly once, and with one worker the
+    epoch equals the serial oracle (the stored order)."""
+    cfg = datagen.CONFIGS["C1"]
+    (u, v, r), _ = datagen.make(cfg)
+    for N in (1, 3, 31, 257, 1001, 49_999):
+        with _gpu(mfmod, cfg, 0, count_updates=1, r_staging=2, batch_f=96) as g:
+            g.load(u[:N], v[:N], r[:N])
+            assert g.epoch("hogwild").updates == N
+    order = oracle.shuffle_perm(cfg.seed_shuffle, 9_999)
+    ref = oracle.Model(cfg.m, cfg.n, cfg.k, oracle.F32, seed=cfg.seed_init)
+    ref.epoch(u[:9_999], v[:9_999], r[:9_999], oracle.eta(cfg.alpha, cfg.beta, 0), cfg.lam, order)
+    with _gpu(mfmod, cfg, 0, workers=1, r_staging=2) as g:
+        g.load(u[:9_999], v[:9_999], r[:9_999])
+        g.epoch("hogwild")
+        P, Q = g.factors()
+    assert frob(P, ref.P) <= 1e-5 and frob(Q, ref.Q) <= 1e-5
+
+
 @pytest.mark.parametrize("k,storage", [(32, 0), (32, 1), (64, 0), (64, 1)])
 def test_netflix_slice_hogwild_small_k(mfmod, k, storage):
     """The k = 32 / 64 batch-Hogwild! shapes (16 lanes per rating, 4- / 8-byte vectors): exactly once per
