@@ -126,7 +126,7 @@ __global__ void __launch_bounds__(kBlock) k_hogwild(UpdateArgs a) {
     const int k = SH::FULL ? SH::KMAX : a.k;
     const int64_t N = a.n;
     const int f = a.batch_f;
-    const int64_t warp_id = (blockIdx.x * kBlock + threadIdx.x) >> 5;
+    const int64_t warp_id = warp_uniform((blockIdx.x * kBlock + threadIdx.x) >> 5);
     // exact worker count: groups beyond a.active_groups idle; a warp with no active group exits
     const int64_t gleft = (int64_t)a.active_groups - warp_id * G;
     if (gleft <= 0) return;  // warp-uniform
@@ -302,13 +302,16 @@ __device__ __forceinline__ void mbar_init1(uint32_t bar) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar) : "memory");
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
 }
+// every lane of the warp waits; the loop exit is a warp vote, so it is uniform to the compiler
 __device__ __forceinline__ void mbar_wait1(uint32_t bar, uint32_t parity) {
-    uint32_t ok = 0;
-    while (!ok)
+    for (;;) {
+        uint32_t ok;
         asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
                      : "=r"(ok)
                      : "r"(bar), "r"(parity)
                      : "memory");
+        if (__all_sync(0xffffffffu, ok)) break;
+    }
 }
 
 template <class SH, int D>
@@ -323,7 +326,7 @@ __global__ void __launch_bounds__(kBlock) k_hogwild_tma(UpdateArgs a) {
     const int k = SH::FULL ? SH::KMAX : a.k;
     const int64_t N = a.n;
     const int f = a.batch_f;  // <= kStageF (launcher)
-    const int64_t warp_id = (blockIdx.x * kBlock + threadIdx.x) >> 5;
+    const int64_t warp_id = warp_uniform((blockIdx.x * kBlock + threadIdx.x) >> 5);
     const int64_t gleft = (int64_t)a.active_groups - warp_id * G;
     if (gleft <= 0) return;  // warp-uniform
     const int gper = gleft < G ? (int)gleft : G;
@@ -635,6 +638,7 @@ __global__ void __launch_bounds__(BLOCK) k_waves(UpdateArgs a) {
     const int k = SH::FULL ? SH::KMAX : a.k;
     const int64_t groups = (int64_t)gridDim.x * BLOCK / L;
     const int64_t gid = ((int64_t)blockIdx.x * BLOCK + threadIdx.x) / L;
+    const int64_t wbase = warp_uniform(gid - lane / L);  // the warp's first group
     int bad = 0;
     unsigned long long done = 0;
     // The triples of a group's first step in the next wave are read-only and independent of the wave's
@@ -646,7 +650,7 @@ __global__ void __launch_bounds__(BLOCK) k_waves(UpdateArgs a) {
         const int64_t lo = a.wave_off[wv], hi = a.wave_off[wv + 1];
 #pragma unroll
         for (int d = 0; d < D; d++) {
-            const int64_t s = lo + (gid - (lane / L)) + d * groups + lane / L;
+            const int64_t s = lo + wbase + d * groups + lane / L;
             const bool ok = s < hi;
             nu[d] = ok ? __ldg(a.u + s) : 0;
             nv[d] = ok ? __ldg(a.v + s) : 0;
@@ -657,7 +661,7 @@ __global__ void __launch_bounds__(BLOCK) k_waves(UpdateArgs a) {
     for (int64_t w = 0; w < a.nwaves; w++) {
         const int64_t lo = a.wave_off[w], hi = a.wave_off[w + 1];
         // warp-uniform trip count so the full-warp shuffles stay converged
-        const int64_t warp_first = lo + (gid - (lane / L));
+        const int64_t warp_first = lo + wbase;
         for (int64_t s0 = warp_first; s0 < hi; s0 += D * groups) {
             int32_t su[D], sv[D];
             float sr[D], dot[D];
@@ -752,7 +756,7 @@ __global__ void __launch_bounds__(kBlock) k_rmse(const int32_t *u, const int32_t
     const int64_t groups = (int64_t)gridDim.x * kBlock / L;
     const int64_t gid = ((int64_t)blockIdx.x * kBlock + threadIdx.x) / L;
     double acc = 0.0;
-    const int64_t warp_first = gid - lane / L;
+    const int64_t warp_first = warp_uniform(gid - lane / L);
     for (int64_t s0 = warp_first; s0 < n; s0 += groups) {
         const int64_t s = s0 + lane / L;
         const bool val = s < n;

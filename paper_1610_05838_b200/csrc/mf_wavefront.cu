@@ -765,8 +765,8 @@ void mf_ctx::release_wavefront() {
     wf_valid = false;
 }
 
-// Auto sizing: up to 8 warp workers per SM, c = 2s column blocks (Latin-rectangle lock
-// utilisation ~95% at c/s = 2), blocks of >= ~32 samples, s <= m, c <= n.
+// Auto sizing: up to 16 warp workers per SM, c = 1.25 s column blocks (Latin-rectangle
+// lock utilisation ~95% at that ratio), blocks of >= ~14 samples, s <= m, c <= n.
 int mf_ctx::build_wavefront() {
     if (wf_valid) return MF_OK;
     release_wavefront();
@@ -794,14 +794,16 @@ int mf_ctx::build_wavefront() {
             c = (int)cc;
         }
     }
+    const bool warp_auto = !wave_cta && s <= 0;
     if (s <= 0) {
-        // warp workers: up to 8 per SM (1,184 on a B200), each with 4 samples of its block in flight, but
-        // blocks of >= ~32 samples (one register tile of triples) so the per-block lock hand-over (~1-2 us)
-        // stays small against the block's updates: s = sqrt(N / 64) with c = 2s
-        const double by_blocks = std::sqrt((double)N / 64.0);
-        s = (int)std::max<double>(1.0, std::min<double>({(double)num_sms * 8, by_blocks, (double)rows}));
+        // warp workers (one-warp CTAs): up to 16 per SM (2,368 on a B200) with c = 1.25 s column blocks
+        // (the Latin rectangle keeps ~95% of the workers busy at that ratio), blocks of >= ~14 samples:
+        // s = sqrt(N / 17.5).  Netflix shape f16: s / c = 1,184 / 2,368 2.19 G updates/s, 2,368 / 2,960
+        // 3.08-3.13, 3,552 / 4,440 3.06, 4,736 / 5,920 2.87 (profiles/r02h_warp_*, r02i_warp_*)
+        const double by_blocks = std::sqrt((double)N / 17.5);
+        s = (int)std::max<double>(1.0, std::min<double>({(double)num_sms * 16, by_blocks, (double)rows}));
     }
-    if (c <= 0) c = (int)std::min<int64_t>(2 * (int64_t)s, n);
+    if (c <= 0) c = (int)std::min<int64_t>(warp_auto ? std::max<int64_t>(s, (5 * (int64_t)s + 3) / 4) : 2 * (int64_t)s, n);
     if (s > rows || c > n || s < 1 || c < s)
         return fail(MF_EINVAL, "wavefront needs 1 <= s <= c, s <= m, c <= n (s=%d c=%d)", s, c);
     if ((int64_t)s * c >= (1ll << 32)) return fail(MF_EINVAL, "wavefront grid s*c too large");

@@ -368,6 +368,15 @@ __device__ __forceinline__ void prefetch_row_l2(const void *base, int64_t row, u
     asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(row_bytes) : "memory");
 }
 
+// A warp-uniform value as the compiler sees it: the broadcast of lane 0's value.  An index derived from
+// threadIdx.x (a warp's id, a warp's first sample) is the same on every lane, but the compiler's
+// divergence analysis cannot know that; branches and loop bounds computed from it make every shuffle
+// after them "possibly divergent", and ptxas then wraps each SHFL in WARPSYNC.COLLECTIVE fix-up code
+// (ncu: 385 instructions per rating in the warp-worker wavefront).  Shuffle results are uniform to it.
+__device__ __forceinline__ int64_t warp_uniform(int64_t x) {
+    return (int64_t)__shfl_sync(0xffffffffu, (unsigned long long)x, 0);
+}
+
 __device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
     uint64_t z = x + 0x9E3779B97F4A7C15ull;
     z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
