@@ -119,22 +119,35 @@ typedef struct {
     int32_t launches;        /* kernels launched by this call */
 } mf_epoch_stats;
 
-/* Create a context for an m x n rating matrix with rank k, initial LR alpha (= lr), regulariser
- * lambda (lambda_p = lambda_q, A-2) and seed (factor init A-7, and shuffle A-8 unless
- * MF_OPT_SEED_SHUFFLE).  Requires 0 < m, n < 2^31, 0 < k <= 1024, lr > 0, lambda >= 0. */
+/* Create a context for an m x n rating matrix R with rank k (R ~ P x Q, P m x k, Q k x n: PAPER.md:116-119,
+ * §2.1), initial learning rate alpha = lr of the schedule s_t = alpha / (1 + beta t^1.5) (PAPER.md:385-388,
+ * §5.1; beta via MF_OPT_BETA), regulariser lambda (the paper's lambda_p = lambda_q; one value
+ * as in Table 3; A-2) and seed (factor init, which the paper leaves open:
+ * DESIGN.md A-7; and the shuffle of PAPER.md:228 unless MF_OPT_SEED_SHUFFLE, A-8).
+ * Requires 0 < m, n < 2^31, 0 < k <= 1024, lr > 0, lambda >= 0 (MF_EINVAL otherwise; *out untouched).
+ * Allocates no device memory (that happens on the first load or factor access); *out is owned by the
+ * caller and released with mf_destroy. */
 int mf_create(int64_t m, int64_t n, int32_t k, float lr, float lambda, uint64_t seed, mf_ctx **out);
 
 /* Set / get an mf_option.  Layout-affecting keys (STORAGE, DEVICE) fail with MF_ESTATE after the factors exist. */
 int mf_set_option(mf_ctx *ctx, int key, double value);
 int mf_get_option(const mf_ctx *ctx, int key, double *value);
 
-/* Load the training set (replacing any previous one): validate 0 <= u < m, 0 <= v < n and finite r on the
- * device (MF_EINVAL on failure, nothing loaded), then permute (MF_OPT_SHUFFLE) and store as device SoA.
- * Allocates and initialises P, Q (A-7) on first use.  nnz >= 1. */
+/* Load the training set, the observed entries of R as COO triples (u, v, r) (12 bytes per
+ * sample), replacing any previous one.  u, v, r are nnz-element arrays in host or device memory
+ * (detected), COPIED; the caller keeps ownership.  On the device: validate 0 <= u < m, 0 <= v < n and finite
+ * r (MF_EINVAL on failure, nothing loaded: SPEC.md:62), then permute once by the A-8 hash order ("we shuffle
+ * samples"; MF_OPT_SHUFFLE) and store as three SoA arrays.  Allocates and initialises P, Q
+ * (A-7) on first use.  nnz >= 1 (MF_EINVAL); MF_ENOMEM / MF_ECUDA on device failures. */
 int mf_load_coo(mf_ctx *ctx, const int32_t *u, const int32_t *v, const float *r, int64_t nnz);
 
-/* Run one epoch (N updates) under `schedule` at eta_t, then t += 1.  stats may be NULL.
- * Returns MF_EDIVERGED if any err was non-finite (factors are left as they are). */
+/* Run one epoch -- every loaded rating updated once by the rule of PAPER.md:124-126 (§2.2: err = r - p.q,
+ * p += eta (err q - lambda p), q += eta (err p - lambda q), both from the pre-update snapshot, A-1) at
+ * eta_t -- under `schedule` (an mf_schedule: batch-Hogwild! PAPER.md:227-228, wavefront-update
+ * PAPER.md:239-245, deterministic waves DESIGN.md D-3, partitioned PAPER.md:287-305), then t += 1.
+ * Synchronous.  stats (may be NULL) receives the update count, device times, eta, workers and launches.
+ * MF_ESTATE before a load; MF_EINVAL for an unknown schedule; MF_EDIVERGED if any err was non-finite
+ * (factors are left as they are); MF_ECUDA / MF_ENCCL on device / NCCL failures. */
 int mf_epoch(mf_ctx *ctx, int schedule, mf_epoch_stats *stats);
 
 /* Streamed epoch: batch-Hogwild! (schedule must be MF_SCHED_HOGWILD) over caller ratings that are NOT
@@ -158,8 +171,11 @@ int mf_epoch_host(mf_ctx *ctx, int schedule, const int32_t *u, const int32_t *v,
  * a rank that did nothing wrong says which status a peer had). */
 int mf_rmse(mf_ctx *ctx, const int32_t *u, const int32_t *v, const float *r, int64_t nnz, double *out);
 
-/* Copy factors to caller host buffers, widened to fp32, row-major (P: m x k, Q: n x k); either may be NULL.
- * In the partitioned NCCL mode P is the local row segment and Q is the full matrix (collective). */
+/* Copy the factors P (m x k) and Q (stored n x k, i.e. the paper's Q^T, PAPER.md:116 / A-4) to caller-
+ * allocated host buffers, widened to fp32 from the storage precision, row-major; either may
+ * be NULL.  In the partitioned NCCL mode P is the local row segment and Q is the full matrix (collective:
+ * every rank must call).  Factors that do not exist yet are created first (A-7 init); MF_EINVAL for a null
+ * context; MF_ECUDA on copy failures. */
 int mf_get_factors(mf_ctx *ctx, float *P, float *Q);
 
 /* Overwrite factors from fp32 host/device buffers (rounded to storage, RNE); either may be NULL. */

@@ -984,11 +984,12 @@ int mf_ctx::run_wavefront(const ShapeId &, const UpdateArgs &ua, int *launches, 
         }));
     } else {
         const ShapeId sh = warp_shape(k, storage);
-        // samples of a block in flight per warp (MF_OPT_VARIANT bits 4..7: 2, 4 or 8; 0 = 4 for the full-row
-        // shapes).  The triples come from two 32-sample register tiles fetched before the lock, so the
-        // only latency on a sample's path is its row loads, issued `depth` samples ahead.
+        // samples of a block in flight per warp (MF_OPT_VARIANT bits 4..7: 2, 4 or 8; 0 = 2).  The triples
+        // come from two 32-sample register tiles fetched before the lock, so the only latency on a sample's
+        // path is its row loads, issued `depth` samples ahead (Netflix shape, s = 2,368: f16 D = 2 3.14 vs
+        // D = 4 2.94 G updates/s, fp32 2.63 vs 2.43; profiles/r02j_warp_C2.log)
         const int dsel = (variant_eff >> 4) & 0xF;
-        const int depth = dsel == 2 || dsel == 8 ? dsel : 4;
+        const int depth = dsel == 4 || dsel == 8 ? dsel : 2;
         CK(dispatch_warp_shape(sh, [&](auto tag) -> cudaError_t {
             using SH = decltype(tag);
             if constexpr (SH::FULL) {

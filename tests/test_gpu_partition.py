@@ -81,6 +81,31 @@ def test_loopback_serial_blocks_match_oracle_block_sweep(mf, G, storage, split):
     assert got_rmse == pytest.approx(ref.rmse(*test), rel=tol)
 
 
+@pytest.mark.parametrize("split", [0, 2])
+def test_layout_change_between_partitioned_epochs_keeps_q(mf, split):
+    """Changing a layout option (MF_OPT_SUBEPOCHS) between partitioned epochs rebuilds the layout; the
+    current Q, which lives only in the partitions' segment buffers after an epoch, must be gathered
+    first.  Exact mode: epoch 0 with S = 4, epoch 1 with S = 2 equals the oracle over the
+    reconstructed orders (fp32, 1e-5)."""
+    cfg = datagen.CONFIGS["C1"]
+    (u, v, r), test = datagen.make(cfg)
+    G = 3
+    with mf.MF(cfg.m, cfg.n, cfg.k, cfg.alpha, cfg.lam, cfg.seed_init, beta=cfg.beta, seed_shuffle=cfg.seed_shuffle,
+               partitions=G, workers=1, count_updates=1, part_split=split, subepochs=4) as g:
+        g.load(u, v, r)
+        perm = g.order()
+        assert g.epoch("partitioned").updates == len(u)
+        g.set(mf.MF_OPT_SUBEPOCHS, 2)
+        assert g.epoch("partitioned").updates == len(u)
+        P, Q = g.factors()
+    ref = oracle.Model(cfg.m, cfg.n, cfg.k, oracle.F32, seed=cfg.seed_init)
+    for e, S in ((0, 4), (1, 2)):
+        ref.epoch(u, v, r, oracle.eta(cfg.alpha, cfg.beta, e), cfg.lam,
+                  _block_sweep_order(mf, perm, u, v, cfg.m, cfg.n, G, cfg.seed_shuffle, e, S=S, split=split))
+    assert np.linalg.norm(P - ref.P) / np.linalg.norm(ref.P) <= 1e-5
+    assert np.linalg.norm(Q - ref.Q) / np.linalg.norm(ref.Q) <= 1e-5
+
+
 def test_loopback_hogwild_rmse_within_half_percent(mf):
     cfg = datagen.CONFIGS["C2-1pct"]
     (u, v, r), test = datagen.make(cfg)
