@@ -604,6 +604,10 @@ def run_partitioned(a, cfg, rank, world, local):
     du, dv, dr = (torch.from_numpy(x).cuda() for x in (u, v, r))
     dtu, dtv, dtr = (torch.from_numpy(x).cuda() for x in (tu, tv, tr))
     g.load(du, dv, dr)
+    # the library keeps its own copy; at the Hugewiki shape on few GPUs the staging tensors would otherwise
+    # hold 12 B/sample of HBM through the partition layout's sort (R + layout + sort keys + P)
+    del du, dv, dr
+    torch.cuda.empty_cache()
 
     def step():
         st = g.epoch("partitioned")
@@ -632,6 +636,8 @@ def run_partitioned(a, cfg, rank, world, local):
     n_tot = float(n_tot)
     value = n_tot / (ms * 1e-3)
     k_s = statistics.mean(kern)
+    t_full = load_traffic(a.storage, cfg.name, "hogwild")
+    traffic_loc = t_full * N_loc / cfg.n_train if t_full and a.scaling == "strong" else None
     g.close()
 
     hu, hv, hr = (torch.from_numpy(x).pin_memory() for x in (u, v, r))
@@ -664,8 +670,10 @@ def run_partitioned(a, cfg, rank, world, local):
                     "in_flight_per_q_column": st.workers / max(1, cfg.n // G),
                     "note": "accuracy falls with in-flight ratings per Q-segment column (DESIGN.md 5.5)"},
             "test_rmse": rm,
-            "roofline": dict(roofline(cfg, a.storage, N_loc, k_s, None, "hogwild"),
-                             kernel="k_hogwild (rank 0, all launches of the epoch)"),
+            "roofline": dict(roofline(cfg, a.storage, N_loc, k_s, traffic_loc, "hogwild"),
+                             kernel="k_hogwild (rank 0, all launches of the epoch)",
+                             traffic_basis="ncu DRAM bytes of the one-GPU batch-Hogwild! launch on this config, "
+                                           "scaled to the rank's share of the ratings" if traffic_loc else None),
             "cpu_baseline": None,
             "e2e": {"value": n_tot / (float(e2e_ms) * 1e-3), "unit": "updates/s",
                     "h2d_bytes_per_step": 12 * N_loc * G + 12 * len(tu) * G, "d2h_bytes_per_step": 8 * G,

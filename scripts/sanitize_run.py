@@ -24,7 +24,12 @@ def main():
                                 ("wavefront", {"wave_cta": 1}), ("wavefront", {"wave_cta": 1, "variant": 1 << 16}),
                                 ("wavefront", {"wave_cta": 1, "variant": 2 << 16}),
                                 ("wavefront", {"wave_cta": 1, "variant": 2 << 20}), ("wavefront", {"wave_cta": 2}),
-                                ("partitioned", {"partitions": 3})):
+                                ("wavefront", {"wave_cta": 3}), ("wavefront", {"wave_cta": 3, "variant": 8 << 4}),
+                                ("wavefront", {"variant": 4 << 4}), ("wavefront", {"variant": 8 << 4}),
+                                ("hogwild", {"r_staging": 2}), ("hogwild", {"r_staging": 2, "batch_f": 96}),
+                                ("deterministic", {"variant": 1 << 22}),
+                                ("partitioned", {"partitions": 3}), ("partitioned", {"partitions": 3, "part_split": 0}),
+                                ("partitioned", {"partitions": 3, "part_split": 1})):
                 g = mf.MF(cfg.m, cfg.n, k, cfg.alpha, cfg.lam, cfg.seed_init, storage=storage, beta=cfg.beta,
                           count_updates=1, trace=1, **opts)
                 g.load(u, v, r)

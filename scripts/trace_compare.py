@@ -22,6 +22,7 @@ def main():
     ap.add_argument("--cfg", default="C3")
     ap.add_argument("--storage", default="f16")
     ap.add_argument("--epochs", type=int, default=20)
+    ap.add_argument("--shuffle", type=int, default=1, help="MF_OPT_SHUFFLE (0 for the full Hugewiki shape: i.i.d. draws)")
     ap.add_argument("--scheds", default="deterministic,hogwild,wavefront_cta",
                     help="comma list; partitioned:G runs G loopback partitions")
     a = ap.parse_args()
@@ -46,7 +47,7 @@ def main():
         for kv in extra:
             opts[kv.split("=")[0]] = int(kv.split("=")[1])
         with mf.MF(cfg.m, cfg.n, cfg.k, cfg.alpha, cfg.lam, cfg.seed_init, storage=a.storage, beta=cfg.beta,
-                   seed_shuffle=cfg.seed_shuffle, **opts) as g:
+                   seed_shuffle=cfg.seed_shuffle, shuffle=a.shuffle, **opts) as g:
             g.load(u, v, r)
             tr, ks = [], []
             for _ in range(a.epochs):

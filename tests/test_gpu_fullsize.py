@@ -76,7 +76,11 @@ def _gates(storage, gold):
 
 @pytest.mark.parametrize("storage", ["f32", "f16"])
 def test_c2_wavefront_cta_rmse_trace_vs_oracle_golden(c2, storage):
-    """The wavefront schedule with CTA workers (bench.py's throughput configuration) at full size."""
+    """The wavefront schedule with CTA workers (bench.py's throughput configuration) at full size, one run,
+    every epoch from the fourth gated against the oracle's trace (0.5%, or the oracle's own shuffle-seed
+    spread where larger: DESIGN.md T3).  Its first epochs trail serial SGD (blocked order, T6 and
+    5.4: +265% after epoch 1, +11% after epoch 2, +1.2% after epoch 3 in fp16); they are checked to be
+    finite and descending, and reported in DESIGN.md, not gated."""
     path = os.path.join(GOLD, f"C2_{storage}_trace.json")
     if not os.path.exists(path):
         pytest.skip(f"{path} not generated yet")
@@ -84,11 +88,15 @@ def test_c2_wavefront_cta_rmse_trace_vs_oracle_golden(c2, storage):
     cfg, ((u, v, r), test) = c2
     with _ctx(cfg, storage, count_updates=1, wave_cta=1) as g:
         g.load(u, v, r)
+        got = []
         for t in range(len(gold)):
             st = g.epoch("wavefront")
             assert st.updates == len(u)
-        got = g.rmse(*test)
-    assert abs(got - gold[-1]) <= 0.005 * gold[-1], (got, gold[-1])
+            got.append(g.rmse(*test))
+    assert all(np.isfinite(got)) and got[0] > got[1] > got[2]
+    gate = _gates(storage, gold)
+    bad = [(t + 1, a, b, gt) for t, (a, b, gt) in enumerate(zip(got, gold, gate)) if t >= 3 and abs(a - b) > gt]
+    assert not bad, bad
 
 
 @pytest.mark.parametrize("storage", ["f32", "f16"])
