@@ -298,11 +298,29 @@ int mf_ctx::build_partition() {
     seg_valid = false;
 
     cudaStream_t st = stream();
-    // passes per epoch: auto = 4.  Serial block-sweep simulation on C2-1pct, 10 epochs, test RMSE vs
-    // the shuffled serial order: S = 1 costs +10..+20%; S = 4 is within 0.05% for G <= 4 and +0.37% at
-    // G = 8 (S = 8: 0.00%).  Every pass costs G launches (2G with MF_OPT_PART_SPLIT = 1; ~35 us fixed
-    // each at this size), so the throughput default is 4.
-    const int S_req = subepochs > 0 ? subepochs : 4;
+    // Passes per epoch S (auto).  In a pass every Q unit is visited once by each partition, so a Q row
+    // takes (N / n) / (S G) consecutive updates from one row segment per visit.  Serial block-sweep
+    // simulation on C2-1pct: S = 1 costs +10..+20% in test RMSE, S = 4 is within 0.05% for G <= 4.  At the
+    // full Hugewiki shape (N / n = 77k ratings per column) S = 4 leaves 2.4k-9.6k updates per visit and
+    // the schedule far behind serial SGD (G = 2 / 4 / 8: +59% / +8.7% / +3.5% after 10 epochs,
+    // profiles/r02m_c4_traces.jsonl), while the Hugewiki parity slice (<= ~1k per visit) stays within
+    // 0.5%.  So S = max(4, ceil(N_total / (n G kVisit))) caps a visit at kVisit updates per Q row; every
+    // pass costs 2G launches (~25-35 us fixed each), so the cap is not smaller.  With NCCL every rank
+    // must run the same S: N_total is all-reduced.
+    constexpr double kVisit = 1000.0;
+    int64_t n_total = N;
+    if (is_distributed()) {
+        if (!agree_buf) CK(cudaMalloc((void **)&agree_buf, sizeof(double) * 8));
+        const double mine = (double)N;
+        CK(cudaMemcpyAsync(agree_buf, &mine, sizeof(double), cudaMemcpyHostToDevice, st));
+        NK(ncclAllReduce(agree_buf, agree_buf, 1, ncclFloat64, ncclSum, nccl->comm, st));
+        double tot = 0.0;
+        CK(cudaMemcpyAsync(&tot, agree_buf, sizeof(double), cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        n_total = (int64_t)tot;
+    }
+    const int S_auto = (int)std::min<double>(512.0, std::max(4.0, std::ceil((double)n_total / ((double)n * G * kVisit))));
+    const int S_req = subepochs > 0 ? subepochs : S_auto;
     const int S = (int)std::max<int64_t>(1, std::min<int64_t>(S_req, std::max<int64_t>(1, N)));
     const int64_t nb = (int64_t)S * local * G * 2;
     if (nb >= (1ll << 31)) return fail(MF_EINVAL, "partitioned: too many blocks (S * G * G * 2)");

@@ -209,6 +209,37 @@ def test_c4_full_size_exactly_once_beyond_int32():
     assert r1 < 0.5 * r0 and r2 < r1, (r0, r1, r2)
 
 
+def test_c4_full_size_schedules_track_serial_sgd():
+    """BASELINE.json configs[3] at FULL size on one GPU (3.07B ratings; the serial CPU oracle would need
+    ~2.5 hours per epoch): exact serial SGD is the deterministic schedule (pinned to the oracle's factors at
+    1e-5 / 2e-3 on the slices, and to its test RMSE at 0.001% on the C4-rows100 slice), and batch-Hogwild!
+    and the partitioned schedule at G = 2 / 4 / 8 loopback partitions -- the per-partition worker counts,
+    passes and Latin squares G GPUs would run -- must be within 0.5% of its test RMSE from the 4th epoch
+    (fp16).  With the round-1 fixed 4 passes per epoch the partitioned schedule was +59% / +8.7% / +3.5%
+    behind after 10 epochs; the auto pass count caps a Q row's updates per visit."""
+    from paper_1610_05838_b200 import mf
+    cfg = datagen.CONFIGS["C4"]
+    (u, v, r), test = datagen.make(cfg)
+    E = 5
+    traces = {}
+    for name, sched, opts in (("serial", "deterministic", {}), ("hogwild", "hogwild", {}),
+                              ("G2", "partitioned", {"partitions": 2}), ("G4", "partitioned", {"partitions": 4}),
+                              ("G8", "partitioned", {"partitions": 8})):
+        with _ctx(cfg, "f16", count_updates=1, shuffle=0, **opts) as g:
+            g.load(u, v, r)
+            tr = []
+            for _ in range(E):
+                assert g.epoch(sched).updates == len(u)
+                tr.append(g.rmse(*test))
+            if sched == "partitioned":
+                assert int(g.get(mf.MF_OPT_SUBEPOCHS)) == 0  # auto
+        traces[name] = tr
+    ref = traces.pop("serial")
+    bad = [(name, t + 1, a, b) for name, tr in traces.items() for t, (a, b) in enumerate(zip(tr, ref))
+           if t >= 3 and abs(a - b) > 0.005 * b]
+    assert not bad, (bad, traces, ref)
+
+
 # ------------------------------------------------- Hugewiki shape, parity slice
 # SURVEY §8(d): the C4 parity config is C4-rows/10 (m = 5,008,260, n = 39,781 kept, N = 306,981,798).
 # Golden: scripts/make_golden.py C4-rows10 f32 10 (and seed 43), oracle/ only.
