@@ -627,7 +627,8 @@ static int epoch_local(mf_ctx *ctx, int schedule, mf_epoch_stats *stats) {
     ctx->seg_valid = false;
     cudaStream_t st = ctx->stream();
     const float eta = ctx->eta_at(ctx->epoch);
-    const ShapeId sh = select_shape(ctx->k, ctx->storage, ctx->variant & 0xF);
+    const ShapeId sh = schedule == MF_SCHED_HOGWILD ? hogwild_shape(ctx->k, ctx->storage, ctx->variant & 0xF)
+                                                    : select_shape(ctx->k, ctx->storage, ctx->variant & 0xF);
     CK(cudaEventRecord(ctx->events[0], st));
     CK(cudaMemsetAsync(ctx->scratch, 0, sizeof(DevScratch), st));
     UpdateArgs a = ctx->update_args(eta);

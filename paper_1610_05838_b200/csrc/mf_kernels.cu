@@ -100,6 +100,15 @@ ShapeId select_shape(int k, int storage, int variant) {
     return select_generic_shape(k, storage);
 }
 
+// batch-Hogwild!'s default shape (MF_OPT_VARIANT bits 0..3 = 0).  16-bit rows at k = 128: one rating per
+// warp, 32 lanes x 8-byte vectors (a row is one 256-B warp access) -- after the warp-uniform index change
+// (47 -> 32 registers) it keeps 64 warps per SM resident: Netflix shape 11.2 vs 10.5 G updates/s for the
+// 16-lane 16-byte shape, Yahoo shape 7.0 vs 7.1 (profiles/r02p_f16_*).  Everything else as select_shape.
+ShapeId hogwild_shape(int k, int storage, int variant) {
+    if (variant == 0 && k == 128 && storage != kF32) return {storage, 32, 1, 8, 1};
+    return select_shape(k, storage, variant);
+}
+
 // generic: L = 32, VB = 4 bytes (or 2 for odd k with 16-bit storage), V vectors per lane
 ShapeId select_generic_shape(int k, int storage) {
     const int bytes = storage == kF32 ? 4 : 2;
@@ -552,16 +561,17 @@ cudaError_t launch_hogwild(const ShapeId &sh, const UpdateArgs &a_in, int worker
         if constexpr (SH::FULL) {
             if (tma && D != 4) {
                 if (workers > 0 && workers < 64) return hogwild_launch<SH, 1, true>(a, workers, st, workers_used);
-                const bool two = D == 2 || D == 3 || (D == 0 && SH::S == kF32 && SH::KMAX >= 128);
+                const bool two = D == 2 || D == 3 || (D == 0 && SH::S == kF32 && SH::KMAX >= 256);
                 if (two && L % 2 == 0) return hogwild_launch<SH, (L % 2 == 0 ? 2 : 1), true>(a, workers, st, workers_used);
                 return hogwild_launch<SH, 1, true>(a, workers, st, workers_used);
             }
             if (workers > 0 && workers < 64) return hogwild_launch<SH, 1>(a, workers, st, workers_used);
             if (D == 4 && L % 4 == 0) return hogwild_launch<SH, (L % 4 == 0 ? 4 : 1)>(a, workers, st, workers_used);
-            // D = 0 (auto): two ratings in flight per group for fp32 rows of k >= 128, one otherwise
-            // (Netflix shape: k = 128 fp32 5.6 vs 5.2 G/s, fp16 8.3 vs 10.1; k = 32 / 64 fp32 one in
-            // flight +28% / +15%; r01_cta_shapes.log, r01c_smallk_probe.log)
-            const bool two = D == 2 || D == 3 || (D == 0 && SH::S == kF32 && SH::KMAX >= 128);
+            // D = 0 (auto): two ratings in flight per group for fp32 rows of k >= 256, one otherwise (round 1
+            // had two for k = 128 fp32: 5.6 vs 5.2 G/s then; since the warp-uniform index change one is
+            // faster -- Netflix shape 5.45 vs 5.27, Yahoo 3.34 vs 3.21, profiles/r02p_f32_*; k = 32 / 64
+            // fp32 one in flight +28% / +15%, r01c_smallk_probe.log)
+            const bool two = D == 2 || D == 3 || (D == 0 && SH::S == kF32 && SH::KMAX >= 256);
             if (two && L % 2 == 0) return hogwild_launch<SH, (L % 2 == 0 ? 2 : 1)>(a, workers, st, workers_used);
         }
         return hogwild_launch<SH, 1>(a, workers, st, workers_used);

@@ -81,6 +81,7 @@ cudaError_t launch_gather(const int32_t *u_in, const int32_t *v_in, const float 
                           int32_t *u_out, int32_t *v_out, float *r_out, cudaStream_t st);
 
 ShapeId select_shape(int k, int storage, int variant);
+ShapeId hogwild_shape(int k, int storage, int variant);  // batch-Hogwild!'s default (variant 0) differs at k = 128
 ShapeId select_generic_shape(int k, int storage);
 int rmse_parts();
 

@@ -257,28 +257,30 @@ def c4r10():
     return cfg, datagen.make(cfg)
 
 
-@pytest.mark.parametrize("schedule,G,split", [
-    ("hogwild", 1, 0), ("partitioned", 2, 2), ("partitioned", 4, 2), ("partitioned", 8, 2),
-    ("partitioned", 2, 0), ("partitioned", 4, 0), ("partitioned", 8, 0),
-    pytest.param("partitioned", 4, 1, marks=pytest.mark.xfail(
+@pytest.mark.parametrize("storage,schedule,G,split", [
+    ("f32", "hogwild", 1, 0), ("f32", "partitioned", 2, 2), ("f32", "partitioned", 4, 2), ("f32", "partitioned", 8, 2),
+    ("f32", "partitioned", 2, 0), ("f32", "partitioned", 4, 0), ("f32", "partitioned", 8, 0),
+    pytest.param("f32", "partitioned", 4, 1, marks=pytest.mark.xfail(
         strict=False, reason="the pipelined half-segment form (MF_OPT_PART_SPLIT = 1) puts a launch's 7,674 "
                              "in-flight ratings on half of a 9,945-column Q segment: +0.69% after 10 epochs "
-                             "(DESIGN.md 5.5)"))])
-def test_c4_rows10_rmse_vs_oracle_golden(c4r10, schedule, G, split):
+                             "(DESIGN.md 5.5)")),
+    ("f16", "hogwild", 1, 0), ("f16", "partitioned", 2, 2), ("f16", "partitioned", 4, 2), ("f16", "partitioned", 8, 2)])
+def test_c4_rows10_rmse_vs_oracle_golden(c4r10, storage, schedule, G, split):
     """BASELINE.json configs[3] (R-block grid partition at 2 / 4 / 8 GPUs) at its parity size: the
     partitioned schedule with G partitions (the loopback transport: the same layout, Latin-square
-    rounds, passes and pipelined half-segment hand-over as G GPUs, run on this one) and batch-Hogwild!
-    end the oracle's 10 epochs within 0.5% of its test RMSE (the north star's gate, "after the same
-    number of epochs").  The model is still descending there (-0.5% per epoch), so a schedule's lag
-    shows as its deviation; earlier epochs are reported in DESIGN.md 5.5, not gated.  The pipelined
-    half-segment form doubles the ratings in flight per Q column and lags more than the gate at G = 4."""
-    path = os.path.join(GOLD, "C4-rows10_f32_trace.json")
+    rounds, passes and unit hand-overs as G GPUs, run on this one) and batch-Hogwild! end the oracle's
+    10 epochs within 0.5% of its test RMSE (the north star's gate, "after the same number of epochs"),
+    in fp32 and in the paper's half precision.  The model is still descending there (-0.5% per
+    epoch), so a schedule's lag shows as its deviation; earlier epochs are reported in DESIGN.md 5.5, not
+    gated.  The pipelined half-segment form doubles the ratings in flight per Q column and lags more
+    than the gate at G = 4."""
+    path = os.path.join(GOLD, f"C4-rows10_{storage}_trace.json")
     if not os.path.exists(path):
         pytest.skip(f"{path} not generated yet")
     gold = json.load(open(path))["rmse"]
     cfg, ((u, v, r), test) = c4r10
     opts = {"partitions": G, "part_split": split} if schedule == "partitioned" else {}
-    with _ctx(cfg, "f32", count_updates=1, **opts) as g:
+    with _ctx(cfg, storage, count_updates=1, **opts) as g:
         g.load(u, v, r)
         for _ in range(len(gold)):
             assert g.epoch(schedule).updates == len(u)
