@@ -104,9 +104,12 @@ typedef enum {
                                  (P:307-314); 0 = one launch per whole block, hand-over after it; 1 = each block as two
                                  half-segment sub-blocks in sequence with all workers each -- twice the ratings in flight
                                  per Q column, so further from serial SGD */
-    MF_OPT_R_STAGING = 20     /* batch-Hogwild! rating batches: 1 = registers (three coalesced 32-bit loads per lane per 32-sample
+    MF_OPT_R_STAGING = 20,    /* batch-Hogwild! rating batches: 1 = registers (three coalesced 32-bit loads per lane per 32-sample
                                  tile, handed to the groups by shuffles); 2 = staged in shared memory by the TMA engine (bulk
                                  copies of each chunk's u, v, r, double-buffered per warp; needs 16-B aligned arrays, else 1) */
+    MF_OPT_WAVE_PASSES = 21   /* wavefront: passes P per epoch, each over 1/P of the shuffled samples with fresh column
+                                 sequences for every worker (0 = auto: blocks of >= 16k samples for CTA workers, >= 64
+                                 for warp workers) */
 } mf_option;
 
 typedef struct {

@@ -323,6 +323,11 @@ extern "C" int mf_set_option(mf_ctx *ctx, int key, double value) {
             ctx->part_split = (int)iv;
             ctx->part_valid = false;
             return MF_OK;
+        case MF_OPT_WAVE_PASSES:
+            if (iv < 0 || iv > 4096) return ctx->fail(MF_EINVAL, "wave passes must be in [0 (auto), 4096]");
+            ctx->wave_passes = (int)iv;
+            ctx->wf_valid = false;
+            return MF_OK;
         case MF_OPT_R_STAGING:
             if (iv < 1 || iv > 2) return ctx->fail(MF_EINVAL, "R staging must be 1 (registers) or 2 (TMA)");
             ctx->r_stage = (int)iv;
@@ -363,6 +368,7 @@ extern "C" int mf_get_option(const mf_ctx *ctx, int key, double *value) {
         case MF_OPT_STREAM_CHUNK: *value = (double)ctx->stream_chunk; return MF_OK;
         case MF_OPT_PART_SPLIT: *value = ctx->part_split; return MF_OK;
         case MF_OPT_R_STAGING: *value = ctx->r_stage; return MF_OK;
+        case MF_OPT_WAVE_PASSES: *value = ctx->wf_valid ? ctx->wf_p : ctx->wave_passes; return MF_OK;
         default: return MF_EINVAL;
     }
 }

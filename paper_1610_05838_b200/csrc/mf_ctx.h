@@ -28,6 +28,7 @@ struct mf_ctx {
     int workers = 0;
     int batch_f = 256;
     int wave_rows = 0, wave_cols = 0, wave_perm = 0;
+    int wave_passes = 0;  // MF_OPT_WAVE_PASSES (0 = 1)
     int shuffle = 1;
     int count_updates = 0;
     int partitions = 0;
@@ -100,7 +101,7 @@ struct mf_ctx {
 
     // wavefront layout (mf_wavefront.cu)
     bool wf_valid = false;
-    int wf_s = 0, wf_c = 0;
+    int wf_s = 0, wf_c = 0, wf_p = 1;
     int32_t *fu = nullptr, *fv = nullptr;
     float *fr = nullptr;
     int64_t *wf_off = nullptr;    // (s*c + 1) block offsets, block (w, c) at w*c + c

@@ -35,11 +35,13 @@ namespace {
 
 
 // row band / column group by balanced segmentation (widths differ by at most one; A-9)
+// pass p of stored sample i is floor(i * P / n): every epoch is P passes over consecutive slices of the
+// shuffled order, each with its own column sequences (block id = (p * s + band) * c + group)
 __global__ void k_block_keys(const int32_t *u, const int32_t *v, int64_t n, int64_t rows, int64_t cols, int s,
-                             int c, uint32_t *keys, uint32_t *idx) {
+                             int c, int P, uint32_t *keys, uint32_t *idx) {
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t b = seg_index(u[i], rows, s), g = seg_index(v[i], cols, c);
-        keys[i] = (uint32_t)(b * c + g);
+        const int64_t b = seg_index(u[i], rows, s), g = seg_index(v[i], cols, c), p = (i * P) / n;
+        keys[i] = (uint32_t)((p * s + b) * c + g);
         idx[i] = (uint32_t)i;
     }
 }
@@ -47,18 +49,19 @@ __global__ void k_block_keys(const int32_t *u, const int32_t *v, int64_t n, int6
 // q-stationary layout (MF_OPT_WAVE_CTA = 3): key = band * n + v, so a block (band, column group) is a
 // contiguous key range and inside it the samples of one Q row (a "run") are contiguous, each run in
 // shuffled order (the sort is stable)
-__global__ void k_run_keys(const int32_t *u, const int32_t *v, int64_t n, int64_t rows, int64_t cols, int s,
+__global__ void k_run_keys(const int32_t *u, const int32_t *v, int64_t n, int64_t rows, int64_t cols, int s, int P,
                            uint32_t *keys, uint32_t *idx) {
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-        keys[i] = (uint32_t)((int64_t)seg_index(u[i], rows, s) * cols + v[i]);
+        const int64_t p = (i * P) / n;
+        keys[i] = (uint32_t)((p * s + seg_index(u[i], rows, s)) * cols + v[i]);
         idx[i] = (uint32_t)i;
     }
 }
 
 // block offsets of the q-stationary layout: off[b] = first sorted position with key >= band * n +
 // first column of group g (b = band * c + g), off[s * c] = n; one binary search per block
-__global__ void k_run_block_offsets(const uint32_t *sorted_keys, int64_t n, int s, int c, int64_t cols, int64_t *off) {
-    const int64_t nb = (int64_t)s * c;
+__global__ void k_run_block_offsets(const uint32_t *sorted_keys, int64_t n, int64_t nb, int c, int64_t cols,
+                                    int64_t *off) {
     for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b <= nb; b += (int64_t)gridDim.x * blockDim.x) {
         if (b == nb) {
             off[b] = n;
@@ -94,6 +97,8 @@ struct WfArgs {
     int64_t *trace;       // optional, 4 per block
     DevScratch *scratch;
     int s, c, k, latin, count_updates;
+    int passes;           // P: the epoch is P passes over consecutive slices of the shuffled samples, each with
+                          // its own column sequences (seq holds P of them)
     int pf;               // CTA workers: L2 prefetch of a tile's P rows when it is claimed (0 off, 1 bulk, 2 per line)
     int min_per_group;    // CTA workers: in-block concurrency clamp, samples per concurrent group
     int tma;              // CTA workers: stage the Q group with bulk async copies (TMA engine) instead of a thread loop
@@ -133,6 +138,17 @@ __device__ __forceinline__ void lock_acquire_warp(int32_t *lock, int lane) {
     }
 }
 
+// column of worker w at step pj = pass * c + wave: Latin rectangle sigma_p((rho_p(w) + j) mod c), or the
+// worker's own random permutation of pass p
+__device__ __forceinline__ int wf_column(const WfArgs &a, int w, int pj) {
+    const int c = a.c, p = pj / c, j = pj - p * c;
+    if (a.latin) {
+        const int32_t *sq = a.seq + (int64_t)p * (c + a.s);
+        return sq[(sq[c + w] + j) % c];
+    }
+    return a.seq[((int64_t)p * a.s + w) * c + j];
+}
+
 __device__ __forceinline__ int64_t globaltimer() {
     int64_t t;
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -152,10 +168,10 @@ __global__ void __launch_bounds__(32) k_wavefront(WfArgs a) {
     const int c = a.c;
     int bad = 0;
     unsigned long long done = 0;
-    for (int j = 0; j < c; j++) {
-        const int col = a.latin ? a.seq[(a.seq[c + w] + j) % c] : a.seq[(int64_t)w * c + j];
+    for (int pj = 0; pj < a.passes * c; pj++) {  // pass pj / c, wave pj % c
+        const int col = wf_column(a, w, pj);
         int32_t *lock = a.locks + col;
-        const int64_t blk = (int64_t)w * c + col;
+        const int64_t blk = ((int64_t)(pj / c) * a.s + w) * c + col;
         const int64_t lo = a.off[blk], hi = a.off[blk + 1];
         // The block's triples are this worker's alone: fetch the first two 32-sample tiles (lane i holds
         // sample tb + i) before taking the lock, so only the Q rows wait for it.
@@ -449,9 +465,9 @@ __global__ void __launch_bounds__(THREADS, THREADS >= 1024 ? 1 : kCtaThreads / T
     unsigned long long done = 0;
     if (a.tma && threadIdx.x == 0) mbar_init((uint32_t)__cvta_generic_to_shared(&s_bar));
     __syncthreads();
-    for (int j = 0; j < c; j++) {
+    for (int pj = 0; pj < a.passes * c; pj++) {  // pass pj / c, wave pj % c
         if (threadIdx.x == 0) {
-            const int col = a.latin ? a.seq[(a.seq[c + w] + j) % c] : a.seq[(int64_t)w * c + j];
+            const int col = wf_column(a, w, pj);
             while (atomicCAS(a.locks + col, 0, 1) != 0) __nanosleep(64);
             __threadfence();  // acquire
             s_col = col;
@@ -468,13 +484,13 @@ __global__ void __launch_bounds__(THREADS, THREADS >= 1024 ? 1 : kCtaThreads / T
                 bulk_copy_in(qbase, qg, (uint32_t)(nrows * row_bytes), (uint32_t)__cvta_generic_to_shared(&s_bar));
             }
             // every group has >= 1 row (c <= n), so block j completes the barrier's phase j
-            mbar_wait((uint32_t)__cvta_generic_to_shared(&s_bar), (uint32_t)j & 1u);
+            mbar_wait((uint32_t)__cvta_generic_to_shared(&s_bar), (uint32_t)pj & 1u);
         } else {
             cta_copy_in(qs, qg, nrows * row_bytes);
             __syncthreads();
         }
         const int64_t t0 = a.trace ? globaltimer() : 0;
-        const int64_t blk = (int64_t)w * c + col;
+        const int64_t blk = ((int64_t)(pj / c) * a.s + w) * c + col;
         const int64_t lo = a.off[blk], hi = a.off[blk + 1];
         // 32-sample tiles.  (Claiming smaller tiles near the end of a block balances the warps but
         // raises the number of a small block's samples in flight at once -- more write conflicts on
@@ -584,9 +600,9 @@ __global__ void __launch_bounds__(THREADS, 1) k_wavefront_q(WfArgs a) {
     const int active_warps = a.min_per_group > 0 ? a.min_per_group : THREADS / 32;  // warps claiming runs
     float chk = 0.f;
     unsigned long long done = 0;
-    for (int j = 0; j < c; j++) {
+    for (int pj = 0; pj < a.passes * c; pj++) {  // pass pj / c, wave pj % c
         if (threadIdx.x == 0) {
-            const int col = a.latin ? a.seq[(a.seq[c + w] + j) % c] : a.seq[(int64_t)w * c + j];
+            const int col = wf_column(a, w, pj);
             lock_acquire(a.locks + col);
             __threadfence();  // acquire
             s_col = col;
@@ -596,7 +612,7 @@ __global__ void __launch_bounds__(THREADS, 1) k_wavefront_q(WfArgs a) {
         const int col = s_col;
         const int64_t q0 = seg_begin(a.n_cols, c, col);
         const int nrows = (int)(seg_begin(a.n_cols, c, col + 1) - q0);
-        const int64_t blk = (int64_t)w * c + col;
+        const int64_t blk = ((int64_t)(pj / c) * a.s + w) * c + col;
         const int64_t lo = a.off[blk], hi = a.off[blk + 1];
         const int64_t t0 = a.trace ? globaltimer() : 0;
         // run table: run_start[r] = first block position whose Q row is >= q0 + r, r in [0, nrows]
@@ -806,9 +822,28 @@ int mf_ctx::build_wavefront() {
     if (c <= 0) c = (int)std::min<int64_t>(warp_auto ? std::max<int64_t>(s, (5 * (int64_t)s + 3) / 4) : 2 * (int64_t)s, n);
     if (s > rows || c > n || s < 1 || c < s)
         return fail(MF_EINVAL, "wavefront needs 1 <= s <= c, s <= m, c <= n (s=%d c=%d)", s, c);
-    if ((int64_t)s * c >= (1ll << 32)) return fail(MF_EINVAL, "wavefront grid s*c too large");
+    // Passes per epoch (MF_OPT_WAVE_PASSES): each pass walks every worker through all c column groups with
+    // fresh sequences, over 1/P of the shuffled samples.  With one pass every row band meets the column
+    // groups in one fixed cyclic order per epoch -- each user's ratings are processed sorted by column
+    // group -- and on the Hugewiki shape (61 ratings per user, 140k-sample blocks) the wavefront never
+    // catches up with serial SGD (test RMSE after 5 epochs: CTA workers 0.40-0.51, warp workers +13% after
+    // 4; batch-Hogwild! 0.1675).  P passes split each user's ratings into P slices visited in independent
+    // orders: P = 8 brings both forms to serial SGD's trajectory (-0.3..-0.6% from epoch 2) at 7% / 10%
+    // more time per epoch; on the Netflix shape P = 4 also removes the first-epoch lag (+1.5% instead of
+    // +265% after epoch 1) but costs the CTA form 70% (4x the blocks at 4.5k samples each, each paying
+    // its Q-group staging and lock hand-over; profiles/r02r_*).  Auto: as many passes as keep blocks at
+    // >= 16k samples (CTA workers) / >= 64 samples (warp workers): Hugewiki 8 / 6, Netflix and Yahoo 1.
+    int npass_auto = 1;
+    {
+        const double per_block = (double)N / ((double)s * (double)c);
+        const double bmin = wave_cta ? 16384.0 : 64.0;
+        npass_auto = (int)std::max(1.0, std::min(64.0, std::floor(per_block / bmin)));
+    }
+    const int npass = (int)std::max<int64_t>(1, std::min<int64_t>(wave_passes > 0 ? wave_passes : npass_auto,
+                                                                  std::max<int64_t>(1, N)));
+    if ((int64_t)npass * s * c >= (1ll << 32)) return fail(MF_EINVAL, "wavefront grid P*s*c too large");
     cudaStream_t st = stream();
-    const int64_t nb = (int64_t)s * c;
+    const int64_t nb = (int64_t)npass * s * c;
     uint32_t *k0 = nullptr, *k1 = nullptr, *i0 = nullptr, *i1 = nullptr;
     void *tmp = nullptr;
     size_t tmp_bytes = 0;
@@ -823,17 +858,17 @@ int mf_ctx::build_wavefront() {
     CK(cudaMallocAsync((void **)&i1, sizeof(uint32_t) * N, st));
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((N + 255) / 256, 148 * 16));
     const bool runs = wave_cta == 3;
-    const uint64_t key_range = runs ? (uint64_t)s * (uint64_t)n : (uint64_t)nb;
-    if (key_range >= (1ull << 32)) return fail(MF_EINVAL, "wavefront: s * n too large for the run layout");
-    if (runs) k_run_keys<<<grid, 256, 0, st>>>(u, v, N, rows, n, s, k0, i0);
-    else k_block_keys<<<grid, 256, 0, st>>>(u, v, N, rows, n, s, c, k0, i0);
+    const uint64_t key_range = runs ? (uint64_t)npass * s * (uint64_t)n : (uint64_t)nb;
+    if (key_range >= (1ull << 32)) return fail(MF_EINVAL, "wavefront: P * s * n too large for the run layout");
+    if (runs) k_run_keys<<<grid, 256, 0, st>>>(u, v, N, rows, n, s, npass, k0, i0);
+    else k_block_keys<<<grid, 256, 0, st>>>(u, v, N, rows, n, s, c, npass, k0, i0);
     CK(cudaGetLastError());
     int bits = 1;
     while (bits < 32 && (1ull << bits) < key_range) bits++;
     CK(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, k0, k1, i0, i1, N, 0, bits, st));
     CK(cudaMallocAsync(&tmp, tmp_bytes, st));
     CK(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, k0, k1, i0, i1, N, 0, bits, st));  // stable
-    if (runs) k_run_block_offsets<<<grid, 256, 0, st>>>(k1, N, s, c, n, wf_off);
+    if (runs) k_run_block_offsets<<<grid, 256, 0, st>>>(k1, N, nb, c, n, wf_off);
     else k_block_offsets<<<grid, 256, 0, st>>>(k1, N, nb, wf_off);
     CK(cudaGetLastError());
     CK(launch_gather(u, v, r, i1, N, fu, fv, fr, st));
@@ -846,35 +881,38 @@ int mf_ctx::build_wavefront() {
     CK(cudaStreamSynchronize(st));
     wf_s = s;
     wf_c = c;
+    wf_p = npass;
     wf_valid = true;
     return MF_OK;
 }
 
 int mf_ctx::run_wavefront(const ShapeId &, const UpdateArgs &ua, int *launches, int *workers_used) {
     cudaStream_t st = stream();
-    const int s = wf_s, c = wf_c;
-    // column sequences for this epoch (host, counter-hash Fisher-Yates keyed by seed and epoch)
-    const uint64_t key = host_mix(seed_shuffle ^ 0x5eedull ^ ((uint64_t)epoch << 32));
+    const int s = wf_s, c = wf_c, npass = wf_p;
+    // column sequences for this epoch, one set per pass (host, counter-hash Fisher-Yates keyed by seed, epoch
+    // and pass; pass 0's key is the single-pass key)
     std::vector<int32_t> seq;
-    if (wave_perm == 0) {
-        std::vector<int32_t> sigma, rho;
-        permutation(sigma, c, key);
-        permutation(rho, c, host_mix(key + 1));
-        seq = sigma;
-        seq.insert(seq.end(), rho.begin(), rho.begin() + s);
-    } else {
-        seq.resize((size_t)s * c);
-        std::vector<int32_t> pw;
-        for (int w = 0; w < s; w++) {
-            permutation(pw, c, host_mix(key + 2 + (uint64_t)w));
-            std::copy(pw.begin(), pw.end(), seq.begin() + (size_t)w * c);
+    for (int p = 0; p < npass; p++) {
+        const uint64_t key = host_mix(seed_shuffle ^ 0x5eedull ^ ((uint64_t)epoch << 32) ^ ((uint64_t)p << 20));
+        if (wave_perm == 0) {
+            std::vector<int32_t> sigma, rho;
+            permutation(sigma, c, key);
+            permutation(rho, c, host_mix(key + 1));
+            seq.insert(seq.end(), sigma.begin(), sigma.end());
+            seq.insert(seq.end(), rho.begin(), rho.begin() + s);
+        } else {
+            std::vector<int32_t> pw;
+            for (int w = 0; w < s; w++) {
+                permutation(pw, c, host_mix(key + 2 + (uint64_t)w));
+                seq.insert(seq.end(), pw.begin(), pw.end());
+            }
         }
     }
     if (wf_seq) cudaFree(wf_seq);
     wf_seq = nullptr;
     CK(cudaMalloc((void **)&wf_seq, sizeof(int32_t) * seq.size()));
     CK(cudaMemcpyAsync(wf_seq, seq.data(), sizeof(int32_t) * seq.size(), cudaMemcpyHostToDevice, st));
-    const int64_t nb = (int64_t)s * c;
+    const int64_t nb = (int64_t)npass * s * c;
     if (trace) {
         if (wf_trace_n != nb) {
             if (wf_trace) cudaFree(wf_trace);
@@ -897,6 +935,7 @@ int mf_ctx::run_wavefront(const ShapeId &, const UpdateArgs &ua, int *launches, 
     a.scratch = scratch;
     a.s = s;
     a.c = c;
+    a.passes = npass;
     a.k = k;
     a.latin = wave_perm == 0;
     a.count_updates = count_updates;

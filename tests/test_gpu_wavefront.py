@@ -20,12 +20,13 @@ def mfmod():
     return mf
 
 
-def _audit(rec, s, c):
-    """rec rows: (worker, block, t_start, t_end). Returns number of column conflicts."""
-    assert len(rec) == s * c
+def _audit(rec, s, c, P=1):
+    """rec rows: (worker, block, t_start, t_end), block = (pass * s + worker) * c + column.  Returns the
+    number of column conflicts (two blocks of one column overlapping in time)."""
+    assert len(rec) == P * s * c
     blocks = rec[:, 1]
-    assert np.array_equal(np.sort(blocks), np.arange(s * c))  # each block exactly once
-    assert np.array_equal(rec[:, 0], blocks // c)             # block (w, col) done by worker w
+    assert np.array_equal(np.sort(blocks), np.arange(P * s * c))  # each block exactly once
+    assert np.array_equal(rec[:, 0], (blocks // c) % s)           # block (p, w, col) done by worker w
     conflicts = 0
     col = blocks % c
     for cc in range(c):
@@ -115,14 +116,15 @@ def test_wavefront_single_worker_is_serial_block_order(mfmod):
     assert np.linalg.norm(Q - ref.Q) / np.linalg.norm(ref.Q) <= 1e-5
 
 
-def _trace_order(mfmod, rec, perm, u, v, m, n, s, c, by_row=False):
+def _trace_order(mfmod, rec, perm, u, v, m, n, s, c, by_row=False, P=1):
     """Serial order of a wavefront epoch reconstructed from its audit trace: blocks by start time, each
     block's samples in stored (shuffled) order.  Blocks of one column never overlap in time and blocks
     of one band run on one worker in sequence, so sorting by start time orders every pair of blocks that
     share a row or a column as the GPU ran them; blocks that overlap in time share neither."""
     band = np.searchsorted([mfmod.mf_segment(m, s, w)[1] for w in range(s)], u[perm], side="right")
     grp = np.searchsorted([mfmod.mf_segment(n, c, g)[1] for g in range(c)], v[perm], side="right")
-    key = band.astype(np.int64) * c + grp
+    pas = (np.arange(len(perm)) * P) // len(perm)  # pass of each stored position
+    key = (pas * s + band.astype(np.int64)) * c + grp
     if by_row:  # q-stationary layout: inside a block the samples are sorted by Q row (stable)
         order_pos = np.lexsort((np.arange(len(perm)), v[perm], key))
         by_blk = {}
@@ -166,6 +168,53 @@ def test_wavefront_equals_serial_sweep_in_trace_order(mfmod, storage, s, c, dept
     tol = {0: 1e-5, 1: 2e-3}[storage]
     assert np.linalg.norm(P - Pr) / np.linalg.norm(Pr) <= tol
     assert np.linalg.norm(Q - Qr) / np.linalg.norm(Qr) <= tol
+
+
+@pytest.mark.parametrize("storage", [0, 1])
+@pytest.mark.parametrize("s,c,P", [(8, 10, 3), (0, 0, 4)])
+def test_wavefront_passes_equal_serial_sweep_in_trace_order(mfmod, storage, s, c, P):
+    """MF_OPT_WAVE_PASSES = P: the epoch is P passes over consecutive slices of the shuffled samples, each
+    with fresh column sequences; still exactly serial SGD over the blocks in trace order (warp workers)."""
+    cfg = datagen.CONFIGS["C1"]
+    (u, v, r), _ = datagen.make(cfg)
+    st = {0: oracle.F32, 1: oracle.F16}[storage]
+    ref = oracle.Model(cfg.m, cfg.n, cfg.k, st, seed=cfg.seed_init)
+    with mfmod.MF(cfg.m, cfg.n, cfg.k, cfg.alpha, cfg.lam, cfg.seed_init, storage=storage, beta=cfg.beta,
+                  wave_rows=s, wave_cols=c, wave_passes=P, trace=1, count_updates=1,
+                  seed_shuffle=cfg.seed_shuffle) as g:
+        g.load(u, v, r)
+        perm = g.order()
+        for e in range(2):
+            stt = g.epoch("wavefront")
+            assert stt.updates == len(u)
+            ss = stt.workers
+            cc = c or int(g.get(mfmod.MF_OPT_WAVE_COLS))
+            assert int(g.get(mfmod.MF_OPT_WAVE_PASSES)) == P
+            rec = mfmod.mf_wavefront_trace(g.h, P * ss * cc + 10)
+            assert _audit(rec, ss, cc, P) == 0
+            ref.epoch(u, v, r, oracle.eta(cfg.alpha, cfg.beta, e), cfg.lam,
+                      _trace_order(mfmod, rec, perm, u, v, cfg.m, cfg.n, ss, cc, P=P))
+        Pg, Qg = g.factors()
+    Pr, Qr = ref.factors_f32()
+    tol = {0: 1e-5, 1: 2e-3}[storage]
+    assert np.linalg.norm(Pg - Pr) / np.linalg.norm(Pr) <= tol
+    assert np.linalg.norm(Qg - Qr) / np.linalg.norm(Qr) <= tol
+
+
+def test_wavefront_cta_passes_exactly_once_and_conflict_free(mfmod):
+    """CTA workers (staged and q-stationary) with P = 4 passes: every sample once per epoch, no column
+    conflict across the 4 x s x c blocks."""
+    cfg = datagen.CONFIGS["C2-1pct"]
+    (u, v, r), _ = datagen.make(cfg)
+    for cta in (1, 3):
+        with mfmod.MF(cfg.m, cfg.n, cfg.k, cfg.alpha, cfg.lam, cfg.seed_init, storage=1, beta=cfg.beta,
+                      wave_cta=cta, wave_passes=4, trace=1, count_updates=1) as g:
+            g.load(u, v, r)
+            for _ in range(2):
+                stt = g.epoch("wavefront")
+                assert stt.updates == len(u)
+            ss, cc = stt.workers, int(g.get(mfmod.MF_OPT_WAVE_COLS))
+            assert _audit(mfmod.mf_wavefront_trace(g.h, 4 * ss * cc + 10), ss, cc, 4) == 0
 
 
 # ------------------------------------------------- q-stationary CTA workers --
