@@ -669,7 +669,8 @@ static int epoch_local(mf_ctx *ctx, int schedule, mf_epoch_stats *stats) {
         // bits 22..23: grid barrier of the 1024-thread forms, 0 = arrival counter polled to its target,
         // 1 = generation flag bumped by the last arriver (r01c)
         a.barrier = ((ctx->variant >> 22) & 0x3) == 1 ? 1 : 0;
-        CK(launch_waves(sh, a, st, &l, wsel == 2 ? 0 : wsel == 1 ? 1 : 2));
+        // bits 24..25 = 3: two 512-thread CTAs per SM with four samples per group and step
+        CK(launch_waves(sh, a, st, &l, wsel == 3 ? 3 : wsel == 2 ? 0 : wsel == 1 ? 1 : 2));
         used = 0;
     } else {  // wavefront
         int l = 0;

@@ -729,6 +729,18 @@ cudaError_t launch_waves(const ShapeId &sh, const UpdateArgs &a, cudaStream_t st
         int dev = 0, sms = 0, per_sm = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if constexpr (SH::FULL && (32 / SH::L) * 4 <= 32 && SH::L % 4 == 0) {
+            if (big == 3) {  // two 512-thread CTAs per SM (128 registers each), four samples per group and step
+                const void *kern = (const void *)k_waves<SH, 512, 4>;
+                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 512, 0);
+                if (per_sm >= 2) {
+                    UpdateArgs args = a;
+                    void *kargs[] = {&args};
+                    if (launches) *launches = 1;
+                    return cudaLaunchCooperativeKernel(kern, dim3(2 * sms), dim3(512), kargs, 0, st);
+                }
+            }
+        }
         if (big) {  // one 1024-thread CTA per SM: a quarter of the barrier arrivals; big = 2: two per group
             const void *kern = (const void *)k_waves<SH, 1024, 1>;
             if constexpr (SH::FULL) {

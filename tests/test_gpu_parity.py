@@ -122,14 +122,15 @@ def test_c1_deterministic_bit_reproducible_and_multi_epoch(mfmod, c1):
 @pytest.mark.parametrize("storage,cfgname", [(0, "C2-1pct"), (1, "C2-1pct"), (2, "C1"), (1, "C2-zipf-1pct")])
 def test_deterministic_executions_bitwise_equal(mfmod, storage, cfgname):
     """The deterministic schedule's executions (MF_OPT_VARIANT bits 24..25): 1024-thread CTAs with two
-    samples of a wave per group (default), with one, and 256-thread CTAs with the fenced barrier, and the
+    samples of a wave per group (default), with one, 256-thread CTAs with the fenced barrier, two
+    512-thread CTAs per SM with four samples per group, and the
     two grid barriers of the 1024-thread form (bits 22..23: arrival counter, generation flag) apply the
     same updates wave by wave with the same per-rating arithmetic, so their factors agree bit for bit
     (3 epochs)."""
     cfg = datagen.CONFIGS[cfgname]
     (u, v, r), _ = datagen.make(cfg)
     out = []
-    for var in (0, 1 << 24, 2 << 24, 1 << 22, (1 << 22) | (1 << 24)):
+    for var in (0, 1 << 24, 2 << 24, 3 << 24, 1 << 22, (1 << 22) | (1 << 24)):
         with _gpu(mfmod, cfg, storage, count_updates=1, variant=var) as g:
             g.load(u, v, r)
             for _ in range(3):

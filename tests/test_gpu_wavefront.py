@@ -20,6 +20,11 @@ def mfmod():
     return mf
 
 
+def _passes(mfmod, g):
+    """Passes per epoch of the current wavefront layout (auto: MF_OPT_WAVE_PASSES = 0)."""
+    return int(g.get(mfmod.MF_OPT_WAVE_PASSES))
+
+
 def _audit(rec, s, c, P=1):
     """rec rows: (worker, block, t_start, t_end), block = (pass * s + worker) * c + column.  Returns the
     number of column conflicts (two blocks of one column overlapping in time)."""
@@ -48,8 +53,9 @@ def test_wavefront_exactly_once_and_conflict_free(mfmod, perm):
             st = g.epoch("wavefront")
             assert st.updates == len(u)
             assert st.workers == s
-            rec = mfmod.mf_wavefront_trace(g.h, s * c + 10)
-            assert _audit(rec, s, c) == 0
+            P = _passes(mfmod, g)
+            rec = mfmod.mf_wavefront_trace(g.h, P * s * c + 10)
+            assert _audit(rec, s, c, P) == 0
 
 
 def test_wavefront_audit_at_scale(mfmod):
@@ -64,7 +70,7 @@ def test_wavefront_audit_at_scale(mfmod):
         s = st.workers
         c = int(g.get(mfmod.MF_OPT_WAVE_COLS)) or 2 * s
         rec = mfmod.mf_wavefront_trace(g.h, 10 ** 8)
-        assert _audit(rec, s, c) == 0
+        assert _audit(rec, s, c, _passes(mfmod, g)) == 0
 
 
 def _oracle_seed_spread(cfg, u, v, r, test, epochs, seeds=(42, 43, 44)):
@@ -159,10 +165,11 @@ def test_wavefront_equals_serial_sweep_in_trace_order(mfmod, storage, s, c, dept
             assert stt.updates == len(u)
             ss = stt.workers
             cc = c or int(g.get(mfmod.MF_OPT_WAVE_COLS)) or 2 * ss
-            rec = mfmod.mf_wavefront_trace(g.h, ss * cc + 10)
-            assert _audit(rec, ss, cc) == 0
+            P = _passes(mfmod, g)
+            rec = mfmod.mf_wavefront_trace(g.h, P * ss * cc + 10)
+            assert _audit(rec, ss, cc, P) == 0
             ref.epoch(u, v, r, oracle.eta(cfg.alpha, cfg.beta, e), cfg.lam,
-                      _trace_order(mfmod, rec, perm, u, v, cfg.m, cfg.n, ss, cc))
+                      _trace_order(mfmod, rec, perm, u, v, cfg.m, cfg.n, ss, cc, P=P))
         P, Q = g.factors()
     Pr, Qr = ref.factors_f32()
     tol = {0: 1e-5, 1: 2e-3}[storage]
@@ -240,10 +247,11 @@ def test_wavefront_q_one_warp_equals_serial_sweep_in_trace_order(mfmod, storage,
             assert stt.updates == len(u)
             ss = stt.workers
             cc = c or int(g.get(mfmod.MF_OPT_WAVE_COLS))
-            rec = mfmod.mf_wavefront_trace(g.h, ss * cc + 10)
-            assert _audit(rec, ss, cc) == 0
+            P = _passes(mfmod, g)
+            rec = mfmod.mf_wavefront_trace(g.h, P * ss * cc + 10)
+            assert _audit(rec, ss, cc, P) == 0
             ref.epoch(u, v, r, oracle.eta(cfg.alpha, cfg.beta, e), cfg.lam,
-                      _trace_order(mfmod, rec, perm, u, v, cfg.m, cfg.n, ss, cc, by_row=True))
+                      _trace_order(mfmod, rec, perm, u, v, cfg.m, cfg.n, ss, cc, by_row=True, P=P))
         P, Q = g.factors()
     Pr, Qr = ref.factors_f32()
     tol = {0: 1e-5, 1: 2e-3}[storage]
@@ -276,7 +284,8 @@ def test_wavefront_q_exactly_once_conflict_free_and_rmse(mfmod, storage, depth):
             assert stt.updates == len(u)
             if e == 0:
                 ss, cc = stt.workers, int(g.get(mfmod.MF_OPT_WAVE_COLS))
-                assert _audit(mfmod.mf_wavefront_trace(g.h, ss * cc + 10), ss, cc) == 0
+                P = _passes(mfmod, g)
+                assert _audit(mfmod.mf_wavefront_trace(g.h, P * ss * cc + 10), ss, cc, P) == 0
         got = g.rmse(*test)
     assert abs(got - gold[E - 1]) <= 0.005 * gold[E - 1], (got, gold[E - 1])
 
@@ -298,7 +307,8 @@ def test_wavefront_cta_exactly_once_conflict_free_and_rmse(mfmod):
             assert st.updates == len(u)
         s, c = int(g.get(mfmod.MF_OPT_WAVE_ROWS)), int(g.get(mfmod.MF_OPT_WAVE_COLS))
         assert s == st.workers and c >= s
-        assert _audit(mfmod.mf_wavefront_trace(g.h, s * c), s, c) == 0
+        P = _passes(mfmod, g)
+        assert _audit(mfmod.mf_wavefront_trace(g.h, P * s * c), s, c, P) == 0
         got = g.rmse(*test)
     assert abs(got - trace[-1]) <= 0.005 * trace[-1], (got, trace[-1])
 
