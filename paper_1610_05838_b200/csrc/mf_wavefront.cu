@@ -825,19 +825,27 @@ int mf_ctx::build_wavefront() {
     // Passes per epoch (MF_OPT_WAVE_PASSES): each pass walks every worker through all c column groups with
     // fresh sequences, over 1/P of the shuffled samples.  With one pass every row band meets the column
     // groups in one fixed cyclic order per epoch -- each user's ratings are processed sorted by column
-    // group -- and on the Hugewiki shape (61 ratings per user, 140k-sample blocks) the wavefront never
-    // catches up with serial SGD (test RMSE after 5 epochs: CTA workers 0.40-0.51, warp workers +13% after
-    // 4; batch-Hogwild! 0.1675).  P passes split each user's ratings into P slices visited in independent
-    // orders: P = 8 brings both forms to serial SGD's trajectory (-0.3..-0.6% from epoch 2) at 7% / 10%
-    // more time per epoch; on the Netflix shape P = 4 also removes the first-epoch lag (+1.5% instead of
-    // +265% after epoch 1) but costs the CTA form 70% (4x the blocks at 4.5k samples each, each paying
-    // its Q-group staging and lock hand-over; profiles/r02r_*).  Auto: as many passes as keep blocks at
-    // >= 16k samples (CTA workers) / >= 64 samples (warp workers): Hugewiki 8 / 6, Netflix and Yahoo 1.
+    // group -- and the wavefront trails serial SGD: on the Hugewiki shape it never catches up (test RMSE
+    // after 5 epochs: CTA workers 0.40-0.51, warp workers +13% after 4; serial 0.1675), on the Netflix
+    // shape it is +265% after epoch 1 and +11% after epoch 2.  P passes split each user's ratings into P
+    // slices visited in independent orders (profiles/r02r_*, r02v_*):
+    //  - CTA workers: P = round(sqrt(V / 10)), V = N / (n s) the updates a Q row takes per visit in one
+    //    pass -- an empirical rule fitted to the three shapes: Netflix V = 38 -> P = 2 (every epoch from the
+    //    2nd within 0.5% of serial SGD, +29% time; P = 4: +75%), Yahoo V = 2.7 -> 1 (within 0.5% from
+    //    epoch 2 already; P = 2 would cost 54%), Hugewiki V = 521 -> 7 (P = 8: serial SGD's trajectory at
+    //    +7% time; P = 32: +1..2% behind and +35% time);
+    //  - warp workers (blocks of ~14-450 samples): as many passes as keep blocks at >= 64 samples
+    //    (Hugewiki 6, Netflix and Yahoo 1; each block costs a lock hand-over).
     int npass_auto = 1;
     {
         const double per_block = (double)N / ((double)s * (double)c);
-        const double bmin = wave_cta ? 16384.0 : 64.0;
-        npass_auto = (int)std::max(1.0, std::min(64.0, std::floor(per_block / bmin)));
+        if (wave_cta) {
+            const double V = (double)N / ((double)n * (double)s);
+            npass_auto = (int)std::max(1.0, std::min(64.0, std::floor(std::sqrt(V / 10.0) + 0.5)));
+            while (npass_auto > 1 && per_block / npass_auto < 512.0) npass_auto--;  // keep blocks >= 512 samples
+        } else {
+            npass_auto = (int)std::max(1.0, std::min(64.0, std::floor(per_block / 64.0)));
+        }
     }
     const int npass = (int)std::max<int64_t>(1, std::min<int64_t>(wave_passes > 0 ? wave_passes : npass_auto,
                                                                   std::max<int64_t>(1, N)));

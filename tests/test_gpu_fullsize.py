@@ -74,20 +74,14 @@ def _gates(storage, gold):
     return gates
 
 
-@pytest.mark.parametrize("storage", [
-    pytest.param("f32", marks=pytest.mark.xfail(strict=False, reason=(
-        "the CTA wavefront's trajectory runs ahead of serial SGD in epochs 5-12: -0.54% at epochs 7-8 "
-        "(profiles/r02o_pytest_gpu.log; DESIGN.md 5.4)"))),
-    pytest.param("f16", marks=pytest.mark.xfail(strict=False, reason=(
-        "the CTA wavefront's trajectory runs ahead of serial SGD in epochs 5-12 (-0.52% at epoch 7) and "
-        "behind in the fp16 escape phase (+0.53..0.57% at epoch 20); oracle seed spread <= 0.14% "
-        "(profiles/r02j_c2_f16.jsonl, r02o_pytest_gpu.log; DESIGN.md 5.4)")))])
+@pytest.mark.parametrize("storage", ["f32", "f16"])
 def test_c2_wavefront_cta_rmse_trace_vs_oracle_golden(c2, storage):
     """The wavefront schedule with CTA workers (bench.py's throughput configuration) at full size, one run,
-    every epoch from the fourth gated against the oracle's trace (0.5%, or the oracle's own shuffle-seed
-    spread where larger: DESIGN.md T3).  Its first epochs trail serial SGD (blocked order, T6 and
-    5.4: +265% after epoch 1, +11% after epoch 2, +1.2% after epoch 3 in fp16); they are checked to be
-    finite and descending, and reported in DESIGN.md, not gated."""
+    every epoch from the third gated against the oracle's trace (0.5%, or the oracle's own shuffle-seed
+    spread where larger: DESIGN.md T3).  Its auto pass count on this shape is 2 (with one
+    pass the blocked order trails serial SGD by +265% / +11% after epochs 1 / 2 and wobbles +-0.57% later;
+    with two: +6% / +0.5% after epochs 1 / 2, then within 0.5% at every epoch to the 20th).  The first two
+    epochs are checked to be finite and descending, and reported in DESIGN.md, not gated (T6)."""
     path = os.path.join(GOLD, f"C2_{storage}_trace.json")
     if not os.path.exists(path):
         pytest.skip(f"{path} not generated yet")
@@ -102,7 +96,7 @@ def test_c2_wavefront_cta_rmse_trace_vs_oracle_golden(c2, storage):
             got.append(g.rmse(*test))
     assert all(np.isfinite(got)) and got[0] > got[1] > got[2]
     gate = _gates(storage, gold)
-    bad = [(t + 1, a, b, gt) for t, (a, b, gt) in enumerate(zip(got, gold, gate)) if t >= 3 and abs(a - b) > gt]
+    bad = [(t + 1, a, b, gt) for t, (a, b, gt) in enumerate(zip(got, gold, gate)) if t >= 2 and abs(a - b) > gt]
     assert not bad, bad
 
 
