@@ -14,8 +14,9 @@ overlapped with the update kernel; other schedules: mf_load_coo H2D + validation
 mf_epoch), then mf_rmse with the test set from host memory and the result D2H.
 N > 1 (torchrun): the partitioned path with NCCL Q rotation, one process per GPU, max-over-ranks time
 (defaults: --config C4 --scaling strong --storage f16).  N = 1 also runs, in `other_runs`, the other
-storage, the CTA wavefront and deterministic schedules on the same workload, and the Hugewiki shape on
-this one GPU (batch-Hogwild!, CTA wavefront and the 1-partition partitioned path; --no-c4 skips it).
+storage, the CTA wavefront and deterministic schedules on the same workload, the Yahoo!Music shape
+(batch-Hogwild!, both wavefront forms: configs[2]) and the Hugewiki shape on this one GPU (batch-Hogwild!,
+CTA wavefront and the 1-partition partitioned path: configs[3]; --no-c4 skips it).
 `--impl reference` times the CPU oracle (the only reference this paper-only task has) on a bounded
 sample of the same workload.
 """
@@ -455,6 +456,8 @@ def main():
                                                   "epochs_done",
                                                   "variant", "frac_of_pattern_ceiling")}
 
+    if not a.no_variants and a.config == "C2":
+        others.update(c3_leg(mf, stream, local, a.storage))
     if not a.no_variants and not a.no_c4 and a.config != "C4":
         others.update(c4_leg(mf, stream, local, a.storage))
 
@@ -518,22 +521,22 @@ def main():
     print(json.dumps(out), flush=True)
 
 
-def c4_leg(mf, stream, local, storage, epochs=5):
-    """BASELINE.json configs[3], the Hugewiki shape (N = 3,069,817,980, m = 50M, n = 39,781, k = 128) on
-    THIS one GPU: batch-Hogwild!, the CTA wavefront and the partitioned schedule with one partition (the
-    multi-GPU code path's kernels and per-round launches, loopback transport).  The R triples (36.8 GB) and
-    P (12.8 GB fp16) are resident; HBM binds here (P is 100x the L2).  Synthetic draws are i.i.d., so the
-    stored order is already random (A-8, MF_OPT_SHUFFLE = 0).  Epochs 0-2 of the auto-tuned schedules are
-    their prefetch trials; the kernel time reported is the mean of the later epochs."""
+def shape_leg(mf, stream, local, storage, name, schedules, epochs=5):
+    """Another BASELINE.json workload on THIS one GPU, as extra lines of `other_runs`: C3 (configs[2], the
+    Yahoo!Music shape, "wavefront-update vs batch-Hogwild!") and C4 (configs[3], the Hugewiki shape: N =
+    3,069,817,980, m = 50M, n = 39,781 -- R 36.8 GB and P 12.8 GB fp16 resident, HBM binds since P is 100x
+    the L2; the partitioned schedule with one partition runs the multi-GPU code path's kernels and
+    launches).  Synthetic draws are i.i.d., so the stored order is already random (A-8, MF_OPT_SHUFFLE =
+    0).  Epochs 0-2 of the auto-tuned schedules are their prefetch trials; the kernel time reported is the
+    mean of the later epochs; the test RMSE after `epochs` epochs is reported beside it."""
     import gc
-    cfg = datagen.CONFIGS["C4"]
+    cfg = datagen.CONFIGS[name]
     t0 = time.perf_counter()
     (u, v, r), (tu, tv, tr) = datagen.make(cfg)
     gen_s = time.perf_counter() - t0
     N = len(u)
     out = {}
-    for key, sched, opts in (("C4:hogwild", "hogwild", {}), ("C4:wavefront_cta", "wavefront", {"wave_cta": 1}),
-                             ("C4:partitioned_1", "partitioned", {"partitions": 1})):
+    for label, sched, opts in schedules:
         g = mf.MF(cfg.m, cfg.n, cfg.k, cfg.alpha, cfg.lam, cfg.seed_init, storage=storage, beta=cfg.beta,
                   seed_shuffle=cfg.seed_shuffle, device=local, stream=stream.cuda_stream, shuffle=0, **opts)
         g.load(u, v, r)
@@ -541,19 +544,32 @@ def c4_leg(mf, stream, local, storage, epochs=5):
         for _ in range(epochs):
             ks.append(g.epoch(sched).kernel_seconds)
         rm = g.rmse(tu, tv, tr)
+        passes = int(g.get(mf.MF_OPT_WAVE_PASSES)) if sched == "wavefront" else None
         g.close()
         k_s = statistics.mean(ks[3:]) if sched != "partitioned" else statistics.mean(ks[1:])
         sname = "wavefront_cta" if opts.get("wave_cta") else "hogwild"
-        rf = roofline(cfg, storage, N, k_s, load_traffic(storage, "C4", sname), sname)
-        out[key + "/" + storage] = {"value": N / k_s, "kernel_s": k_s, "rmse_after_%d_epochs" % epochs: rm,
-                                    "roofline_bound": rf["bound"], "roofline_frac": rf["frac"],
-                                    "hbm": rf["hbm"], "l2_frac": (rf["l2"] or {}).get("frac"), "N": N}
-    out["C4:note"] = ("kernel-timed (CUDA events inside libmf), inputs resident; host generation %.0f s; "
-                      "partitioned_1 = MF_SCHED_PARTITIONED with one loopback partition: %d passes x 1 round of "
-                      "two concurrent half-segment launches per epoch" % (gen_s, 4))
+        rf = roofline(cfg, storage, N, k_s, load_traffic(storage, name, sname), sname)
+        out[f"{name}:{label}/{storage}"] = {"value": N / k_s, "kernel_s": k_s, "rmse_after_%d_epochs" % epochs: rm,
+                                            "roofline_bound": rf["bound"], "roofline_frac": rf["frac"],
+                                            "hbm": rf["hbm"], "l2_frac": (rf["l2"] or {}).get("frac"), "N": N,
+                                            **({"wave_passes": passes} if passes else {})}
+    out[f"{name}:note"] = ("kernel-timed (CUDA events inside libmf), inputs resident; host generation %.0f s"
+                           % gen_s)
     del u, v, r
     gc.collect()
     return out
+
+
+def c4_leg(mf, stream, local, storage, epochs=5):
+    return shape_leg(mf, stream, local, storage, "C4",
+                     (("hogwild", "hogwild", {}), ("wavefront_cta", "wavefront", {"wave_cta": 1}),
+                      ("partitioned_1", "partitioned", {"partitions": 1})), epochs)
+
+
+def c3_leg(mf, stream, local, storage, epochs=5):
+    return shape_leg(mf, stream, local, storage, "C3",
+                     (("hogwild", "hogwild", {}), ("wavefront_cta", "wavefront", {"wave_cta": 1}),
+                      ("wavefront_warp", "wavefront", {})), epochs)
 
 
 def run_partitioned(a, cfg, rank, world, local):
