@@ -107,9 +107,13 @@ typedef enum {
     MF_OPT_R_STAGING = 20,    /* batch-Hogwild! rating batches: 1 = registers (three coalesced 32-bit loads per lane per 32-sample
                                  tile, handed to the groups by shuffles); 2 = staged in shared memory by the TMA engine (bulk
                                  copies of each chunk's u, v, r, double-buffered per warp; needs 16-B aligned arrays, else 1) */
-    MF_OPT_WAVE_PASSES = 21   /* wavefront: passes P per epoch, each over 1/P of the shuffled samples with fresh column
+    MF_OPT_WAVE_PASSES = 21,  /* wavefront: passes P per epoch, each over 1/P of the shuffled samples with fresh column
                                  sequences for every worker (0 = auto: blocks of >= 16k samples for CTA workers, >= 64
                                  for warp workers) */
+    MF_OPT_P_HOST = 22        /* 1 = out-of-core factors: P lives in caller host memory and streams through the GPU row block
+                                 by row block (mf_epoch_host_blocks, mf_rmse_host_blocks); no device P is allocated, and
+                                 mf_epoch / mf_epoch_host / mf_rmse and P in mf_get/set_factors fail with MF_ESTATE.  Set
+                                 before the factors exist. */
 } mf_option;
 
 typedef struct {
@@ -163,6 +167,26 @@ int mf_epoch(mf_ctx *ctx, int schedule, mf_epoch_stats *stats);
  * must exist or are created (A-7) on first use; no prior mf_load_coo is needed. */
 int mf_epoch_host(mf_ctx *ctx, int schedule, const int32_t *u, const int32_t *v, const float *r, int64_t nnz,
                   mf_epoch_stats *stats);
+
+/* Out-of-core factors (MF_OPT_P_HOST = 1): the paper's own path for a problem whose factors exceed device
+ * memory -- R divided into row blocks, each block's P segment and ratings copied in, updated, and the P
+ * segment copied back while the next block is in flight (§4.1; 307-320, §4.2; the
+ * Hugewiki run used 64 x 1 blocks).  Q (n x k) stays on the device.
+ * P_host: caller memory (pinned host memory for full overlap; pageable or device memory also work), m x k
+ * row-major in the context's STORAGE precision (fp32 / fp16 / bf16 bit patterns), owned by the caller.
+ * Row block b covers rows [floor(b m / nblocks), floor((b+1) m / nblocks)) and its ratings are
+ * u/v/r[block_off[b] .. block_off[b+1]) (block_off: nblocks + 1 host int64, 0 .. nnz, nondecreasing).
+ * mf_init_rows_host writes the A-7 initial values of rows [row0, row0 + rows) of P (tag 0) or Q (tag 1)
+ * in storage precision to `out` (host).  mf_epoch_host_blocks runs one batch-Hogwild! epoch (t += 1) over
+ * the blocks in order (with MF_OPT_WORKERS = 1: serial SGD over the given order); a sample outside its
+ * block's rows, an out-of-range column or a non-finite rating returns MF_EINVAL and skips the remaining
+ * chunks (earlier ones stay applied).  mf_rmse_host_blocks: test RMSE over test triples grouped the same
+ * way, fp64 sum in fixed order.  MF_ESTATE without MF_OPT_P_HOST; MF_EINVAL for bad pointers / offsets. */
+int mf_init_rows_host(mf_ctx *ctx, int32_t tag, int64_t row0, int64_t rows, void *out);
+int mf_epoch_host_blocks(mf_ctx *ctx, const int32_t *u, const int32_t *v, const float *r, int64_t nnz,
+                         const int64_t *block_off, int32_t nblocks, void *P_host, mf_epoch_stats *stats);
+int mf_rmse_host_blocks(mf_ctx *ctx, const int32_t *u, const int32_t *v, const float *r, int64_t nnz,
+                        const int64_t *block_off, int32_t nblocks, const void *P_host, double *out);
 
 /* Test RMSE sqrt(sum (r - p_u.q_v)^2 / nnz) over the given triples: fp32 dot, fp64 sum,
  * deterministic reduction order.  nnz >= 1.  In the partitioned NCCL mode the call is collective and

@@ -111,17 +111,18 @@ int mf_ctx::ensure_device() {
 cudaStream_t mf_ctx::stream() const { return user_stream ? user_stream : own_stream; }
 
 int mf_ctx::ensure_factors() {
-    if (P && Q) return MF_OK;
+    if ((P || p_host) && Q) return MF_OK;
     RC(ensure_device());
     mf_ctx *ctx = this;
     CK(cudaSetDevice(device));
     const size_t b = (size_t)storage_bytes();
     const int64_t prow = p_rows();
-    RC(dev_alloc(this, (char **)&P, b * (size_t)prow * k, "alloc P"));
+    if (!p_host) RC(dev_alloc(this, (char **)&P, b * (size_t)prow * k, "alloc P"));
     RC(dev_alloc(this, (char **)&Q, b * (size_t)n * k, "alloc Q"));
     // A-7 init; in the partitioned NCCL mode P holds rows [p_begin, p_end) of the global P:
-    // the hash index is the global row*k+col, so shift the row origin.
-    CK(launch_init_rows(storage, P, p_begin, prow, k, seed, 0, stream()));
+    // the hash index is the global row*k+col, so shift the row origin.  With MF_OPT_P_HOST the caller
+    // owns P (mf_init_rows_host gives the same values).
+    if (!p_host) CK(launch_init_rows(storage, P, p_begin, prow, k, seed, 0, stream()));
     CK(launch_init_rows(storage, Q, 0, n, k, seed, 1, stream()));
     CK(cudaStreamSynchronize(stream()));
     return MF_OK;
@@ -186,6 +187,7 @@ void mf_ctx::release() {
     release_wavefront();
     release_partition();
     release_stream();
+    release_outcore();
     if (scratch) cudaFree(scratch);
     scratch = nullptr;
     if (h_scratch) cudaFreeHost(h_scratch);
@@ -328,6 +330,11 @@ extern "C" int mf_set_option(mf_ctx *ctx, int key, double value) {
             ctx->wave_passes = (int)iv;
             ctx->wf_valid = false;
             return MF_OK;
+        case MF_OPT_P_HOST:
+            if (iv < 0 || iv > 1) return ctx->fail(MF_EINVAL, "P host must be 0 or 1");
+            if (ctx->Q || ctx->P) return ctx->fail(MF_ESTATE, "MF_OPT_P_HOST must be set before the factors exist");
+            ctx->p_host = (int)iv;
+            return MF_OK;
         case MF_OPT_R_STAGING:
             if (iv < 1 || iv > 2) return ctx->fail(MF_EINVAL, "R staging must be 1 (registers) or 2 (TMA)");
             ctx->r_stage = (int)iv;
@@ -369,6 +376,7 @@ extern "C" int mf_get_option(const mf_ctx *ctx, int key, double *value) {
         case MF_OPT_PART_SPLIT: *value = ctx->part_split; return MF_OK;
         case MF_OPT_R_STAGING: *value = ctx->r_stage; return MF_OK;
         case MF_OPT_WAVE_PASSES: *value = ctx->wf_valid ? ctx->wf_p : ctx->wave_passes; return MF_OK;
+        case MF_OPT_P_HOST: *value = ctx->p_host; return MF_OK;
         default: return MF_EINVAL;
     }
 }
@@ -602,6 +610,7 @@ int mf_ctx::finish_epoch(int schedule, float eta, int launches, int workers_used
 static int epoch_local(mf_ctx *ctx, int schedule, mf_epoch_stats *stats);
 
 extern "C" int mf_epoch(mf_ctx *ctx, int schedule, mf_epoch_stats *stats) {
+    if (ctx && ctx->p_host) return ctx->fail(MF_ESTATE, "P lives in caller memory (MF_OPT_P_HOST): use mf_epoch_host_blocks");
     if (!ctx) return MF_EINVAL;
     if (!ctx->is_distributed()) return epoch_local(ctx, schedule, stats);
     // collective: a precondition failure on any rank is agreed before the exchange rounds start, and
@@ -688,6 +697,7 @@ static int epoch_local(mf_ctx *ctx, int schedule, mf_epoch_stats *stats) {
 
 // -------------------------------------------------------------------- rmse --
 extern "C" int mf_rmse(mf_ctx *ctx, const int32_t *u, const int32_t *v, const float *r, int64_t nnz, double *out) {
+    if (ctx && ctx->p_host) return ctx->fail(MF_ESTATE, "P lives in caller memory (MF_OPT_P_HOST): use mf_rmse_host_blocks");
     if (!ctx || !out) return MF_EINVAL;
     const bool dist = ctx->is_distributed();
     if (!dist) {
@@ -784,6 +794,7 @@ int mf_ctx::copy_in(void *X, int64_t count, const float *src) {
 
 extern "C" int mf_get_factors(mf_ctx *ctx, float *P, float *Q) {
     if (!ctx) return MF_EINVAL;
+    if (ctx->p_host && P) return ctx->fail(MF_ESTATE, "P lives in caller memory (MF_OPT_P_HOST): pass P = NULL");
     RC(ctx->agree(ctx->ensure_factors()));  // collective with NCCL: the all-gather below
     CK(cudaSetDevice(ctx->device));
     RC(ctx->gather_q());
@@ -794,6 +805,7 @@ extern "C" int mf_get_factors(mf_ctx *ctx, float *P, float *Q) {
 
 extern "C" int mf_set_factors(mf_ctx *ctx, const float *P, const float *Q) {
     if (!ctx) return MF_EINVAL;
+    if (ctx->p_host && P) return ctx->fail(MF_ESTATE, "P lives in caller memory (MF_OPT_P_HOST): pass P = NULL");
     RC(ctx->ensure_factors());
     CK(cudaSetDevice(ctx->device));
     RC(ctx->gather_q());

@@ -148,6 +148,14 @@ struct mf_ctx {
     cudaEvent_t sb_copied[kStreamBufs] = {}, sb_used[kStreamBufs] = {};
     void release_stream();
 
+    // out-of-core factors (mf_outcore.cu): P in caller host memory, streamed by row block
+    int p_host = 0;                        // MF_OPT_P_HOST: 1 = no device P; epochs via mf_epoch_host_blocks
+    void *oc_slot[kStreamBufs] = {};       // device P-segment slots
+    int64_t oc_cap = 0;                    // bytes per slot
+    cudaEvent_t oc_in[kStreamBufs] = {}, oc_done[kStreamBufs] = {}, oc_out[kStreamBufs] = {};
+    cudaStream_t d2h_stream = nullptr;     // P-segment write-backs
+    void release_outcore();
+
     // scratch for rmse / factors
     int32_t *tu = nullptr, *tv = nullptr;
     float *tr = nullptr;

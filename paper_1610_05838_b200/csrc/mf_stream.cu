@@ -44,6 +44,7 @@ extern "C" int mf_epoch_host(mf_ctx *ctx, int schedule, const int32_t *u, const 
     if (schedule != MF_SCHED_HOGWILD) return ctx->fail(MF_EINVAL, "mf_epoch_host supports MF_SCHED_HOGWILD only");
     if (!u || !v || !r || nnz <= 0) return ctx->fail(MF_EINVAL, "mf_epoch_host: null pointer or nnz <= 0");
     if (ctx->is_distributed()) return ctx->fail(MF_EINVAL, "mf_epoch_host: not available with NCCL attached");
+    if (ctx->p_host) return ctx->fail(MF_ESTATE, "P lives in caller memory (MF_OPT_P_HOST): use mf_epoch_host_blocks");
     int rc = ctx->ensure_factors();
     if (rc != MF_OK) return rc;
     CK(cudaSetDevice(ctx->device));

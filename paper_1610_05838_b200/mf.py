@@ -26,7 +26,7 @@ SCHEDULES = {"hogwild": 0, "wavefront": 1, "deterministic": 2, "partitioned": 3}
 (MF_OPT_STORAGE, MF_OPT_BETA, MF_OPT_WORKERS, MF_OPT_BATCH_F, MF_OPT_WAVE_ROWS, MF_OPT_WAVE_COLS, MF_OPT_DEVICE,
  MF_OPT_STREAM, MF_OPT_SHUFFLE, MF_OPT_COUNT_UPDATES, MF_OPT_WAVE_PERM, MF_OPT_EPOCH, MF_OPT_PARTITIONS,
  MF_OPT_SEED_SHUFFLE, MF_OPT_VARIANT, MF_OPT_TRACE, MF_OPT_SUBEPOCHS, MF_OPT_WAVE_CTA,
- MF_OPT_STREAM_CHUNK, MF_OPT_PART_SPLIT, MF_OPT_R_STAGING, MF_OPT_WAVE_PASSES) = range(22)
+ MF_OPT_STREAM_CHUNK, MF_OPT_PART_SPLIT, MF_OPT_R_STAGING, MF_OPT_WAVE_PASSES, MF_OPT_P_HOST) = range(23)
 STORAGE = {"f32": 0, "fp32": 0, "f16": 1, "fp16": 1, "bf16": 2}
 
 
@@ -59,6 +59,9 @@ _sig = {
     "mf_unit_peers": ([c.c_uint64, c.c_int32, c.c_int32, c.c_int32, c.c_int32, c.c_int32, c.POINTER(c.c_int32),
                        c.POINTER(c.c_int32)], c.c_int),
     "mf_wavefront_trace": ([_P, _P, c.c_int64, c.POINTER(c.c_int64)], c.c_int),
+    "mf_init_rows_host": ([_P, c.c_int32, c.c_int64, c.c_int64, _P], c.c_int),
+    "mf_epoch_host_blocks": ([_P, _P, _P, _P, c.c_int64, _P, c.c_int32, _P, c.POINTER(mf_epoch_stats)], c.c_int),
+    "mf_rmse_host_blocks": ([_P, _P, _P, _P, c.c_int64, _P, c.c_int32, _P, c.POINTER(c.c_double)], c.c_int),
     "mf_feasibility": ([c.c_int64, c.c_int64, c.c_int32, c.c_int32, c.c_int64, c.c_int32, c.POINTER(c.c_int64)],
                        c.c_int),
     "mf_destroy": ([_P], None),
@@ -147,6 +150,41 @@ def mf_rmse(ctx, u, v, r):
     n = len(au) if not hasattr(au, "numel") else au.numel()
     out = c.c_double()
     _check(ctx, _lib.mf_rmse(ctx, pu, pv, pr, n, c.byref(out)))
+    return out.value
+
+
+def mf_init_rows_host(ctx, tag, row0, rows, out):
+    """A-7 initial values of rows [row0, row0 + rows) of P (tag 0) or Q (tag 1), in storage precision, into
+    `out` (numpy array of the storage dtype: float32, or uint16 bit patterns for fp16 / bf16)."""
+    _check(ctx, _lib.mf_init_rows_host(ctx, tag, row0, rows, out.ctypes.data))
+
+
+def _blocks(block_off):
+    bo = np.ascontiguousarray(block_off, dtype=np.int64)
+    return bo, len(bo) - 1
+
+
+def mf_epoch_host_blocks(ctx, u, v, r, block_off, P_host):
+    pu, au = _ptr(u, np.int32)
+    pv, av = _ptr(v, np.int32)
+    pr, ar = _ptr(r, np.float32)
+    n = len(au) if not hasattr(au, "numel") else au.numel()
+    bo, nb = _blocks(block_off)
+    pp, ap = _ptr(P_host)
+    st = mf_epoch_stats()
+    _check(ctx, _lib.mf_epoch_host_blocks(ctx, pu, pv, pr, n, bo.ctypes.data, nb, pp, c.byref(st)))
+    return st
+
+
+def mf_rmse_host_blocks(ctx, u, v, r, block_off, P_host):
+    pu, au = _ptr(u, np.int32)
+    pv, av = _ptr(v, np.int32)
+    pr, ar = _ptr(r, np.float32)
+    n = len(au) if not hasattr(au, "numel") else au.numel()
+    bo, nb = _blocks(block_off)
+    pp, ap = _ptr(P_host)
+    out = c.c_double()
+    _check(ctx, _lib.mf_rmse_host_blocks(ctx, pu, pv, pr, n, bo.ctypes.data, nb, pp, c.byref(out)))
     return out.value
 
 
