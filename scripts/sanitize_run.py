@@ -43,6 +43,17 @@ def main():
             g = mf.MF(cfg.m, cfg.n, k, cfg.alpha, cfg.lam, cfg.seed_init, storage=storage, stream_chunk=7000)
             g.epoch_host(u, v, r)
             g.close()
+            # out-of-core factors: P in host memory, 5 row blocks
+            ends = np.array([mf.mf_segment(cfg.m, 5, b)[1] for b in range(5)])
+            blk = np.searchsorted(ends, u, side="right")
+            o = np.argsort(blk, kind="stable")
+            off = np.concatenate([[0], np.cumsum(np.bincount(blk, minlength=5))]).astype(np.int64)
+            g = mf.MF(cfg.m, cfg.n, k, cfg.alpha, cfg.lam, cfg.seed_init, storage=storage, stream_chunk=7000, p_host=1)
+            Ph = np.zeros((cfg.m, k), np.float32 if storage == "f32" else np.uint16)
+            mf.mf_init_rows_host(g.h, 0, 0, cfg.m, Ph)
+            mf.mf_epoch_host_blocks(g.h, u[o], v[o], r[o], off, Ph)
+            mf.mf_rmse_host_blocks(g.h, u[o], v[o], r[o], off, Ph)
+            g.close()
     print("sanitize run ok")
 
 
