@@ -37,9 +37,9 @@ def main():
     for storage in a.storage.split(","):
         b = 4 if storage == "f32" else 2
         B = 12 + 4 * cfg.k * b
-        extra = {kv.split("=")[0]: float(kv.split("=")[1]) for kv in a.opt}
-        g = mf.MF(cfg.m, cfg.n, cfg.k, cfg.alpha, cfg.lam, cfg.seed_init, storage=storage, beta=cfg.beta, shuffle=0,
-                  **extra)
+        extra = {"shuffle": 0}
+        extra.update({kv.split("=")[0]: float(kv.split("=")[1]) for kv in a.opt})
+        g = mf.MF(cfg.m, cfg.n, cfg.k, cfg.alpha, cfg.lam, cfg.seed_init, storage=storage, beta=cfg.beta, **extra)
         g.load(u, v, r)
         for var in [int(x) for x in a.variants.split(",")]:
             for w in [int(x) for x in a.workers.split(",")]:
