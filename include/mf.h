@@ -110,10 +110,15 @@ typedef enum {
     MF_OPT_WAVE_PASSES = 21,  /* wavefront: passes P per epoch, each over 1/P of the shuffled samples with fresh column
                                  sequences for every worker (0 = auto: blocks of >= 16k samples for CTA workers, >= 64
                                  for warp workers) */
-    MF_OPT_P_HOST = 22        /* 1 = out-of-core factors: P lives in caller host memory and streams through the GPU row block
+    MF_OPT_P_HOST = 22,       /* 1 = out-of-core factors: P lives in caller host memory and streams through the GPU row block
                                  by row block (mf_epoch_host_blocks, mf_rmse_host_blocks); no device P is allocated, and
                                  mf_epoch / mf_epoch_host / mf_rmse and P in mf_get/set_factors fail with MF_ESTATE.  Set
                                  before the factors exist. */
+    MF_OPT_Q_UPDATE = 23      /* batch-Hogwild! (also inside partitioned blocks and streamed epochs) Q write-back: 1 = atomic add
+                                 of the row's change q' - q (red.global.add; concurrent updates of one Q row all land,
+                                 Hogwild!'s atomic component-wise add; A-20) (default); 0 = store q' (the
+                                 paper's worker writes the row back: of two concurrent updates the last store wins).
+                                 The deterministic and wavefront schedules always store. */
 } mf_option;
 
 typedef struct {

@@ -335,6 +335,10 @@ extern "C" int mf_set_option(mf_ctx *ctx, int key, double value) {
             if (ctx->Q || ctx->P) return ctx->fail(MF_ESTATE, "MF_OPT_P_HOST must be set before the factors exist");
             ctx->p_host = (int)iv;
             return MF_OK;
+        case MF_OPT_Q_UPDATE:
+            if (iv < 0 || iv > 1) return ctx->fail(MF_EINVAL, "Q update must be 0 (store) or 1 (atomic add)");
+            ctx->q_update = (int)iv;
+            return MF_OK;
         case MF_OPT_R_STAGING:
             if (iv < 1 || iv > 2) return ctx->fail(MF_EINVAL, "R staging must be 1 (registers) or 2 (TMA)");
             ctx->r_stage = (int)iv;
@@ -377,6 +381,7 @@ extern "C" int mf_get_option(const mf_ctx *ctx, int key, double *value) {
         case MF_OPT_R_STAGING: *value = ctx->r_stage; return MF_OK;
         case MF_OPT_WAVE_PASSES: *value = ctx->wf_valid ? ctx->wf_p : ctx->wave_passes; return MF_OK;
         case MF_OPT_P_HOST: *value = ctx->p_host; return MF_OK;
+        case MF_OPT_Q_UPDATE: *value = ctx->q_update; return MF_OK;
         default: return MF_EINVAL;
     }
 }
@@ -578,6 +583,7 @@ UpdateArgs mf_ctx::update_args(float eta) const {
     a.count_updates = count_updates;
     a.scratch = scratch;
     a.r_stage = r_stage;
+    a.q_red = q_update == 1;
     return a;
 }
 

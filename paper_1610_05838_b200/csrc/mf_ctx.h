@@ -38,6 +38,7 @@ struct mf_ctx {
                         // families with their own Latin squares, each hand-over overlapping the other's compute)
     int wave_cta = 0;   // wavefront worker = CTA with shared-memory Q group (MF_OPT_WAVE_CTA)
     int variant = 0;
+    int q_update = 1;   // MF_OPT_Q_UPDATE: batch-Hogwild! Q write-back 1 = atomic add of the change (A-20), 0 = store
     int r_stage = 1;    // MF_OPT_R_STAGING: batch-Hogwild! triples 1 = registers, 2 = TMA bulk copies into shared memory
     int trace = 0;
     // L2 prefetch, auto mode (MF_OPT_VARIANT bits 16..19 = 0).  Whether a prefetch pays depends on

@@ -278,9 +278,13 @@ __global__ void __launch_bounds__(kBlock) k_hogwild(UpdateArgs a) {
                     if (val[d] && !isfinite(err)) bad = 1;
                     sgd_step<SH>(pf[d], qf[d], err, a.eta, a.lam);
                     narrow_row<SH>(pf[d], pr[d]);
-                    narrow_row<SH>(qf[d], qr[d]);
                     store_row_pol<SH>(a.P, su[d], k, sub, val[d], pr[d], pol_p);
-                    store_row_pol<SH>(a.Q, sv[d], k, sub, val[d], qr[d], pol_q);
+                    if (a.q_red) {  // q_v += (q' - q): concurrent updates of one Q row all land (A-20)
+                        red_row_delta<SH>(a.Q, sv[d], k, sub, val[d], qr[d], qf[d], pol_q);
+                    } else {
+                        narrow_row<SH>(qf[d], qr[d]);
+                        store_row_pol<SH>(a.Q, sv[d], k, sub, val[d], qr[d], pol_q);
+                    }
                 }
             }
         }
@@ -462,9 +466,13 @@ __global__ void __launch_bounds__(kBlock) k_hogwild_tma(UpdateArgs a) {
                     if (val[d] && !isfinite(err)) bad = 1;
                     sgd_step<SH>(pf[d], qf[d], err, a.eta, a.lam);
                     narrow_row<SH>(pf[d], pr[d]);
-                    narrow_row<SH>(qf[d], qr[d]);
                     store_row_pol<SH>(a.P, su[d], k, sub, val[d], pr[d], pol_p);
-                    store_row_pol<SH>(a.Q, sv[d], k, sub, val[d], qr[d], pol_q);
+                    if (a.q_red) {  // q_v += (q' - q): concurrent updates of one Q row all land (A-20)
+                        red_row_delta<SH>(a.Q, sv[d], k, sub, val[d], qr[d], qf[d], pol_q);
+                    } else {
+                        narrow_row<SH>(qf[d], qr[d]);
+                        store_row_pol<SH>(a.Q, sv[d], k, sub, val[d], qr[d], pol_q);
+                    }
                 }
             }
         }

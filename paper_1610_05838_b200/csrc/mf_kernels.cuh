@@ -47,6 +47,8 @@ struct UpdateArgs {
                         // evict_last
     int r_stage;        // batch-Hogwild! triples: 2 = TMA bulk copies of each chunk into shared memory, else
                         // registers (3 coalesced 32-bit loads per lane per 32-sample tile, shuffled to groups)
+    int q_red;          // batch-Hogwild!: Q rows written back as an atomic add of their change (red.global.add,
+                        // DESIGN.md A-20) instead of a store of the new row (MF_OPT_Q_UPDATE)
     int barrier;        // deterministic waves, 1024-thread CTAs: 0 = arrival counter polled to (w+1) x CTAs
                         // (one release reduction + acquire polls), 1 = last arriver bumps a generation flag
 };

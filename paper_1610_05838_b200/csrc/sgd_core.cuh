@@ -292,6 +292,98 @@ __device__ __forceinline__ void store_row(void *base, int64_t row, int k, int su
     }
 }
 
+// ------------------------------------------------------ atomic write-back --
+// One vector of a row increased in place by an L2 atomic add (red.global.add, no return value): the
+// vector forms of sm_90+ (.v4/.v2 .f32, .v4/.v2 .f16x2 / .bf16x2), one 16-, 8- or 4-byte request per
+// lane like the plain store.  fp32 adds flush subnormal results to zero (REDG ...FTZ.RN); 16-bit adds
+// round to nearest even (.noftz).
+template <int S, int VB>
+struct RedVec;
+template <>
+struct RedVec<kF32, 16> {
+    static __device__ __forceinline__ void red(void *p, const uint32_t (&w)[4], uint64_t pol) {
+        asm volatile("red.global.add.L2::cache_hint.v4.f32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(p), "f"(__uint_as_float(w[0])),
+                     "f"(__uint_as_float(w[1])), "f"(__uint_as_float(w[2])), "f"(__uint_as_float(w[3])), "l"(pol)
+                     : "memory");
+    }
+};
+template <>
+struct RedVec<kF32, 8> {
+    static __device__ __forceinline__ void red(void *p, const uint32_t (&w)[2], uint64_t pol) {
+        asm volatile("red.global.add.L2::cache_hint.v2.f32 [%0], {%1, %2}, %3;" ::"l"(p), "f"(__uint_as_float(w[0])),
+                     "f"(__uint_as_float(w[1])), "l"(pol)
+                     : "memory");
+    }
+};
+template <>
+struct RedVec<kF32, 4> {
+    static __device__ __forceinline__ void red(void *p, const uint32_t (&w)[1], uint64_t pol) {
+        asm volatile("red.global.add.L2::cache_hint.f32 [%0], %1, %2;" ::"l"(p), "f"(__uint_as_float(w[0])), "l"(pol)
+                     : "memory");
+    }
+};
+#define MF_RED16(S_, T_)                                                                                          \
+    template <>                                                                                                   \
+    struct RedVec<S_, 16> {                                                                                       \
+        static __device__ __forceinline__ void red(void *p, const uint32_t (&w)[4], uint64_t pol) {               \
+            asm volatile("red.global.add.noftz.L2::cache_hint.v4." T_ "x2 [%0], {%1, %2, %3, %4}, %5;" ::"l"(p),  \
+                         "r"(w[0]), "r"(w[1]), "r"(w[2]), "r"(w[3]), "l"(pol)                                     \
+                         : "memory");                                                                             \
+        }                                                                                                         \
+    };                                                                                                            \
+    template <>                                                                                                   \
+    struct RedVec<S_, 8> {                                                                                        \
+        static __device__ __forceinline__ void red(void *p, const uint32_t (&w)[2], uint64_t pol) {               \
+            asm volatile("red.global.add.noftz.L2::cache_hint.v2." T_ "x2 [%0], {%1, %2}, %3;" ::"l"(p), "r"(w[0]), \
+                         "r"(w[1]), "l"(pol)                                                                      \
+                         : "memory");                                                                             \
+        }                                                                                                         \
+    };                                                                                                            \
+    template <>                                                                                                   \
+    struct RedVec<S_, 4> {                                                                                        \
+        static __device__ __forceinline__ void red(void *p, const uint32_t (&w)[1], uint64_t pol) {               \
+            asm volatile("red.global.add.noftz.L2::cache_hint." T_ "x2 [%0], %1, %2;" ::"l"(p), "r"(w[0]), "l"(pol) \
+                         : "memory");                                                                             \
+        }                                                                                                         \
+    };                                                                                                            \
+    template <>                                                                                                   \
+    struct RedVec<S_, 2> {                                                                                        \
+        static __device__ __forceinline__ void red(void *p, const uint32_t (&w)[1], uint64_t pol) {               \
+            const unsigned short h = (unsigned short)(w[0] & 0xFFFFu);                                            \
+            asm volatile("red.global.add.noftz.L2::cache_hint." T_ " [%0], %1, %2;" ::"l"(p), "h"(h), "l"(pol)    \
+                         : "memory");                                                                             \
+        }                                                                                                         \
+    };
+MF_RED16(kF16, "f16")
+MF_RED16(kBF16, "bf16")
+#undef MF_RED16
+
+template <class SH>
+__device__ __forceinline__ void widen_row(const RowRaw<SH> &in, float (&x)[SH::E]);
+template <class SH>
+__device__ __forceinline__ void narrow_row(const float (&x)[SH::E], RowRaw<SH> &out);
+
+// Write-back of an updated row as the atomic add of its change: the row in memory becomes
+// row + (new - old), old being the snapshot this update read (A-20).  With no concurrent
+// writer that is the new row (to the rounding of the change into storage precision); with one, both
+// changes land, where a plain store keeps only the last writer's row.
+template <class SH>
+__device__ __forceinline__ void red_row_delta(void *base, int64_t row, int k, int sub, bool valid,
+                                              const RowRaw<SH> &old, const float (&nw)[SH::E], uint64_t pol) {
+    float dl[SH::E];
+    widen_row<SH>(old, dl);
+#pragma unroll
+    for (int e = 0; e < SH::E; e++) dl[e] = nw[e] - dl[e];
+    RowRaw<SH> w;
+    narrow_row<SH>(dl, w);
+    char *rp = reinterpret_cast<char *>(base) + row * (int64_t)k * SH::BYTES;
+#pragma unroll
+    for (int j = 0; j < SH::V; j++) {
+        const int64_t e = vec_elem<SH>(j, sub);
+        if (valid && (SH::FULL || e < k)) RedVec<SH::S, SH::VB>::red(rp + e * SH::BYTES, w.w[j], pol);
+    }
+}
+
 template <class SH>
 __device__ __forceinline__ void widen_row(const RowRaw<SH> &in, float (&x)[SH::E]) {
 #pragma unroll

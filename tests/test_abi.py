@@ -35,6 +35,11 @@ def test_create_validates_arguments_without_device():
     try:
         mf.mf_set_option(h, mf.MF_OPT_BETA, 0.3)
         assert mf.mf_get_option(h, mf.MF_OPT_BETA) == 0.3
+        assert mf.mf_get_option(h, mf.MF_OPT_Q_UPDATE) == 1  # default: atomic add of the change (A-20)
+        mf.mf_set_option(h, mf.MF_OPT_Q_UPDATE, 0)
+        assert mf.mf_get_option(h, mf.MF_OPT_Q_UPDATE) == 0
+        with pytest.raises(mf.MFError):
+            mf.mf_set_option(h, mf.MF_OPT_Q_UPDATE, 2)
         with pytest.raises(mf.MFError):
             mf.mf_set_option(h, mf.MF_OPT_STORAGE, 7)
         with pytest.raises(mf.MFError):

@@ -268,6 +268,20 @@ def test_netflix_slice_hogwild_many_workers(mfmod):
     assert abs(got - gold[E - 1]) <= 0.005 * gold[E - 1], (got, gold[E - 1])
 
 
+@pytest.mark.parametrize("storage", [0, 1])
+def test_q_store_form_still_tracks_the_oracle(mfmod, storage):
+    """MF_OPT_Q_UPDATE = 0: the Q row written back by a plain store (the paper's worker; of two concurrent
+    updates of one Q row the last store wins) instead of the default atomic add of the change (DESIGN.md
+    A-20).  On the Netflix slice one run is within 0.5% of the serial oracle at the storage's gate epoch,
+    every sample once per epoch."""
+    cfg, (train, test) = _c2_10pct_data()
+    gold = _c2_10pct_gold(storage)
+    E = GATE_EPOCH[storage]
+    got = _hogwild_run(mfmod, cfg, storage, train, test, E, q_update=0,
+                       check=lambda g: int(g.get(mfmod.MF_OPT_Q_UPDATE)) == 0)
+    assert abs(got - gold[E - 1]) <= 0.005 * gold[E - 1], (got, gold[E - 1])
+
+
 @pytest.mark.parametrize("storage,pf", [(0, 15), (0, 1), (1, 15), (1, 1), (1, 2), (2, 15), (2, 1)])
 def test_netflix_slice_hogwild_l2_prefetch(mfmod, storage, pf):
     """The L2 row prefetch of batch-Hogwild! (MF_OPT_VARIANT bits 16..19; 15 = off) only moves cache lines:
@@ -397,7 +411,7 @@ def test_degenerate_shapes_every_schedule_is_serial(mfmod, storage, m_, n_, N, k
         ref.epoch(u, v, r, oracle.eta(0.05, 0.3, t), 0.02)
     Pr, Qr = ref.factors_f32()
     tol = TOL[storage]
-    runs = [("hogwild", {"workers": 1}), ("deterministic", {}), ("wavefront", {"wave_rows": 1, "wave_cols": 1}),
+    runs = [("hogwild", {"workers": 1}), ("hogwild", {"workers": 1, "q_update": 0}), ("deterministic", {}), ("wavefront", {"wave_rows": 1, "wave_cols": 1}),
             ("host", {"workers": 1})]
     if k == 7 and N <= 32:  # a masked 32-lane CTA shape, one rating at a time, one 32-sample tile
         runs.append(("wavefront", {"wave_cta": 1, "wave_rows": 1, "wave_cols": 1}))
