@@ -86,7 +86,8 @@ typedef enum {
                                  in steps (0 = auto: MF_SCHED_HOGWILD epochs 0, 1, 2 run off, 1 step, off and the
                                  prefetch is kept iff its epoch was > 3% faster; 15 = off); for CTA wavefront workers
                                  1 = bulk, 2 = per-line P-row prefetch per tile (0 = auto: kept unless > 3% slower).  20..21: CTA Q-group staging, 2 = thread
-                                 loop instead of bulk async copies.  24..25: deterministic execution, 0 = 1024-thread
+                                 loop instead of bulk async copies.  22..23: CTA wavefront q_v read from shared memory, 1 = when p_u's
+                                 load is issued, else (default) once p_u has arrived.  24..25: deterministic execution, 0 = 1024-thread
                                  CTAs with 2 samples of a wave per group, 1 = 1 sample, 2 = 256-thread CTAs (identical
                                  results).  26..27: CTA in-block clamp, samples per concurrent group 0 -> 16, 1 -> 32,
                                  2 -> 64, 3 -> 8.  Only bits 26..27 change what is computed (how many of a block's
@@ -114,11 +115,22 @@ typedef enum {
                                  by row block (mf_epoch_host_blocks, mf_rmse_host_blocks); no device P is allocated, and
                                  mf_epoch / mf_epoch_host / mf_rmse and P in mf_get/set_factors fail with MF_ESTATE.  Set
                                  before the factors exist. */
-    MF_OPT_Q_UPDATE = 23      /* batch-Hogwild! (also inside partitioned blocks and streamed epochs) Q write-back: 1 = atomic add
+    MF_OPT_Q_UPDATE = 23,     /* batch-Hogwild! (also inside partitioned blocks and streamed epochs) Q write-back: 1 = atomic add
                                  of the row's change q' - q (red.global.add; concurrent updates of one Q row all land,
-                                 Hogwild!'s atomic component-wise add; A-20) (default); 0 = store q' (the
-                                 paper's worker writes the row back: of two concurrent updates the last store wins).
+                                 Hogwild!'s atomic component-wise add); 0 = store q' (the paper's worker writes the row
+                                 back: of two concurrent updates the last store wins); 2 = auto (default): atomic add iff
+                                 kappa = workers x sum_v (deg v / N)^2 over the launch's Q rows -- the expected number of
+                                 concurrent updates an update shares its Q row with -- is below 0.5 (A-20).
                                  The deterministic and wavefront schedules always store. */
+    MF_OPT_DET_FLOW = 24,     /* MF_SCHED_DETERMINISTIC execution: 0 = the waves one after another with a grid barrier between
+                                 them (default); 1 = no barriers -- the wave-sorted samples stream through persistent warps
+                                 (warp w of W owns positions w, w + W, ...; MF_OPT_VARIANT bits 24..25 = 2: 32-sample tiles
+                                 claimed in order) and each rating waits, only when it has to, until per-row update
+                                 counters reach its ordinals in the serial order (slower on every measured shape; DESIGN.md
+                                 5.3).  Both are serial SGD (D-3) and bit-reproducible;
+                                 their dot products use different lane shapes, so they agree to rounding, not bit for bit. */
+    MF_OPT_Q_KAPPA = 25       /* read-only (mf_get_option): kappa of the last batch-Hogwild! or partitioned epoch, the largest
+                                 over its launches (-1 before one) */
 } mf_option;
 
 typedef struct {

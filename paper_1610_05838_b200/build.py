@@ -8,7 +8,8 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 SO = os.path.join(HERE, "libmf.so")
-SOURCES = ["mf_api.cu", "mf_kernels.cu", "mf_wavefront.cu", "mf_partition.cu", "mf_stream.cu", "mf_outcore.cu"]
+SOURCES = ["mf_api.cu", "mf_kernels.cu", "mf_wavefront.cu", "mf_partition.cu", "mf_stream.cu", "mf_outcore.cu",
+           "mf_flow.cu"]
 HEADERS = ["mf_ctx.h", "mf_kernels.cuh", "sgd_core.cuh", "mf_host_util.h"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

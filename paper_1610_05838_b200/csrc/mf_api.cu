@@ -139,6 +139,9 @@ void mf_ctx::drop_layouts() {
     dev_free(&wv);
     dev_free(&wr);
     dev_free(&wave_off);
+    dev_free(&ord_u);
+    dev_free(&ord_v);
+    dev_free(&cnt_uv);
     nwaves = -1;
     wf_valid = false;
     part_valid = false;
@@ -153,6 +156,9 @@ int mf_ctx::drop_other_layouts(int schedule) {
         dev_free(&wv);
         dev_free(&wr);
         dev_free(&wave_off);
+        dev_free(&ord_u);
+        dev_free(&ord_v);
+        dev_free(&cnt_uv);
         nwaves = -1;
     }
     if (schedule != MF_SCHED_WAVEFRONT && fu) release_wavefront();
@@ -335,8 +341,12 @@ extern "C" int mf_set_option(mf_ctx *ctx, int key, double value) {
             if (ctx->Q || ctx->P) return ctx->fail(MF_ESTATE, "MF_OPT_P_HOST must be set before the factors exist");
             ctx->p_host = (int)iv;
             return MF_OK;
+        case MF_OPT_DET_FLOW:
+            if (iv < 0 || iv > 1) return ctx->fail(MF_EINVAL, "det flow must be 0 (waves) or 1 (row counters)");
+            ctx->det_flow = (int)iv;
+            return MF_OK;
         case MF_OPT_Q_UPDATE:
-            if (iv < 0 || iv > 1) return ctx->fail(MF_EINVAL, "Q update must be 0 (store) or 1 (atomic add)");
+            if (iv < 0 || iv > 2) return ctx->fail(MF_EINVAL, "Q update must be 0 (store), 1 (atomic add) or 2 (auto)");
             ctx->q_update = (int)iv;
             return MF_OK;
         case MF_OPT_R_STAGING:
@@ -382,6 +392,8 @@ extern "C" int mf_get_option(const mf_ctx *ctx, int key, double *value) {
         case MF_OPT_WAVE_PASSES: *value = ctx->wf_valid ? ctx->wf_p : ctx->wave_passes; return MF_OK;
         case MF_OPT_P_HOST: *value = ctx->p_host; return MF_OK;
         case MF_OPT_Q_UPDATE: *value = ctx->q_update; return MF_OK;
+        case MF_OPT_DET_FLOW: *value = ctx->det_flow; return MF_OK;
+        case MF_OPT_Q_KAPPA: *value = ctx->last_kappa; return MF_OK;
         default: return MF_EINVAL;
     }
 }
@@ -462,6 +474,17 @@ extern "C" int mf_load_coo(mf_ctx *ctx, const int32_t *u, const int32_t *v, cons
                          (unsigned long long)ctx->h_scratch->bad, (long long)ctx->p_begin, (long long)ctx->p_end,
                          (long long)ctx->n);
     ctx->N = nnz;
+    {  // sum_v (deg v / N)^2: the Q-row collision rate per Hogwild! worker (MF_OPT_Q_UPDATE auto, A-20)
+        unsigned *deg = nullptr;
+        double *d_sq = nullptr, h_sq = 0;
+        CK(cudaMallocAsync((void **)&deg, sizeof(unsigned) * (size_t)(ctx->n + 2) + sizeof(double), st));
+        d_sq = reinterpret_cast<double *>(deg + ((ctx->n + 1) & ~1ll));  // 8-B aligned after the histogram
+        CK(launch_col_sq(ctx->v, nnz, ctx->n, deg, d_sq, st));
+        CK(cudaMemcpyAsync(&h_sq, d_sq, sizeof(double), cudaMemcpyDeviceToHost, st));
+        CK(cudaFreeAsync(deg, st));
+        CK(cudaStreamSynchronize(st));
+        ctx->col_sq = nnz > 0 ? h_sq / ((double)nnz * (double)nnz) : 0.0;
+    }
     ctx->reshuffle_due = false;  // the first epoch after a load uses the load's order
     ctx->shuffled = ctx->shuffle;
     RC(ctx->ensure_factors());
@@ -506,7 +529,14 @@ int mf_ctx::reshuffle() {
 // wave(i) = max(last[u_i], last[v_i]) + 1, last[] = -1 initially.  Samples are
 // then stably bucketed by wave; inside a wave no two share a row or column.
 int mf_ctx::build_waves() {
-    if (nwaves >= 0) return MF_OK;
+    if (nwaves >= 0 && (!det_flow || ord_u)) return MF_OK;
+    if (nwaves >= 0) {  // the wave layout exists without the dataflow ordinals: rebuild both
+        dev_free(&wu);
+        dev_free(&wv);
+        dev_free(&wr);
+        dev_free(&wave_off);
+        nwaves = -1;
+    }
     mf_ctx *ctx = this;
     cudaStream_t st = stream();
     std::vector<int32_t> hu((size_t)N), hv((size_t)N);
@@ -544,6 +574,26 @@ int mf_ctx::build_waves() {
     CK(cudaMemcpyAsync(wave_off, off.data(), sizeof(int64_t) * (nw + 1), cudaMemcpyHostToDevice, st));
     CK(launch_gather(u, v, r, didx, N, wu, wv, wr, st));
     CK(cudaFreeAsync(didx, st));
+    if (det_flow) {
+        // ordinals of each sample's update of its row and of its column in the serial (stored) order,
+        // written in wave order: a row's updates keep their serial order in the wave layout (waves
+        // increase along a row), so k_flow runs them in that order by waiting for counter == ordinal
+        std::vector<int32_t> ou((size_t)N), ov((size_t)N);
+        {
+            std::vector<int32_t> cnt_u((size_t)p_rows(), 0), cnt_v((size_t)n, 0);
+            for (int64_t i = 0; i < N; i++) {  // stored order = serial order
+                ou[(size_t)i] = cnt_u[(size_t)hu[(size_t)i]]++;
+                ov[(size_t)i] = cnt_v[(size_t)hv[(size_t)i]]++;
+            }
+        }
+        std::vector<int32_t> wou((size_t)N), wov((size_t)N);
+        for (int64_t j = 0; j < N; j++) wou[(size_t)j] = ou[idx[(size_t)j]], wov[(size_t)j] = ov[idx[(size_t)j]];
+        RC(dev_alloc(this, &ord_u, N, "alloc flow ordinals u"));
+        RC(dev_alloc(this, &ord_v, N, "alloc flow ordinals v"));
+        RC(dev_alloc(this, &cnt_uv, (size_t)(p_rows() + n), "alloc flow counters"));
+        CK(cudaMemcpyAsync(ord_u, wou.data(), sizeof(int32_t) * N, cudaMemcpyHostToDevice, st));
+        CK(cudaMemcpyAsync(ord_v, wov.data(), sizeof(int32_t) * N, cudaMemcpyHostToDevice, st));
+    }
     CK(cudaStreamSynchronize(st));
     nwaves = nw;
     return MF_OK;
@@ -583,7 +633,8 @@ UpdateArgs mf_ctx::update_args(float eta) const {
     a.count_updates = count_updates;
     a.scratch = scratch;
     a.r_stage = r_stage;
-    a.q_red = q_update == 1;
+    a.q_mode = q_update;
+    a.q_share = (float)(col_sq > 0 ? col_sq : 1.0 / (double)n);  // before a load: uniform columns
     return a;
 }
 
@@ -609,6 +660,7 @@ int mf_ctx::finish_epoch(int schedule, float eta, int launches, int workers_used
         stats->launches = launches;
     }
     (void)schedule;
+    if (h_scratch->diverged & 2) return fail(MF_ECUDA, "deterministic dataflow: a rating waited > 2 s in epoch %d", (int)t);
     if (h_scratch->diverged) return fail(MF_EDIVERGED, "non-finite prediction error in epoch %d", (int)t);
     return MF_OK;
 }
@@ -643,7 +695,10 @@ static int epoch_local(mf_ctx *ctx, int schedule, mf_epoch_stats *stats) {
     RC(ctx->drop_other_layouts(schedule));
     if (schedule == MF_SCHED_DETERMINISTIC) RC(ctx->build_waves());
     if (schedule == MF_SCHED_WAVEFRONT) RC(ctx->build_wavefront());
-    if (schedule == MF_SCHED_PARTITIONED) return ctx->epoch_partitioned(stats);
+    if (schedule == MF_SCHED_PARTITIONED) {
+        ctx->last_kappa = 0;
+        return ctx->epoch_partitioned(stats);
+    }
     RC(ctx->gather_q());
     ctx->seg_valid = false;
     cudaStream_t st = ctx->stream();
@@ -671,6 +726,7 @@ static int epoch_local(mf_ctx *ctx, int schedule, mf_epoch_stats *stats) {
     if (schedule == MF_SCHED_HOGWILD) {
         const int w = ctx->workers > 0 ? ctx->workers : ctx->auto_workers();
         CK(launch_hogwild(sh, a, w, ctx->variant_eff, st, &used));
+        ctx->last_kappa = (double)used * a.q_share;
     } else if (schedule == MF_SCHED_DETERMINISTIC) {
         a.u = ctx->wu;
         a.v = ctx->wv;
@@ -685,8 +741,18 @@ static int epoch_local(mf_ctx *ctx, int schedule, mf_epoch_stats *stats) {
         // 1 = generation flag bumped by the last arriver (r01c)
         a.barrier = ((ctx->variant >> 22) & 0x3) == 1 ? 1 : 0;
         // bits 24..25 = 3: two 512-thread CTAs per SM with four samples per group and step
-        CK(launch_waves(sh, a, st, &l, wsel == 3 ? 3 : wsel == 2 ? 0 : wsel == 1 ? 1 : 2));
-        used = 0;
+        if (ctx->det_flow) {  // no barriers: per-row update counters (mf_flow.cu)
+            a.ord_u = ctx->ord_u;
+            a.ord_v = ctx->ord_v;
+            a.cnt_u = ctx->cnt_uv;
+            a.cnt_v = ctx->cnt_uv + ctx->p_rows();
+            CK(cudaMemsetAsync(ctx->cnt_uv, 0, sizeof(unsigned) * (size_t)(ctx->p_rows() + ctx->n), st));
+            // MF_OPT_VARIANT bits 24..25 select the dataflow form (mf_flow.cu launch_flow)
+            CK(launch_flow(flow_shape(ctx->k, ctx->storage), a, st, &used, wsel));
+        } else {
+            CK(launch_waves(sh, a, st, &l, wsel == 3 ? 3 : wsel == 2 ? 0 : wsel == 1 ? 1 : 2));
+            used = 0;
+        }
     } else {  // wavefront
         int l = 0;
         RC(ctx->run_wavefront(sh, a, &l, &used));

@@ -38,7 +38,11 @@ struct mf_ctx {
                         // families with their own Latin squares, each hand-over overlapping the other's compute)
     int wave_cta = 0;   // wavefront worker = CTA with shared-memory Q group (MF_OPT_WAVE_CTA)
     int variant = 0;
-    int q_update = 1;   // MF_OPT_Q_UPDATE: batch-Hogwild! Q write-back 1 = atomic add of the change (A-20), 0 = store
+    int det_flow = 0;   // MF_OPT_DET_FLOW: deterministic schedule executed by per-row counters (1) or grid-barrier waves (0)
+    int q_update = 2;   // MF_OPT_Q_UPDATE: batch-Hogwild! Q write-back 1 = atomic add of the change (A-20), 0 = store,
+                        // 2 = auto by the expected concurrent updates per Q row
+    double last_kappa = -1;  // kappa of the last batch-Hogwild! epoch (max over its launches; MF_OPT_Q_KAPPA)
+    double col_sq = 0;  // sum_v (deg v / N)^2 of the loaded samples (0 before a load: launches use 1 / n)
     int r_stage = 1;    // MF_OPT_R_STAGING: batch-Hogwild! triples 1 = registers, 2 = TMA bulk copies into shared memory
     int trace = 0;
     // L2 prefetch, auto mode (MF_OPT_VARIANT bits 16..19 = 0).  Whether a prefetch pays depends on
@@ -99,6 +103,10 @@ struct mf_ctx {
     float *wr = nullptr;
     int64_t *wave_off = nullptr;
     int64_t nwaves = -1;
+    // deterministic dataflow execution (MF_OPT_DET_FLOW, mf_flow.cu): per wave-sorted sample the ordinals of its
+    // update of row u / column v in the serial order, and per row the updates applied so far
+    int32_t *ord_u = nullptr, *ord_v = nullptr;
+    unsigned *cnt_uv = nullptr;  // p_rows() + n counters
 
     // wavefront layout (mf_wavefront.cu)
     bool wf_valid = false;

@@ -539,6 +539,7 @@ static cudaError_t hogwild_launch(const UpdateArgs &a, int workers, cudaStream_t
     const int blocks = (int)((warps + kWarpsPerBlock - 1) / kWarpsPerBlock);
     if (used) *used = (int)(groups * D);
     UpdateArgs args = a;
+    args.q_red = a.q_mode == 1 || (a.q_mode == 2 && (double)(groups * D) * a.q_share < kQRedKappa);
     args.active_groups = groups;
     args.batch_f = batch_f;
     // every launch claims chunks from 0 (the partitioned path launches once per block)
@@ -771,6 +772,27 @@ cudaError_t launch_waves(const ShapeId &sh, const UpdateArgs &a, cudaStream_t st
         if (launches) *launches = 1;
         return cudaLaunchCooperativeKernel((const void *)k_waves<SH>, dim3(blocks), dim3(kBlock), kargs, 0, st);
     });
+}
+
+// ------------------------------------------------------- column degree moment --
+__global__ void k_col_hist(const int32_t *v, int64_t n, unsigned *deg) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        atomicAdd(deg + v[i], 1u);
+}
+__global__ void k_sq_sum(const unsigned *deg, int64_t n_cols, double *out) {
+    double s = 0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_cols; i += (int64_t)gridDim.x * blockDim.x)
+        s += (double)deg[i] * (double)deg[i];
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if ((threadIdx.x & 31) == 0 && s != 0) atomicAdd(out, s);  // integer-valued terms: exact in any order
+}
+cudaError_t launch_col_sq(const int32_t *v, int64_t n, int64_t n_cols, unsigned *tmp, double *out, cudaStream_t st) {
+    cudaError_t e = cudaMemsetAsync(tmp, 0, sizeof(unsigned) * n_cols, st);
+    if (e == cudaSuccess) e = cudaMemsetAsync(out, 0, sizeof(double), st);
+    if (e != cudaSuccess) return e;
+    if (n > 0) k_col_hist<<<148 * 8, 256, 0, st>>>(v, n, tmp);
+    k_sq_sum<<<148, 256, 0, st>>>(tmp, n_cols, out);
+    return cudaGetLastError();
 }
 
 // -------------------------------------------------------------------- RMSE --

@@ -48,10 +48,20 @@ struct UpdateArgs {
     int r_stage;        // batch-Hogwild! triples: 2 = TMA bulk copies of each chunk into shared memory, else
                         // registers (3 coalesced 32-bit loads per lane per 32-sample tile, shuffled to groups)
     int q_red;          // batch-Hogwild!: Q rows written back as an atomic add of their change (red.global.add,
-                        // DESIGN.md A-20) instead of a store of the new row (MF_OPT_Q_UPDATE)
+                        // DESIGN.md A-20) instead of a store of the new row -- resolved by launch_hogwild from:
+    int q_mode;         //   MF_OPT_Q_UPDATE: 0 store, 1 atomic add, 2 auto (atomic add iff kappa < kQRedKappa)
+    float q_share;      //   sum over the launch's Q rows of (degree / samples)^2: kappa = workers x q_share is the
+                        //   expected number of concurrent updates an update shares its Q row with
+    const int32_t *ord_u;  // deterministic dataflow (k_flow): per sample, # earlier samples (serial order) of its row u
+    const int32_t *ord_v;  //   ... and of its column v
+    unsigned *cnt_u;       //   per P row / Q row: updates applied so far this epoch
+    unsigned *cnt_v;
     int barrier;        // deterministic waves, 1024-thread CTAs: 0 = arrival counter polled to (w+1) x CTAs
                         // (one release reduction + acquire polls), 1 = last arriver bumps a generation flag
 };
+
+// MF_OPT_Q_UPDATE = 2 (auto): atomic Q write-back iff kappa < this (A-20)
+constexpr float kQRedKappa = 0.5f;
 
 // Kernel-shape choice for (k, storage); filled by select_shape().
 struct ShapeId {
@@ -78,9 +88,14 @@ cudaError_t launch_shuffle_perm(int64_t n, uint64_t seed, uint32_t *perm_out, cu
 cudaError_t launch_gather_validate(const int32_t *u_in, const int32_t *v_in, const float *r_in, const uint32_t *idx,
                                    int64_t n, int64_t row_lo, int64_t row_hi, int64_t n_cols, int32_t *u_out,
                                    int32_t *v_out, float *r_out, DevScratch *scratch, cudaStream_t st);
+// sum over columns of deg(v)^2 (exact in fp64 below 2^53), deg = histogram of v[0..n); tmp: n_cols words
+cudaError_t launch_col_sq(const int32_t *v, int64_t n, int64_t n_cols, unsigned *tmp, double *out, cudaStream_t st);
 cudaError_t launch_compose(const uint32_t *a, const uint32_t *b, uint32_t *out, int64_t n, cudaStream_t st);
 cudaError_t launch_gather(const int32_t *u_in, const int32_t *v_in, const float *r_in, const uint32_t *idx, int64_t n,
                           int32_t *u_out, int32_t *v_out, float *r_out, cudaStream_t st);
+
+cudaError_t launch_flow(const ShapeId &sh, const UpdateArgs &a, cudaStream_t st, int *warps_used, int form = 0);
+ShapeId flow_shape(int k, int storage);  // the one-rating-per-warp shape k_flow runs
 
 ShapeId select_shape(int k, int storage, int variant);
 ShapeId hogwild_shape(int k, int storage, int variant);  // batch-Hogwild!'s default (variant 0) differs at k = 128

@@ -534,11 +534,13 @@ int mf_ctx::epoch_partitioned(mf_epoch_stats *stats) {
                     a.r = br + lo;
                     a.n = hi - lo;
                     a.Q = q_cur[li];
+                    a.q_share *= (float)(part_mode ? 2 * G : G);  // the launch's Q rows: a segment or half of one
                     const int w = workers > 0 ? workers
                                               : (int)std::max<int64_t>(1, std::min<int64_t>(n_local[li] / 10000, 1 << 30));
                     int used = 0;
                     CK(launch_hogwild(sh, a, w, variant, st, &used));
                     used_max = std::max(used_max, used);
+                    last_kappa = std::max(last_kappa, (double)used * a.q_share);
                     launches++;
                 }
                 rc = exchange_half(next, h);
@@ -761,12 +763,14 @@ int mf_ctx::epoch_units(mf_epoch_stats *stats) {
                     a.r = br + lo;
                     a.n = hi - lo;
                     a.Q = u_cur[h][li];
+                    a.q_share *= (float)(2 * G);  // the launch's Q rows: one unit (half a segment)
                     a.chunk_ctr = h ? &scratch->chunk2 : &scratch->chunk;
                     const int64_t wp = workers > 0 ? workers : std::max<int64_t>(1, std::min<int64_t>(n_local[li] / 10000, 1 << 30));
                     const int w = serial ? 1 : (int)std::max<int64_t>(1, wp / 2);  // half of the partition's workers per family
                     int used = 0;
                     CK(launch_hogwild(sh, a, w, variant, hs, &used));
                     used_round += used;
+                    last_kappa = std::max(last_kappa, (double)used * a.q_share);
                     launches++;
                 }
                 rc = exchange_unit(next[h], h, hs);

@@ -102,6 +102,7 @@ struct WfArgs {
     int pf;               // CTA workers: L2 prefetch of a tile's P rows when it is claimed (0 off, 1 bulk, 2 per line)
     int min_per_group;    // CTA workers: in-block concurrency clamp, samples per concurrent group
     int tma;              // CTA workers: stage the Q group with bulk async copies (TMA engine) instead of a thread loop
+    int q_late;           // CTA workers: read a rating's q_v from shared memory only once its p_u has arrived
     float eta, lam;
     int64_t n_cols;       // column groups are balanced segments [floor(g n / c), floor((g+1) n / c))
 };
@@ -412,6 +413,12 @@ __device__ __forceinline__ void cta_tile(const WfArgs &a, uint32_t qbase, int k,
         }
 #pragma unroll
         for (int d = 0; d < D; d++) {
+            // Late Q read: the group's q_v is read from shared memory after p_u has arrived from L2 / DRAM
+            // (an empty asm that consumes p_u's first word and "produces" the address), not when p_u's
+            // load is issued.  128 groups share a column group of ~100 Q rows, so the read-to-write window
+            // decides how many updates of a row overlap and are lost to a later store: it shrinks from
+            // a global-load latency to the dot product and the update.
+            if (a.q_late) asm volatile("" : "+r"(qa[d]) : "r"(pr[d].w[0][0]));
 #pragma unroll
             for (int jv = 0; jv < SH::V; jv++) {
                 const int e = (int)vec_elem<SH>(jv, sub);
@@ -999,6 +1006,9 @@ int mf_ctx::run_wavefront(const ShapeId &, const UpdateArgs &ua, int *launches, 
             const int sel = (variant_eff >> 26) & 0x3;
             a.min_per_group = sel == 0 ? (int)kCtaMinPerGroup : sel == 1 ? 32 : sel == 2 ? 64 : 8;
         }
+        // bits 22..23: 1 = read q_v from shared memory when p_u's load is issued (before r02ab), else once p_u
+        // has arrived (default: a shorter race window on the group's Q rows)
+        a.q_late = ((variant_eff >> 22) & 0x3) != 1;
         // bits 20..21: Q-group staging, 0 = bulk async copies when rows are 16-B multiples, 2 = thread loop
         a.tma = ((variant_eff >> 20) & 0x3) != 2 && row_bytes % 16 == 0 && ((uintptr_t)Q & 15) == 0;
         // (k = 32 / 64 keep the 16-byte-vector shapes: 4 / 8 lanes (16-bit rows), 8 / 16 lanes (fp32) --

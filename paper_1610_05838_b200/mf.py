@@ -27,7 +27,7 @@ SCHEDULES = {"hogwild": 0, "wavefront": 1, "deterministic": 2, "partitioned": 3}
  MF_OPT_STREAM, MF_OPT_SHUFFLE, MF_OPT_COUNT_UPDATES, MF_OPT_WAVE_PERM, MF_OPT_EPOCH, MF_OPT_PARTITIONS,
  MF_OPT_SEED_SHUFFLE, MF_OPT_VARIANT, MF_OPT_TRACE, MF_OPT_SUBEPOCHS, MF_OPT_WAVE_CTA,
  MF_OPT_STREAM_CHUNK, MF_OPT_PART_SPLIT, MF_OPT_R_STAGING, MF_OPT_WAVE_PASSES, MF_OPT_P_HOST,
- MF_OPT_Q_UPDATE) = range(24)
+ MF_OPT_Q_UPDATE, MF_OPT_DET_FLOW, MF_OPT_Q_KAPPA) = range(26)
 STORAGE = {"f32": 0, "fp32": 0, "f16": 1, "fp16": 1, "bf16": 2}
 
 

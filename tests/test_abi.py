@@ -35,11 +35,13 @@ def test_create_validates_arguments_without_device():
     try:
         mf.mf_set_option(h, mf.MF_OPT_BETA, 0.3)
         assert mf.mf_get_option(h, mf.MF_OPT_BETA) == 0.3
-        assert mf.mf_get_option(h, mf.MF_OPT_Q_UPDATE) == 1  # default: atomic add of the change (A-20)
+        assert mf.mf_get_option(h, mf.MF_OPT_Q_UPDATE) == 2  # default: auto by kappa (A-20)
+        assert mf.mf_get_option(h, mf.MF_OPT_Q_KAPPA) == -1
+        assert mf.mf_get_option(h, mf.MF_OPT_DET_FLOW) == 0
         mf.mf_set_option(h, mf.MF_OPT_Q_UPDATE, 0)
         assert mf.mf_get_option(h, mf.MF_OPT_Q_UPDATE) == 0
         with pytest.raises(mf.MFError):
-            mf.mf_set_option(h, mf.MF_OPT_Q_UPDATE, 2)
+            mf.mf_set_option(h, mf.MF_OPT_Q_UPDATE, 3)
         with pytest.raises(mf.MFError):
             mf.mf_set_option(h, mf.MF_OPT_STORAGE, 7)
         with pytest.raises(mf.MFError):

@@ -121,17 +121,18 @@ def test_c1_deterministic_bit_reproducible_and_multi_epoch(mfmod, c1):
 
 @pytest.mark.parametrize("storage,cfgname", [(0, "C2-1pct"), (1, "C2-1pct"), (2, "C1"), (1, "C2-zipf-1pct")])
 def test_deterministic_executions_bitwise_equal(mfmod, storage, cfgname):
-    """The deterministic schedule's executions (MF_OPT_VARIANT bits 24..25): 1024-thread CTAs with two
-    samples of a wave per group (default), with one, 256-thread CTAs with the fenced barrier, two
-    512-thread CTAs per SM with four samples per group, and the
-    two grid barriers of the 1024-thread form (bits 22..23: arrival counter, generation flag) apply the
-    same updates wave by wave with the same per-rating arithmetic, so their factors agree bit for bit
-    (3 epochs)."""
+    """The wave executions of the deterministic schedule (MF_OPT_DET_FLOW = 0; MF_OPT_VARIANT bits 24..25):
+    1024-thread CTAs with two samples of a wave per group, with one, 256-thread CTAs with the fenced
+    barrier, two 512-thread CTAs per SM with four samples per group, and the two grid barriers of the
+    1024-thread form (bits 22..23: arrival counter, generation flag) apply the same updates wave by wave
+    with the same per-rating arithmetic, so their factors agree bit for bit (3 epochs).  The dataflow
+    execution (MF_OPT_DET_FLOW = 1) gives the same bits in both of its forms and run to run, and agrees
+    with the waves to the rounding of its 32-lane dot product."""
     cfg = datagen.CONFIGS[cfgname]
     (u, v, r), _ = datagen.make(cfg)
     out = []
     for var in (0, 1 << 24, 2 << 24, 3 << 24, 1 << 22, (1 << 22) | (1 << 24)):
-        with _gpu(mfmod, cfg, storage, count_updates=1, variant=var) as g:
+        with _gpu(mfmod, cfg, storage, count_updates=1, variant=var, det_flow=0) as g:
             g.load(u, v, r)
             for _ in range(3):
                 assert g.epoch("deterministic").updates == len(u)
@@ -139,6 +140,18 @@ def test_deterministic_executions_bitwise_equal(mfmod, storage, cfgname):
     for P, Q in out[1:]:
         np.testing.assert_array_equal(P, out[0][0])
         np.testing.assert_array_equal(Q, out[0][1])
+    flow = []
+    for var in (0, 0, 2 << 24):  # round-robin ownership twice, then tiles claimed in order
+        with _gpu(mfmod, cfg, storage, count_updates=1, det_flow=1, variant=var) as g:
+            g.load(u, v, r)
+            for _ in range(3):
+                assert g.epoch("deterministic").updates == len(u)
+            flow.append(g.factors())
+    for P, Q in flow[1:]:  # every row sees its serial sequence of updates with the same arithmetic
+        np.testing.assert_array_equal(P, flow[0][0])
+        np.testing.assert_array_equal(Q, flow[0][1])
+    for X, R in zip(flow[0], out[0]):
+        assert frob(X, R) <= TOL[storage], frob(X, R)
 
 
 @pytest.mark.parametrize("k", [2, 7, 32, 33, 64, 100, 128, 256])
@@ -159,7 +172,8 @@ def test_deterministic_k_sweep_ragged(mfmod, k, storage):
 
 
 @pytest.mark.parametrize("storage", [0, 1])
-def test_netflix_slice_deterministic(mfmod, storage):
+@pytest.mark.parametrize("det_flow", [1, 0])
+def test_netflix_slice_deterministic(mfmod, storage, det_flow):
     """C2-1pct (Netflix degrees, k=128): ~8k waves of ~120 samples; fast vectorised shape."""
     cfg = datagen.CONFIGS["C2-1pct"]
     (u, v, r), (tu, tv, tr) = datagen.make(cfg)
@@ -167,7 +181,7 @@ def test_netflix_slice_deterministic(mfmod, storage):
     ref = oracle.Model(cfg.m, cfg.n, cfg.k, ORC[storage], seed=cfg.seed_init)
     ref.epoch(u, v, r, oracle.eta(cfg.alpha, cfg.beta, 0), cfg.lam, order)
     Pr, Qr = ref.factors_f32()
-    with _gpu(mfmod, cfg, storage) as g:
+    with _gpu(mfmod, cfg, storage, det_flow=det_flow) as g:
         g.load(u, v, r)
         nw = mfmod.mf_wave_count(g.h)
         _, nw_ref = oracle.waves(cfg.m, cfg.n, u, v, order)
@@ -411,7 +425,8 @@ def test_degenerate_shapes_every_schedule_is_serial(mfmod, storage, m_, n_, N, k
         ref.epoch(u, v, r, oracle.eta(0.05, 0.3, t), 0.02)
     Pr, Qr = ref.factors_f32()
     tol = TOL[storage]
-    runs = [("hogwild", {"workers": 1}), ("hogwild", {"workers": 1, "q_update": 0}), ("deterministic", {}), ("wavefront", {"wave_rows": 1, "wave_cols": 1}),
+    runs = [("hogwild", {"workers": 1}), ("hogwild", {"workers": 1, "q_update": 0}),
+            ("hogwild", {"workers": 1, "q_update": 1}), ("deterministic", {}), ("deterministic", {"det_flow": 1}), ("wavefront", {"wave_rows": 1, "wave_cols": 1}),
             ("host", {"workers": 1})]
     if k == 7 and N <= 32:  # a masked 32-lane CTA shape, one rating at a time, one 32-sample tile
         runs.append(("wavefront", {"wave_cta": 1, "wave_rows": 1, "wave_cols": 1}))
