@@ -263,7 +263,8 @@ cudaError_t launch_flow(const ShapeId &sh, const UpdateArgs &a, cudaStream_t st,
         int dev = 0, sms = 0, per_sm = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        const void *kern = (const void *)k_flow<SH, true, 4>;
+        // (the masked generic shapes get a 128-register budget: under 64 they spill)
+        const void *kern = (const void *)k_flow<SH, true, SH::FULL ? 4 : 2>;
         if constexpr (SH::FULL) {  // tile claims for the vectorised shapes only
             if (form == 2) kern = (const void *)k_flow<SH, false, 4>;
             else form = 0;

@@ -750,17 +750,19 @@ cudaError_t launch_waves(const ShapeId &sh, const UpdateArgs &a, cudaStream_t st
                 }
             }
         }
-        if (big) {  // one 1024-thread CTA per SM: a quarter of the barrier arrivals; big = 2: two per group
-            const void *kern = (const void *)k_waves<SH, 1024, 1>;
-            if constexpr (SH::FULL) {
-                if (big == 2) kern = (const void *)k_waves<SH, 1024, 2>;
-            }
-            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 1024, 0);
-            if (per_sm >= 1) {
-                UpdateArgs args = a;
-                void *kargs[] = {&args};
-                if (launches) *launches = 1;
-                return cudaLaunchCooperativeKernel(kern, dim3(sms), dim3(1024), kargs, 0, st);
+        // one 1024-thread CTA per SM: a quarter of the barrier arrivals; big = 2: two per group.  The
+        // masked generic shapes (k outside 32 / 64 / 128 / 256) keep more than 64 registers per thread,
+        // so they run the 256-thread form (identical results) instead of spilling under the 1024-thread cap.
+        if constexpr (SH::FULL) {
+            if (big) {
+                const void *kern = big == 2 ? (const void *)k_waves<SH, 1024, 2> : (const void *)k_waves<SH, 1024, 1>;
+                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 1024, 0);
+                if (per_sm >= 1) {
+                    UpdateArgs args = a;
+                    void *kargs[] = {&args};
+                    if (launches) *launches = 1;
+                    return cudaLaunchCooperativeKernel(kern, dim3(sms), dim3(1024), kargs, 0, st);
+                }
             }
         }
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_waves<SH>, kBlock, 0);
