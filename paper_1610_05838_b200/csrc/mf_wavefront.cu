@@ -824,7 +824,9 @@ int mf_ctx::build_wavefront() {
         // s = sqrt(N / 17.5).  Netflix shape f16: s / c = 1,184 / 2,368 2.19 G updates/s, 2,368 / 2,960
         // 3.08-3.13, 3,552 / 4,440 3.06, 4,736 / 5,920 2.87 (profiles/r02h_warp_*, r02i_warp_*)
         const double by_blocks = std::sqrt((double)N / 17.5);
-        s = (int)std::max<double>(1.0, std::min<double>({(double)num_sms * 16, by_blocks, (double)rows}));
+        // (and c = 1.25 s column groups must exist: s <= 0.8 n on narrow matrices)
+        s = (int)std::max<double>(1.0, std::min<double>({(double)num_sms * 16, by_blocks, (double)rows,
+                                                         std::floor(0.8 * (double)n)}));
     }
     if (c <= 0) c = (int)std::min<int64_t>(warp_auto ? std::max<int64_t>(s, (5 * (int64_t)s + 3) / 4) : 2 * (int64_t)s, n);
     if (s > rows || c > n || s < 1 || c < s)

@@ -2,8 +2,12 @@
 
 C2-zipf-1pct has the Netflix 1% slice's size with Zipf(0.3) rows and Zipf(0.5) columns: the hottest
 column holds ~4% of the ratings (39k samples, 7x the uniform slice's maximum degree), so Hogwild
-conflicts concentrate on it and the deterministic schedule needs ~39k waves.
+conflicts concentrate on it and the deterministic schedule needs ~39k waves.  C2-zipf-10pct is the
+10% slice with the same skew, where the schedules are gated against the oracle's golden traces.
 """
+import json
+import os
+
 import numpy as np
 import pytest
 
@@ -44,36 +48,54 @@ def test_skewed_deterministic_parity(mf, zipf):
     assert np.linalg.norm(Q - ref.Q) / np.linalg.norm(ref.Q) <= 1e-5
 
 
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def _gold(storage, seed=None):
+    tag = "" if seed is None else f"_seed{seed}"
+    path = os.path.join(GOLD, f"C2-zipf-10pct_{storage}{tag}_trace.json")
+    return json.load(open(path))["rmse"] if os.path.exists(path) else None
+
+
 @pytest.fixture(scope="module")
-def zipf_oracle(zipf):
-    """Oracle test RMSE after 10 epochs on the A-8 order (seed 42) and its spread over seeds 42-44
-    (0.75% here: the order alone moves the result by more than the 0.5% gate; reading T3)."""
-    cfg, ((u, v, r), test) = zipf
-    out = []
-    for sd in (cfg.seed_shuffle, 43, 44):
-        _, tr = oracle.train(cfg.m, cfg.n, cfg.k, oracle.F32, cfg.seed_init, u, v, r, cfg.alpha, cfg.beta, cfg.lam,
-                             10, order=oracle.shuffle_perm(sd, len(u)), test=test)
-        out.append(tr[-1])
-    return out[0], max(out) - min(out)
+def zipf10():
+    cfg = datagen.CONFIGS["C2-zipf-10pct"]
+    return cfg, datagen.make(cfg)
 
 
-@pytest.mark.parametrize("schedule,opts", [
-    ("hogwild", {}), ("wavefront", {"wave_cta": 1}), ("partitioned", {"partitions": 4}),
-    pytest.param("wavefront", {}, marks=pytest.mark.xfail(
-        strict=False, reason="paper-literal wavefront (warp workers, serial ~100-sample blocks) under power-law "
-                             "degrees: +2.8% vs the oracle after 10 epochs, beyond the oracle's 0.75% seed spread; "
-                             "the paper already notes wavefront converges slower (PAPER.md:256); DESIGN.md 8.1"))])
-def test_skewed_schedules_rmse_within_gate(mf, zipf, zipf_oracle, schedule, opts):
-    cfg, ((u, v, r), test) = zipf
-    E = 10
-    ref, spread = zipf_oracle
-    gate = max(0.005 * ref, spread)
-    with _ctx(mf, cfg, count_updates=1, **opts) as g:
+# Every parallel schedule on the 10% Zipf slice (48,019 x 1,777, 9.9M ratings, hottest column 1.2% of them):
+# ONE run against the oracle's golden trace (scripts/make_golden.py, oracle/ only), gated from `first` on at
+# 0.5% or the oracle's own shuffle-seed spread at that epoch where larger (T3; <= 0.27% here --
+# on the 1% slice the order alone moved the oracle by 0.75% after 10 epochs, so that slice could not show
+# a 0.5% gate).  Blocked orders (the wavefront forms) are gated after the 10 epochs (T6; their traces are in
+# DESIGN.md 8.1).
+CASES = [("hogwild", {}, 2), ("partitioned", {"partitions": 2}, 4), ("partitioned", {"partitions": 4}, 4),
+         ("partitioned", {"partitions": 8}, 4), ("wavefront", {"wave_cta": 1}, 10),
+         pytest.param("wavefront", {}, 10, marks=pytest.mark.xfail(
+             strict=False, reason="paper-literal wavefront (warp workers, serial ~40-sample blocks) under power-law "
+                                  "degrees: +0.9% vs the oracle after 10 epochs (its trace swings between +0.06% and "
+                                  "+1.3% over epochs 7-10); the paper notes wavefront converges slower (PAPER.md:256); "
+                                  "DESIGN.md 8.1, profiles/r02ah_zipf10_*"))]
+
+
+@pytest.mark.parametrize("storage", ["f32", "f16"])
+@pytest.mark.parametrize("schedule,opts,first", CASES)
+def test_skewed_schedules_track_the_oracle(mf, zipf10, storage, schedule, opts, first):
+    gold = _gold(storage)
+    if gold is None:
+        pytest.skip(f"golden C2-zipf-10pct_{storage} not generated")
+    traces = [gold] + [t for t in (_gold(storage, 43), _gold(storage, 44)) if t]
+    gates = [max(0.005 * g, max(tr[t] for tr in traces) - min(tr[t] for tr in traces)) for t, g in enumerate(gold)]
+    cfg, ((u, v, r), test) = zipf10
+    got = []
+    with _ctx(mf, cfg, storage=storage, count_updates=1, **opts) as g:
         g.load(u, v, r)
-        for _ in range(E):
+        for _ in range(len(gold)):
             assert g.epoch(schedule).updates == len(u)
-        got = g.rmse(*test)
-    assert abs(got - ref) <= gate, (got, ref, gate)
+            got.append(g.rmse(*test))
+    bad = [(t + 1, a, b, round(100 * (a - b) / b, 3), gt) for t, (a, b, gt) in enumerate(zip(got, gold, gates))
+           if t + 1 >= first and abs(a - b) > gt]
+    assert not bad, bad
 
 
 def test_per_epoch_reshuffle_is_serial_sgd_on_the_composed_orders(mf):
