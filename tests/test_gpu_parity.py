@@ -282,6 +282,27 @@ def test_netflix_slice_hogwild_many_workers(mfmod):
     assert abs(got - gold[E - 1]) <= 0.005 * gold[E - 1], (got, gold[E - 1])
 
 
+def test_q_update_kappa_follows_the_degrees(mfmod):
+    """MF_OPT_Q_UPDATE = 2 (auto, A-20) decides by kappa = workers x sum_v (deg v / N)^2 of the launch's Q
+    rows; MF_OPT_Q_KAPPA reports it after an epoch: on the Netflix slice (1,777 columns) it is the worker
+    count over ~1,777, for batch-Hogwild! and (per unit launch: half of a partition's workers on 1/(2G) of
+    the columns) for the partitioned schedule."""
+    cfg, (train, _) = _c2_10pct_data()
+    u, v, r = train
+    deg = np.bincount(v, minlength=cfg.n).astype(np.float64)
+    share = float(((deg / len(v)) ** 2).sum())
+    for w in (990, 400):
+        with _gpu(mfmod, cfg, 1, workers=w) as g:
+            assert g.get(mfmod.MF_OPT_Q_KAPPA) == -1
+            g.load(u, v, r)
+            st = g.epoch("hogwild")
+            assert g.get(mfmod.MF_OPT_Q_KAPPA) == pytest.approx(st.workers * share, rel=1e-5)
+    with _gpu(mfmod, cfg, 1, partitions=2, workers=400) as g:
+        g.load(u, v, r)
+        g.epoch("partitioned")
+        assert g.get(mfmod.MF_OPT_Q_KAPPA) == pytest.approx(200 * share * 4, rel=1e-5)
+
+
 @pytest.mark.parametrize("storage", [0, 1])
 def test_q_store_form_still_tracks_the_oracle(mfmod, storage):
     """MF_OPT_Q_UPDATE = 0: the Q row written back by a plain store (the paper's worker; of two concurrent
