@@ -740,8 +740,6 @@ static int epoch_local(mf_ctx *ctx, int schedule, mf_epoch_stats *stats) {
         // bits 22..23: grid barrier of the 1024-thread forms, 0 = arrival counter polled to its target,
         // 1 = generation flag bumped by the last arriver (r01c)
         a.barrier = ((ctx->variant >> 22) & 0x3) == 1 ? 1 : 0;
-        // bits 16..19 = 1: L2 prefetch of the next wave's first-step rows before the barrier (k_waves)
-        a.prefetch = ((ctx->variant >> 16) & 0xF) == 1 ? 1 : 0;
         // bits 24..25 = 3: two 512-thread CTAs per SM with four samples per group and step
         if (ctx->det_flow) {  // no barriers: per-row update counters (mf_flow.cu)
             a.ord_u = ctx->ord_u;

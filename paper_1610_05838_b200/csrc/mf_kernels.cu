@@ -723,22 +723,7 @@ __global__ void __launch_bounds__(BLOCK) k_waves(UpdateArgs a) {
                 if (val[d] && sub == 0) done++;
             }
         }
-        if (w + 1 < a.nwaves) {
-            fetch_first(w + 1);
-            // optional (MF_OPT_VARIANT bits 16..19 = 1): ask L2 for the rows of the group's first step of the
-            // next wave before waiting at the barrier -- it moves no values into registers (L2 is the point of
-            // coherence, so a row still being updated by this wave is fetched again by the real load), and the
-            // loads after the barrier then wait for L2 instead of DRAM
-            if constexpr (SH::FULL && (SH::KMAX * SH::BYTES) % 16 == 0) {
-                if (a.prefetch && sub == 0) {
-#pragma unroll
-                    for (int d = 0; d < D; d++) {
-                        prefetch_row_l2(a.P, nu[d], (uint32_t)(SH::KMAX * SH::BYTES));
-                        prefetch_row_l2(a.Q, nv[d], (uint32_t)(SH::KMAX * SH::BYTES));
-                    }
-                }
-            }
-        }
+        if (w + 1 < a.nwaves) fetch_first(w + 1);
         if (BLOCK == kBlock) grid_barrier(a.scratch, gridDim.x);
         else if (a.barrier == 0) grid_barrier_count(a.scratch, (unsigned)(w + 1) * gridDim.x);
         else grid_barrier_ra(a.scratch, gridDim.x);
