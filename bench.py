@@ -407,10 +407,12 @@ def main():
         if clk:
             clk.__exit__(None, None, None)
         var_eff = int(g.get(mf.MF_OPT_VARIANT))  # the auto fields resolved (hogwild L2 prefetch pick)
+        kappa = g.get(mf.MF_OPT_Q_KAPPA)  # batch-Hogwild!: expected concurrent updates per Q row (A-20)
         g.close()
         ms_ = e0.elapsed_time(e1) / steps
         return {"ms": ms_, "value": N / (ms_ * 1e-3), "kernel_s": statistics.mean(kern), "launches": launches,
-                "rmse": rm, "workers": workers, "epochs_done": warmup + steps, "variant": var_eff}
+                "rmse": rm, "workers": workers, "epochs_done": warmup + steps, "variant": var_eff,
+                "q_kappa": kappa if kappa >= 0 else None}
 
     clk = Clocks(local)
     head = measure(a.storage, a.schedule, a.steps, a.warmup, clk=clk)
@@ -501,7 +503,10 @@ def main():
         "dtype": "f32", "storage": a.storage, "data": "synthetic",
         "config": workload_config(cfg, 1, a.storage, a.schedule),
         "arm": {"workers": workers, "batch_f": 256, "variant": head["variant"],
-                "l2_row_prefetch": ((head["variant"] >> 16) & 0xF) not in (0, 15)},
+                "l2_row_prefetch": ((head["variant"] >> 16) & 0xF) not in (0, 15),
+                "q_kappa": head["q_kappa"],
+                "q_write_back": None if head["q_kappa"] is None else
+                ("atomic add" if head["q_kappa"] < 0.5 else "store") + " (MF_OPT_Q_UPDATE auto, DESIGN.md A-20)"},
         "test_rmse": rmses[-1],
         "roofline": roof,
         "cpu_baseline": cpu,

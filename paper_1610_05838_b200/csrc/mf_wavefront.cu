@@ -838,11 +838,13 @@ int mf_ctx::build_wavefront() {
     // after 5 epochs: CTA workers 0.40-0.51, warp workers +13% after 4; serial 0.1675), on the Netflix
     // shape it is +265% after epoch 1 and +11% after epoch 2.  P passes split each user's ratings into P
     // slices visited in independent orders (profiles/r02r_*, r02v_*):
-    //  - CTA workers: P = round(sqrt(V / 10)), V = N / (n s) the updates a Q row takes per visit in one
-    //    pass -- an empirical rule fitted to the three shapes: Netflix V = 38 -> P = 2 (every epoch from the
-    //    2nd within 0.5% of serial SGD, +29% time; P = 4: +75%), Yahoo V = 2.7 -> 1 (within 0.5% from
-    //    epoch 2 already; P = 2 would cost 54%), Hugewiki V = 521 -> 7 (P = 8: serial SGD's trajectory at
-    //    +7% time; P = 32: +1..2% behind and +35% time);
+    //  - CTA workers: P = 1 + round(log2(V / 10)) (at least 1), V = N / (n s) the updates a Q row takes per
+    //    visit in one pass -- an empirical rule fitted to the three shapes: Netflix V = 38 -> P = 3 (fp16:
+    //    +1.7% / +0.04% after epochs 1 / 2 and within 0.42% to epoch 20 at +9% time over P = 2, which was
+    //    +6.5% / +0.46% and +0.51% at epoch 20; profiles/r02ak_c2_f16.jsonl), Yahoo V = 2.7 -> 1 (within
+    //    0.5% from epoch 2 already; P = 2 would cost 54%), Hugewiki V = 521 -> 7 (P = 8: serial SGD's
+    //    trajectory at +7% time; P = 10: the same test RMSE after 5 epochs at +11% time over 7, r02al;
+    //    P = 32: +1..2% behind and +35% time);
     //  - warp workers (blocks of ~14-450 samples): as many passes as keep blocks at >= 64 samples
     //    (Hugewiki 6, Netflix and Yahoo 1; each block costs a lock hand-over).
     int npass_auto = 1;
@@ -850,7 +852,7 @@ int mf_ctx::build_wavefront() {
         const double per_block = (double)N / ((double)s * (double)c);
         if (wave_cta) {
             const double V = (double)N / ((double)n * (double)s);
-            npass_auto = (int)std::max(1.0, std::min(64.0, std::floor(std::sqrt(V / 10.0) + 0.5)));
+            npass_auto = (int)std::max(1.0, std::min(64.0, 1.0 + std::floor(std::log2(V / 10.0) + 0.5)));
             while (npass_auto > 1 && per_block / npass_auto < 512.0) npass_auto--;  // keep blocks >= 512 samples
         } else {
             npass_auto = (int)std::max(1.0, std::min(64.0, std::floor(per_block / 64.0)));

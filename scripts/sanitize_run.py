@@ -29,7 +29,10 @@ def main():
                                 ("hogwild", {"r_staging": 2}), ("hogwild", {"r_staging": 2, "batch_f": 96}),
                                 ("deterministic", {"variant": 1 << 22}),
                                 ("partitioned", {"partitions": 3}), ("partitioned", {"partitions": 3, "part_split": 0}),
-                                ("partitioned", {"partitions": 3, "part_split": 1})):
+                                ("partitioned", {"partitions": 3, "part_split": 1}),
+                                ("hogwild", {"q_update": 1}), ("hogwild", {"q_update": 1, "r_staging": 2}),
+                                ("partitioned", {"partitions": 3, "q_update": 1}),
+                                ("deterministic", {"det_flow": 1}), ("deterministic", {"det_flow": 1, "variant": 2 << 24})):
                 g = mf.MF(cfg.m, cfg.n, k, cfg.alpha, cfg.lam, cfg.seed_init, storage=storage, beta=cfg.beta,
                           count_updates=1, trace=1, **opts)
                 g.load(u, v, r)
