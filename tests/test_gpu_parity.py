@@ -156,15 +156,17 @@ def test_deterministic_executions_bitwise_equal(mfmod, storage, cfgname):
 
 @pytest.mark.parametrize("k", [2, 7, 32, 33, 64, 100, 128, 256])
 @pytest.mark.parametrize("storage", [0, 1])
-def test_deterministic_k_sweep_ragged(mfmod, k, storage):
-    """Generic (masked) and fast (vectorised) shapes; N not a multiple of 32 or 256."""
+@pytest.mark.parametrize("det_flow", [0, 1])
+def test_deterministic_k_sweep_ragged(mfmod, k, storage, det_flow):
+    """Generic (masked) and fast (vectorised) shapes; N not a multiple of 32 or 256; both executions (the
+    waves and the barrier-free dataflow, MF_OPT_DET_FLOW)."""
     m_, n_, N = 301, 97, 12_345
     u, v, r = datagen.planted_coo(21, m_, n_, 8, 0.1, N)
     order = oracle.shuffle_perm(5, N)
     ref = oracle.Model(m_, n_, k, ORC[storage], seed=13)
     ref.epoch(u, v, r, 0.02, 0.03, order)
     Pr, Qr = ref.factors_f32()
-    with mfmod.MF(m_, n_, k, 0.02, 0.03, 13, storage=storage, seed_shuffle=5) as g:
+    with mfmod.MF(m_, n_, k, 0.02, 0.03, 13, storage=storage, seed_shuffle=5, det_flow=det_flow) as g:
         g.load(u, v, r)
         g.epoch("deterministic")
         P, Q = g.factors()
