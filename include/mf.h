@@ -86,8 +86,9 @@ typedef enum {
                                  in steps (0 = auto: MF_SCHED_HOGWILD epochs 0, 1, 2 run off, 1 step, off and the
                                  prefetch is kept iff its epoch was > 3% faster; 15 = off); for CTA wavefront workers
                                  1 = bulk, 2 = per-line P-row prefetch per tile (0 = auto: kept unless > 3% slower).  20..21: CTA Q-group staging, 2 = thread
-                                 loop instead of bulk async copies.  22..23: CTA wavefront q_v read from shared memory, 1 = when p_u's
-                                 load is issued, else (default) once p_u has arrived.  24..25: deterministic execution, 0 = 1024-thread
+                                 loop instead of bulk async copies.  22: CTA wavefront q_v read from shared memory, 1 = when p_u's
+                                 load is issued, else (default) once p_u has arrived; 23: CTA wavefront, 1 = wait for the
+                                 Q group's copy-in before claiming tiles, else (default) at a thread's first rating.  24..25: deterministic execution, 0 = 1024-thread
                                  CTAs with 2 samples of a wave per group, 1 = 1 sample, 2 = 256-thread CTAs (identical
                                  results).  26..27: CTA in-block clamp, samples per concurrent group 0 -> 16, 1 -> 32,
                                  2 -> 64, 3 -> 8.  Only bits 26..27 change what is computed (how many of a block's

@@ -103,6 +103,7 @@ struct WfArgs {
     int min_per_group;    // CTA workers: in-block concurrency clamp, samples per concurrent group
     int tma;              // CTA workers: stage the Q group with bulk async copies (TMA engine) instead of a thread loop
     int q_late;           // CTA workers: read a rating's q_v from shared memory only once its p_u has arrived
+    int q_wait_late;      // CTA workers: wait for the Q group's copy-in at a thread's first rating of the block
     float eta, lam;
     int64_t n_cols;       // column groups are balanced segments [floor(g n / c), floor((g+1) n / c))
 };
@@ -490,8 +491,10 @@ __global__ void __launch_bounds__(THREADS, THREADS >= 1024 ? 1 : kCtaThreads / T
                 asm volatile("fence.proxy.async.global;" ::: "memory");  // acquired state -> async proxy
                 bulk_copy_in(qbase, qg, (uint32_t)(nrows * row_bytes), (uint32_t)__cvta_generic_to_shared(&s_bar));
             }
-            // every group has >= 1 row (c <= n), so block j completes the barrier's phase j
-            mbar_wait((uint32_t)__cvta_generic_to_shared(&s_bar), (uint32_t)pj & 1u);
+            // every group has >= 1 row (c <= n), so block j completes the barrier's phase j.  A thread waits
+            // for it just before its first rating of the block (the claim and the triple loads of its first
+            // tile overlap the copy), or after the block's tiles if it gets none (a.q_wait_late = 0: here)
+            if (!a.q_wait_late) mbar_wait((uint32_t)__cvta_generic_to_shared(&s_bar), (uint32_t)pj & 1u);
         } else {
             cta_copy_in(qs, qg, nrows * row_bytes);
             __syncthreads();
@@ -509,6 +512,7 @@ __global__ void __launch_bounds__(THREADS, THREADS >= 1024 ? 1 : kCtaThreads / T
         // many of the block's ratings.  Full-size shapes are not clamped (Netflix: 4,523 samples per
         // block for 128 groups; Yahoo: 2,184); 1% slices are (C3-1pct: 115 samples per block, where all
         // 128-256 groups at once left test RMSE +1.2..1.6% behind serial SGD at k = 32).
+        bool q_in = !a.tma || !a.q_wait_late;  // this thread has seen the Q group's copy-in complete
         for (;;) {
             int t = 0x3fffffff;  // warp w claims iff w * G * kCtaMinPerGroup < block size (w = 0 always)
             if (lane == 0 && ((threadIdx.x >> 5) == 0 || (int64_t)(threadIdx.x >> 5) * SH::G * a.min_per_group < hi - lo))
@@ -534,9 +538,14 @@ __global__ void __launch_bounds__(THREADS, THREADS >= 1024 ? 1 : kCtaThreads / T
                         asm volatile("prefetch.global.L2 [%0];" ::"l"(pp + off));
                 }
             }
+            if (!q_in) {
+                mbar_wait((uint32_t)__cvta_generic_to_shared(&s_bar), (uint32_t)pj & 1u);
+                q_in = true;
+            }
             if (cnt == 32) cta_tile<SH, D, true>(a, qbase, k, grp, sub, cnt, tu, tv, tr, chk);
             else cta_tile<SH, D, false>(a, qbase, k, grp, sub, cnt, tu, tv, tr, chk);
         }
+        if (!q_in) mbar_wait((uint32_t)__cvta_generic_to_shared(&s_bar), (uint32_t)pj & 1u);  // every phase, every thread
         if (a.tma) {
             // this thread's st.shared to the group must be visible to the async proxy that reads it
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -1010,9 +1019,12 @@ int mf_ctx::run_wavefront(const ShapeId &, const UpdateArgs &ua, int *launches, 
             const int sel = (variant_eff >> 26) & 0x3;
             a.min_per_group = sel == 0 ? (int)kCtaMinPerGroup : sel == 1 ? 32 : sel == 2 ? 64 : 8;
         }
-        // bits 22..23: 1 = read q_v from shared memory when p_u's load is issued (before r02ab), else once p_u
+        // bit 22: 1 = read q_v from shared memory when p_u's load is issued (before r02ab), else once p_u
         // has arrived (default: a shorter race window on the group's Q rows)
-        a.q_late = ((variant_eff >> 22) & 0x3) != 1;
+        a.q_late = ((variant_eff >> 22) & 0x1) == 0;
+        // bit 23: 1 = wait for the Q group's copy-in before claiming tiles (before r02ao), else at a thread's
+        // first rating of the block, so the tile claim and triple loads overlap the copy
+        a.q_wait_late = ((variant_eff >> 23) & 0x1) == 0;
         // bits 20..21: Q-group staging, 0 = bulk async copies when rows are 16-B multiples, 2 = thread loop
         a.tma = ((variant_eff >> 20) & 0x3) != 2 && row_bytes % 16 == 0 && ((uintptr_t)Q & 15) == 0;
         // (k = 32 / 64 keep the 16-byte-vector shapes: 4 / 8 lanes (16-bit rows), 8 / 16 lanes (fp32) --
