@@ -161,9 +161,9 @@ def _c3_gates(storage, gold):
             for t, g in enumerate(gold)]
 
 
-# fp32 only: the oracle's fp16 storage (software _Float16 conversions) needs about an hour per epoch at
-# this size; full-size fp16 parity is checked on the Netflix shape
-@pytest.mark.parametrize("storage", ["f32"])
+# fp16 golden: the oracle's -mf16c build (hardware half conversions) at ~7 min per epoch, written late in
+# round 2 (scripts/make_golden.py C3 f16 10 [42|43])
+@pytest.mark.parametrize("storage", ["f32", "f16"])
 @pytest.mark.parametrize("schedule", ["hogwild", "wavefront_cta"])
 def test_c3_rmse_trace_vs_oracle_golden(c3, storage, schedule):
     """Yahoo shape, both single-GPU schedules of configs[2], every epoch of the oracle's trace from the
