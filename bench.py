@@ -459,6 +459,7 @@ def main():
                                                   "variant", "frac_of_pattern_ceiling")}
 
     if not a.no_variants and a.config == "C2":
+        others.update(c5_leg(mf, stream, local, cfg, (du, dv, dr), (dtu, dtv, dtr)))
         others.update(c3_leg(mf, stream, local, a.storage))
     if not a.no_variants and not a.no_c4 and a.config != "C4":
         others.update(c4_leg(mf, stream, local, a.storage))
@@ -569,6 +570,32 @@ def c4_leg(mf, stream, local, storage, epochs=5):
     return shape_leg(mf, stream, local, storage, "C4",
                      (("hogwild", "hogwild", {}), ("wavefront_cta", "wavefront", {"wave_cta": 1}),
                       ("partitioned_1", "partitioned", {"partitions": 1})), epochs)
+
+
+def c5_leg(mf, stream, local, cfg, train, test, epochs=5):
+    """BASELINE.json configs[4]: the k sweep on the Netflix shape (the headline's own inputs, resident), batch-
+    Hogwild! in fp16 and fp32 storage, k = 32 / 64 / 256 (k = 128 is the headline and the `hogwild/f32`
+    line).  Kernel time = mean of the epochs after the prefetch trials (epochs 0-2); roofline per k against
+    the L2 ceiling (B_alg = 12 + 4kb) and, from the committed ncu bytes for that k, HBM."""
+    N = len(train[0])
+    out = {}
+    for storage in ("f16", "f32"):
+        for k in (32, 64, 256):
+            kc = cfg.scaled(k=k)
+            g = mf.MF(kc.m, kc.n, k, kc.alpha, kc.lam, kc.seed_init, storage=storage, beta=kc.beta,
+                      seed_shuffle=kc.seed_shuffle, device=local, stream=stream.cuda_stream)
+            g.load(*train)
+            ks = [g.epoch("hogwild").kernel_seconds for _ in range(epochs)]
+            rm = g.rmse(*test)
+            g.close()
+            k_s = statistics.mean(ks[3:])
+            rf = roofline(kc, storage, N, k_s, load_traffic(storage, f"C2-k{k}"), "hogwild")
+            out[f"C5:k{k}/{storage}"] = {"value": N / k_s, "kernel_s": k_s, "rmse_after_%d_epochs" % epochs: rm,
+                                         "roofline_bound": rf["bound"], "roofline_frac": rf["frac"],
+                                         "l2_frac": (rf["l2"] or {}).get("frac"),
+                                         "hbm_frac": (rf["hbm"] or {}).get("frac")}
+    out["C5:note"] = "k sweep on the Netflix shape (configs[4]); k = 128 is the headline / hogwild/f32 lines"
+    return out
 
 
 def c3_leg(mf, stream, local, storage, epochs=5):

@@ -73,9 +73,10 @@ CASES = [("hogwild", {}, 2), ("partitioned", {"partitions": 2}, 4), ("partitione
          ("partitioned", {"partitions": 8}, 4), ("wavefront", {"wave_cta": 1}, 10),
          pytest.param("wavefront", {}, 10, marks=pytest.mark.xfail(
              strict=False, reason="paper-literal wavefront (warp workers, serial ~40-sample blocks) under power-law "
-                                  "degrees: +0.9% vs the oracle after 10 epochs (its trace swings between +0.06% and "
-                                  "+1.3% over epochs 7-10); the paper notes wavefront converges slower (PAPER.md:256); "
-                                  "DESIGN.md 8.1, profiles/r02ah_zipf10_*"))]
+                                  "degrees: intermittent -- +0.9% (fp32) / -0.63% (fp16) vs the oracle after 10 epochs "
+                                  "in one trace run (its trace swings between +0.06% and +1.3% over epochs 7-10), "
+                                  "within the gate in the three full-suite runs r02ai / r02an / r02au; the paper notes "
+                                  "wavefront converges slower (PAPER.md:256); DESIGN.md 8.1, profiles/r02ah_zipf10_*"))]
 
 
 @pytest.mark.parametrize("storage", ["f32", "f16"])
