@@ -590,10 +590,17 @@ def c5_leg(mf, stream, local, cfg, train, test, epochs=5):
             g.close()
             k_s = statistics.mean(ks[3:])
             rf = roofline(kc, storage, N, k_s, load_traffic(storage, f"C2-k{k}"), "hogwild")
-            out[f"C5:k{k}/{storage}"] = {"value": N / k_s, "kernel_s": k_s, "rmse_after_%d_epochs" % epochs: rm,
-                                         "roofline_bound": rf["bound"], "roofline_frac": rf["frac"],
-                                         "l2_frac": (rf["l2"] or {}).get("frac"),
-                                         "hbm_frac": (rf["hbm"] or {}).get("frac")}
+            row = {"value": N / k_s, "kernel_s": k_s, "rmse_after_%d_epochs" % epochs: rm,
+                   "roofline_bound": rf["bound"], "roofline_frac": rf["frac"],
+                   "l2_frac": (rf["l2"] or {}).get("frac"), "hbm_frac": (rf["hbm"] or {}).get("frac"),
+                   "alg_GBps": b_alg(k, storage) * N / k_s / 1e9}
+            if rf["l2"] is None:
+                # rows under 256 B: no L2 ceiling measured for that row size; neither memory level binds
+                # (P fits L2 at k = 32 fp16, DRAM carries the triples) -- the A-10 worker clamp does
+                # (9.5k ratings in flight x the update's latency)
+                row["roofline_bound"] = "latency (A-10 worker clamp; no L2 ceiling measured for %d-B rows)" % (
+                    k * (4 if storage == "f32" else 2))
+            out[f"C5:k{k}/{storage}"] = row
     out["C5:note"] = "k sweep on the Netflix shape (configs[4]); k = 128 is the headline / hogwild/f32 lines"
     return out
 
