@@ -80,7 +80,9 @@ typedef enum {
     MF_OPT_EPOCH = 11,        /* set the epoch index t used by the LR schedule */
     MF_OPT_PARTITIONS = 12,   /* MF_SCHED_PARTITIONED without NCCL: G logical partitions run on this GPU (loopback) */
     MF_OPT_SEED_SHUFFLE = 13, /* seed of the A-8 shuffle (default: the mf_create seed) */
-    MF_OPT_VARIANT = 14,      /* kernel variant selector for tuning (0 = default).  Bit fields: 0..3 group shape; 4..7
+    MF_OPT_VARIANT = 14,      /* kernel variant selector for tuning (0 = default).  Bit fields: 0..3 group shape (0 = auto:
+                                 for batch-Hogwild! at k = 128 in 16-bit storage, 8 lanes per rating where P exceeds
+                                 twice the L2 and Q is under a quarter of it, else 32); 4..7
                                  ratings in flight per batch-Hogwild! group (0 = auto: 2 for fp32 rows of k >= 128,
                                  else 1); 8..15 wavefront-CTA shape; 16..19 batch-Hogwild! L2 row prefetch distance
                                  in steps (0 = auto: MF_SCHED_HOGWILD epochs 0, 1, 2 run off, 1 step, off and the

@@ -613,6 +613,24 @@ float mf_ctx::eta_at(int32_t t) const {
     return (float)((double)alpha / (1.0 + beta * std::pow((double)t, 1.5)));
 }
 
+// batch-Hogwild!'s group shape (MF_OPT_VARIANT bits 0..3; 0 = auto).  16-bit rows at k = 128 take one rating
+// per warp (32 lanes x 8 B) by default; where P is far larger than the L2 (> 2x) and Q small (< 1/4 of it), the
+// update waits on DRAM for p_u and more ratings in flight pay: the 8-lane shape (4 ratings per warp, 14,208 in
+// flight at full residency) is 3-4% faster on the Hugewiki shapes (full, rows/10, the partitioned kernels)
+// and is taken there; not on the Yahoo shape, whose Q misses L2 too (profiles/r02ap_*, r02aq_*).
+int mf_ctx::hog_shape_sel() const {
+    if (variant & 0xF) return variant & 0xF;
+    if (k != 128 || storage == kF32) return 0;
+    static const int64_t l2 = [] {
+        int dev = 0, v = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&v, cudaDevAttrL2CacheSize, dev);
+        return (int64_t)v;
+    }();
+    const int64_t row = (int64_t)k * storage_bytes();
+    return (l2 > 0 && p_rows() * row > 2 * l2 && n * row < l2 / 4) ? 1 : 0;
+}
+
 int mf_ctx::auto_workers() const {
     // DESIGN.md A-10: every worker processes >= 10^4 samples per epoch
     return (int)std::max<int64_t>(1, std::min<int64_t>(N / 10000, 1 << 30));
@@ -703,7 +721,7 @@ static int epoch_local(mf_ctx *ctx, int schedule, mf_epoch_stats *stats) {
     ctx->seg_valid = false;
     cudaStream_t st = ctx->stream();
     const float eta = ctx->eta_at(ctx->epoch);
-    const ShapeId sh = schedule == MF_SCHED_HOGWILD ? hogwild_shape(ctx->k, ctx->storage, ctx->variant & 0xF)
+    const ShapeId sh = schedule == MF_SCHED_HOGWILD ? hogwild_shape(ctx->k, ctx->storage, ctx->hog_shape_sel())
                                                     : select_shape(ctx->k, ctx->storage, ctx->variant & 0xF);
     CK(cudaEventRecord(ctx->events[0], st));
     CK(cudaMemsetAsync(ctx->scratch, 0, sizeof(DevScratch), st));

@@ -184,6 +184,7 @@ struct mf_ctx {
     bool is_distributed() const { return nccl != nullptr; }
     float eta_at(int32_t t) const;
     int auto_workers() const;
+    int hog_shape_sel() const;  // batch-Hogwild! group shape: MF_OPT_VARIANT bits 0..3, or the auto rule
     mf::UpdateArgs update_args(float eta) const;
     int finish_epoch(int schedule, float eta, int launches, int workers_used, mf_epoch_stats *stats);
     int build_waves();

@@ -134,7 +134,7 @@ extern "C" int mf_epoch_host_blocks(mf_ctx *ctx, const int32_t *u, const int32_t
     cudaStream_t st = ctx->stream(), cs = ctx->copy_stream, ds = ctx->d2h_stream;
     const cudaMemcpyKind kind = cudaMemcpyDefault;  // ratings and P may be host (pinned or pageable) or device
     const float eta = ctx->eta_at(ctx->epoch);
-    const ShapeId sh = hogwild_shape(ctx->k, ctx->storage, ctx->variant & 0xF);
+    const ShapeId sh = hogwild_shape(ctx->k, ctx->storage, ctx->hog_shape_sel());
     CK(cudaEventRecord(ctx->events[0], st));
     CK(cudaMemsetAsync(ctx->scratch, 0, sizeof(DevScratch), st));
     CK(cudaEventRecord(ctx->events[1], st));

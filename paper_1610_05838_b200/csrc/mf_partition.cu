@@ -475,7 +475,7 @@ int mf_ctx::epoch_partitioned(mf_epoch_stats *stats) {
     cudaStream_t st = stream();
     const int S = part_S, L = part_local;
     const float eta = eta_at(epoch);
-    const ShapeId sh = hogwild_shape(k, storage, variant & 0xF);
+    const ShapeId sh = hogwild_shape(k, storage, hog_shape_sel());
     auto blk = [&](int s, int li, int c, int h) { return ((((size_t)s * L + li) * G + c) << 1) | (size_t)h; };
     std::vector<int64_t> n_local(L, 0);  // samples of each hosted partition per epoch (worker clamp, A-10)
     for (int s = 0; s < S; s++)
@@ -701,7 +701,7 @@ int mf_ctx::epoch_units(mf_epoch_stats *stats) {
     cudaStream_t st = stream();
     const int S = part_S, L = part_local;
     const float eta = eta_at(epoch);
-    const ShapeId sh = hogwild_shape(k, storage, variant & 0xF);
+    const ShapeId sh = hogwild_shape(k, storage, hog_shape_sel());
     auto blk = [&](int s, int li, int c, int h) { return ((((size_t)s * L + li) * G + c) << 1) | (size_t)h; };
     std::vector<int64_t> n_local(L, 0);  // samples of each hosted partition per epoch (worker clamp, A-10)
     for (int s = 0; s < S; s++)

@@ -71,7 +71,7 @@ extern "C" int mf_epoch_host(mf_ctx *ctx, int schedule, const int32_t *u, const 
     cudaGetLastError();
     const cudaMemcpyKind kind = dev_src ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
     const float eta = ctx->eta_at(ctx->epoch);
-    const ShapeId sh = hogwild_shape(ctx->k, ctx->storage, ctx->variant & 0xF);
+    const ShapeId sh = hogwild_shape(ctx->k, ctx->storage, ctx->hog_shape_sel());
     const int workers = ctx->workers > 0 ? ctx->workers
                                          : (int)std::max<int64_t>(1, std::min<int64_t>(nnz / 10000, 1 << 30));
     CK(cudaEventRecord(ctx->events[0], st));
