@@ -594,7 +594,7 @@ def c5_leg(mf, stream, local, cfg, train, test, epochs=5):
                    "roofline_bound": rf["bound"], "roofline_frac": rf["frac"],
                    "l2_frac": (rf["l2"] or {}).get("frac"), "hbm_frac": (rf["hbm"] or {}).get("frac"),
                    "alg_GBps": b_alg(k, storage) * N / k_s / 1e9}
-            if rf["l2"] is None:
+            if rf["l2"] is None and k * (4 if storage == "f32" else 2) < 256:
                 # rows under 256 B: no L2 ceiling measured for that row size; neither memory level binds
                 # (P fits L2 at k = 32 fp16, DRAM carries the triples) -- the A-10 worker clamp does
                 # (9.5k ratings in flight x the update's latency)
