@@ -514,7 +514,7 @@ def main():
         "e2e": {"value": N / (e2e_ms * 1e-3), "unit": "updates/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": 8, "ms_per_step": e2e_ms, "wall_ms_per_step": wall_ms,
                 "includes": ("mf_epoch_host: every step streams R (12 B/sample) from pinned host memory in "
-                             "2^23-sample chunks, device validation per chunk, batch-Hogwild! overlapped with "
+                             "2^22-sample chunks, device validation per chunk, batch-Hogwild! overlapped with "
                              "the copies; then mf_rmse with the test set copied from pinned host, result D2H"
                              if streamed else
                              "mf_load_coo (H2D of R from pinned host, validation, A-8 shuffle), mf_epoch, "

@@ -100,7 +100,7 @@ typedef enum {
     MF_OPT_WAVE_CTA = 17,     /* wavefront worker: 0 = one warp, block processed serially; 1 = one 1024-thread CTA
                                  per SM with the column group's Q rows staged in shared memory, lock-free inside the block;
                                  2 = as 1 with two 512-thread CTA workers per SM */
-    MF_OPT_STREAM_CHUNK = 18, /* mf_epoch_host: samples per streamed chunk (default 2^23) */
+    MF_OPT_STREAM_CHUNK = 18, /* mf_epoch_host: samples per streamed chunk (default 2^22) */
     MF_OPT_PART_SPLIT = 19,   /* partitioned: 2 = unit grid (default): 2G column units (segment halves), each family of
                                  halves rotating by its own Latin square (a randomized G x 2G Latin rectangle per pass,
                                  P:525-535), the two units of a partition updated concurrently on two streams with half

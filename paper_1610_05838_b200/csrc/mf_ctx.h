@@ -149,7 +149,7 @@ struct mf_ctx {
 
     // streamed epochs from caller memory (mf_stream.cu)
     static constexpr int kStreamBufs = 3;
-    int64_t stream_chunk = 1 << 23;  // samples per chunk (MF_OPT_STREAM_CHUNK)
+    int64_t stream_chunk = 1 << 22;  // samples per chunk (MF_OPT_STREAM_CHUNK; 2^21..2^23 within 1%, 2^25 -8%: r02bb)
     cudaStream_t copy_stream = nullptr;
     int32_t *sb_u[kStreamBufs] = {}, *sb_v[kStreamBufs] = {};
     float *sb_r[kStreamBufs] = {};
