@@ -768,7 +768,18 @@ static int epoch_local(mf_ctx *ctx, int schedule, mf_epoch_stats *stats) {
             // MF_OPT_VARIANT bits 24..25 select the dataflow form (mf_flow.cu launch_flow)
             CK(launch_flow(flow_shape(ctx->k, ctx->storage), a, st, &used, wsel));
         } else {
-            CK(launch_waves(sh, a, st, &l, wsel == 3 ? 3 : wsel == 2 ? 0 : wsel == 1 ? 1 : 2));
+            // auto (bits 0..3 and 24..25 both 0): large waves (>= 64k samples on average: the Yahoo shape's
+            // 183k) run the 8 / 16-lane shape with one sample per group and step -- Yahoo f16 51.8 -> 45.5 ms
+            // per epoch, fp32 105 -> 91 -- small ones keep the 2-sample form (the Netflix shape's 11.6k-sample
+            // waves: 31 vs 55 ms; profiles/r02bd_*, r02be_*).  Exact either way; the shapes round the dot
+            // differently.
+            ShapeId wsh = sh;
+            int form = wsel == 3 ? 3 : wsel == 2 ? 0 : wsel == 1 ? 1 : 2;
+            if ((ctx->variant & 0xF) == 0 && wsel == 0 && ctx->nwaves > 0 && ctx->N / ctx->nwaves >= 65536) {
+                wsh = select_shape(ctx->k, ctx->storage, 1);
+                form = 1;
+            }
+            CK(launch_waves(wsh, a, st, &l, form));
             used = 0;
         }
     } else {  // wavefront

@@ -164,7 +164,7 @@ def _c3_gates(storage, gold):
 # fp16 golden: the oracle's -mf16c build (hardware half conversions) at ~7 min per epoch, written late in
 # round 2 (scripts/make_golden.py C3 f16 10 [42|43])
 @pytest.mark.parametrize("storage", ["f32", "f16"])
-@pytest.mark.parametrize("schedule", ["hogwild", "wavefront_cta"])
+@pytest.mark.parametrize("schedule", ["hogwild", "wavefront_cta", "deterministic"])
 def test_c3_rmse_trace_vs_oracle_golden(c3, storage, schedule):
     """Yahoo shape, both single-GPU schedules of configs[2], every epoch of the oracle's trace from the
     second on within the gate (0.5%, or the oracle's own shuffle-seed spread where larger).  The first
@@ -178,12 +178,17 @@ def test_c3_rmse_trace_vs_oracle_golden(c3, storage, schedule):
     gold = json.load(open(path))["rmse"]
     cfg, ((u, v, r), test) = c3
     opts = {"wave_cta": 1} if schedule == "wavefront_cta" else {}
+    sched = "wavefront" if opts else schedule
     with _ctx(cfg, storage, count_updates=1, **opts) as g:
         g.load(u, v, r)
         got = []
         for _ in range(len(gold)):
-            assert g.epoch("wavefront" if opts else "hogwild").updates == len(u)
+            assert g.epoch(sched).updates == len(u)
             got.append(g.rmse(*test))
+    if schedule == "deterministic":  # exact serial SGD (its large-wave execution, 5.3): every epoch at 0.05%
+        bad = [(t, a, b) for t, (a, b) in enumerate(zip(got, gold)) if abs(a - b) > 0.0005 * b]
+        assert not bad, bad
+        return
     gate = _c3_gates(storage, gold)
     bad = [(t, a, b, gt) for t, (a, b, gt) in enumerate(zip(got, gold, gate)) if t >= 1 and abs(a - b) > gt]
     assert not bad, bad
