@@ -164,8 +164,9 @@ int mf_get_option(const mf_ctx *ctx, int key, double *value);
  * sample), replacing any previous one.  u, v, r are nnz-element arrays in host or device memory
  * (detected), COPIED; the caller keeps ownership.  On the device: validate 0 <= u < m, 0 <= v < n and finite
  * r (MF_EINVAL on failure, nothing loaded: SPEC.md:62), then permute once by the A-8 hash order ("we shuffle
- * samples"; MF_OPT_SHUFFLE) and store as three SoA arrays.  Allocates and initialises P, Q
- * (A-7) on first use.  nnz >= 1 (MF_EINVAL); MF_ENOMEM / MF_ECUDA on device failures. */
+ * samples"; MF_OPT_SHUFFLE) and store as three SoA arrays; the column-degree moment
+ * sum_v (deg v / N)^2 is computed once here for the Q write-back rule (MF_OPT_Q_UPDATE).  Allocates and
+ * initialises P, Q (A-7) on first use.  nnz >= 1 (MF_EINVAL); MF_ENOMEM / MF_ECUDA on device failures. */
 int mf_load_coo(mf_ctx *ctx, const int32_t *u, const int32_t *v, const float *r, int64_t nnz);
 
 /* Run one epoch -- every loaded rating updated once by the rule of PAPER.md:124-126 (§2.2: err = r - p.q,
